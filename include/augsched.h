@@ -1,0 +1,242 @@
+/*
+ * augsched.h — C ABI of libaugsched, a B200-native (sm_100a) implementation of
+ * the per-iteration scheduling pass of AugServe (arXiv 2512.04013).
+ *
+ * Citations: "P:n" is line n of the paper's text; "Eq.k" follows the
+ * order of \begin{equation} there (Eq.4 = P:479 ... Eq.32 = P:741); "Rk" is a
+ * reading fixed in DESIGN.md where the paper is silent.
+ *
+ * What one scheduling step computes (Algorithm 1), per instance:
+ *   1. Stage I on arrivals: policy argmin of Eq.4-8, value V1 of Eq.9-15.
+ *   2. Stage II on returned calls: V2 of Eq.16-22 and V_final of Eq.23-25;
+ *      route Preserve->running, Swap->swapped, Discard->waiting.
+ *   3. Token limit: Eq.27-32 on the KV ledger, clamped to
+ *      [floor(beta_low*target_max), floor(beta_high*target_max)].
+ *   4. Score: key = orderable_u32(fp32(V - alpha*(now-last)*T)) (Eq.26, R1, R3).
+ *   5. Order: running => swapped => waiting, each ascending by key, ties by
+ *      request id (R2, R16).
+ *   6. Admit the prefix whose preceding demand is below the limit, with a
+ *      partial last chunk (P:1225-1229 + chunked prefill P:1102, R17).
+ *   7. Rare memory resolution: demote Preserve-paused KV, then evict from the
+ *      tail of the order (R20).
+ * augsched_simulate additionally runs the engine model (R21-R24) and the
+ * metrics to completion.
+ *
+ * Conventions
+ *   - Every call returns an int status: AUGSCHED_OK (0) or a negative code; no
+ *     C++ exception crosses the ABI; augsched_last_error() gives a
+ *     thread-local message for the last non-zero status.
+ *   - Time is integer: iterations (uint64) and microsecond ticks (uint64).
+ *     Token counts are integers; values/scores are IEEE binary64 computed
+ *     without FMA contraction, converted once to fp32 for the key (R3).
+ *   - A handle owns every device buffer it allocates and issues all work on the
+ *     CUDA stream given at creation (a cudaStream_t, e.g. a torch stream's
+ *     pointer; NULL = legacy default stream).  Calls are asynchronous with
+ *     respect to the host unless documented otherwise.  A handle may move
+ *     between threads but must not be used by two threads at once.
+ *   - Device-side faults (a state violation seen by a kernel) are latched in a
+ *     device error word and returned by the next call that synchronizes
+ *     (augsched_sync, augsched_simulate with AUGSCHED_HOST_RESULTS) as
+ *     AUGSCHED_E_STATE.
+ */
+#ifndef AUGSCHED_H_
+#define AUGSCHED_H_
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define AUGSCHED_API __attribute__((visibility("default")))
+#else
+#define AUGSCHED_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes -------------------------------------------------------- */
+#define AUGSCHED_OK 0
+#define AUGSCHED_E_INVALID (-1)       /* bad argument or configuration */
+#define AUGSCHED_E_CAPACITY (-2)      /* a queue/slot/trace exceeds the handle's capacity */
+#define AUGSCHED_E_CUDA (-3)          /* a CUDA runtime error (message has the name) */
+#define AUGSCHED_E_STATE (-4)         /* a record violates the request state machine */
+#define AUGSCHED_E_OOM (-5)           /* device allocation failed */
+#define AUGSCHED_E_UNIMPLEMENTED (-6)
+
+/* ---- policies and ranking/budget modes ----------------------- */
+#define AUGSCHED_PRESERVE 0
+#define AUGSCHED_SWAP 1
+#define AUGSCHED_DISCARD 2
+
+#define AUGSCHED_RANK_AUGSERVE 0      /* value order of Eq.26 */
+#define AUGSCHED_RANK_FCFS 1          /* key = 0: order (tier, id) (R33) */
+#define AUGSCHED_BUDGET_DYNAMIC 0     /* Eq.27-32 + clamp */
+#define AUGSCHED_BUDGET_STATIC 1      /* fixed l_static tokens */
+#define AUGSCHED_POLICY_ARGMIN 0      /* Eq.7-8 */
+#define AUGSCHED_POLICY_PRESERVE 1    /* forced policy (baseline emulation) */
+#define AUGSCHED_POLICY_SWAP 2
+#define AUGSCHED_POLICY_DISCARD 3
+
+/* Per-instance sweep parameters (one serving instance = one queue set). */
+typedef struct augsched_instance_params {
+  uint32_t target_max;       /* target_max of P:749; also N^fwd_max in Eq.6/9/17/18 (R9); >= 1 */
+  uint32_t l_static;         /* static token limit when budget_mode == STATIC */
+  double alpha;              /* anti-starvation coefficient of Eq.26, value units per second; >= 0 */
+  uint64_t slo_ttft_ticks;   /* TTFT SLO in µs (1 s) */
+  uint32_t slo_norm_num;     /* normalized-latency SLO = num/den x T^fwd (10/1) */
+  uint32_t slo_norm_den;
+  uint32_t ranking;          /* AUGSCHED_RANK_* */
+  uint32_t budget_mode;      /* AUGSCHED_BUDGET_* */
+  uint32_t policy_mode;      /* AUGSCHED_POLICY_* */
+  uint32_t reserved;         /* must be 0 */
+} augsched_instance_params;
+
+/* System constants (SPEC SimConfig). */
+typedef struct augsched_config {
+  uint64_t m_per_token;      /* M: KV bytes per token; >= 1 */
+  uint64_t g_total;          /* G_total bytes (Eq.30) */
+  uint64_t g_model, g_runtime, g_safety;  /* G_fixed = sum (Eq.29); G_fixed < G_total */
+  uint64_t t_fwd_ticks;      /* T^fwd in µs; >= 1 */
+  uint32_t s_in, s_out;      /* S^fwd_in / S^fwd_out tokens per iteration; >= 1 */
+  uint32_t gamma_num, gamma_den;  /* gamma of Eq.31 = num/den in [0, 1]; den >= 1 */
+  double beta_low, beta_high;     /* clamp factors, 0 <= beta_low <= beta_high */
+  augsched_instance_params defaults;  /* used when create() gets per_inst == NULL */
+} augsched_config;
+
+/* ---- simulation inputs (all arrays in one memory space, see flags) --------
+ * CSR trace set: trace k owns requests [req_off[k], req_off[k+1]) in arrival
+ * order; request r owns segments [seg_off[r], seg_off[r] + n_seg[r]).  A
+ * segment is a decode phase of gen_true tokens followed (except the last) by
+ * a tool call of dur_true µs that returns ret_len tokens.
+ * gen_pred / dur_pred are the predictor's outputs.  Arrival
+ * ticks must be nondecreasing within a trace; gen_true >= 1 (R29).           */
+typedef struct augsched_trace {
+  const uint32_t* req_off;   /* [n_traces + 1] */
+  const uint64_t* arr_tick;  /* [n_req] arrival time, µs */
+  const uint32_t* l_pre;     /* [n_req] prompt tokens L^pre (>= 1) */
+  const uint32_t* seg_off;   /* [n_req] */
+  const uint32_t* n_seg;     /* [n_req] >= 1 */
+  const uint32_t* gen_true;  /* [n_seg_total] */
+  const uint32_t* gen_pred;  /* [n_seg_total] predicted L^out */
+  const uint32_t* dur_true;  /* [n_seg_total] call duration µs (ignored for last segment) */
+  const float* dur_pred;     /* [n_seg_total] predicted T^api, seconds */
+  const uint32_t* ret_len;   /* [n_seg_total] returned tokens R (ignored for last) */
+  uint32_t n_traces;
+  uint32_t n_req;            /* total requests (length of per-request arrays) */
+  uint32_t n_seg_total;      /* total segments */
+  uint32_t reserved;
+} augsched_trace;
+
+/* Per-instance result record of augsched_simulate (fixed size, byte-comparable). */
+enum {
+  AUGSCHED_R_NREQ = 0, AUGSCHED_R_ARRIVED, AUGSCHED_R_COMPLETED, AUGSCHED_R_SLO_OK,
+  AUGSCHED_R_SLO_OK_5X, AUGSCHED_R_BUSY_STEPS, AUGSCHED_R_DECISIONS, AUGSCHED_R_EVICTIONS,
+  AUGSCHED_R_DEMOTIONS, AUGSCHED_R_CALLS_PRESERVE, AUGSCHED_R_CALLS_SWAP,
+  AUGSCHED_R_CALLS_DISCARD, AUGSCHED_R_RETURNS, AUGSCHED_R_TOKENS, AUGSCHED_R_FINAL_T,
+  AUGSCHED_R_MAKESPAN, AUGSCHED_R_SUM_TTFT, AUGSCHED_R_SUM_E2E, AUGSCHED_R_SUM_GEN,
+  AUGSCHED_R_ADMITTED, AUGSCHED_R_ERR, AUGSCHED_R_MAXQ, AUGSCHED_R_RSV22, AUGSCHED_R_RSV23,
+  AUGSCHED_R_NFIELD
+};
+#define AUGSCHED_NBIN 160   /* integer log-linear bins: v<16 -> v; else 16+4(e-4)+2 mantissa bits */
+typedef struct augsched_result {
+  uint64_t f[AUGSCHED_R_NFIELD];
+  uint32_t hist_ttft[AUGSCHED_NBIN];   /* TTFT in µs */
+  uint32_t hist_norm[AUGSCHED_NBIN];   /* floor(e2e µs / generated tokens) */
+} augsched_result;
+
+/* simulate flags */
+#define AUGSCHED_HOST_TRACES 1u   /* traces + inst_trace_id are host pointers: copied in (timed) */
+#define AUGSCHED_HOST_RESULTS 2u  /* results is a host pointer: copied out, call synchronizes */
+#define AUGSCHED_RESUME 4u        /* continue from the handle's state instead of t = 0 */
+
+/* ---- step mode (the scheduler as a library) ------------------------------
+ * Record kinds enqueued between steps; processed at the start of the next
+ * augsched_step in the order CALL/FINISH (engine events of the last forward),
+ * snapshot, RETURN (Stage II), NEW/IMPORT (Stage I / restore).             */
+#define AUGSCHED_K_NEW 1      /* id empty -> waiting; la = l_pre, lb = gen_pred, ta = dur_pred, flags bit0 = has call */
+#define AUGSCHED_K_RETURN 2   /* id paused -> routed; la = returned tokens R, lb = next gen_pred, ta = next dur_pred, bit0 = next call */
+#define AUGSCHED_K_CALL 3     /* id running & decode-ready -> paused with S~ (R13); ta = dur_pred of the call */
+#define AUGSCHED_K_FINISH 4   /* id active -> empty, KV released */
+#define AUGSCHED_K_IMPORT 5   /* id empty -> given state: flags bits4-6 status (1 run,2 swap,3 wait,4 paused),
+                                 bits 8-9 applied policy, bit 12 stage II; la/lb/lc/ta value features
+                                 (stage I: L, O, -, A; stage II: Lt, R, O', A'); last/ctx/kv/cpu/pend token state */
+typedef struct augsched_record_soa {
+  const uint32_t* kind;
+  const uint32_t* id;      /* slot index < max_active_per_instance */
+  const uint32_t* la;
+  const uint32_t* lb;
+  const uint32_t* lc;
+  const float* ta;
+  const uint32_t* flags;
+  const uint32_t* last;
+  const uint32_t* ctx;
+  const uint32_t* kv;
+  const uint32_t* cpu;
+  const uint32_t* pend;
+} augsched_record_soa;
+
+/* Outputs of one step: device pointers owned by the handle, valid until the
+ * next call on it.  Per instance i the queue segment is
+ * [i*max_active, i*max_active + n_active[i]) of order/grant/key.          */
+typedef struct augsched_step_out {
+  const int64_t* budget;     /* [n_instances] token limit N_max of this step */
+  const uint32_t* n_active;  /* [n_instances] |running u swapped u waiting| */
+  const uint32_t* admitted;  /* [n_instances] entries granted > 0 */
+  const uint32_t* order;     /* slot ids in scheduling order */
+  const uint32_t* grant;     /* tokens granted to order[j] this step */
+  const uint32_t* key;       /* orderable u32 of the fp32 score of order[j] */
+} augsched_step_out;
+
+typedef struct augsched_handle augsched_t;
+
+/* Create a handle for n_instances independent instances with room for
+ * max_active_per_instance requests each (simulate: >= the longest trace and
+ * <= 65535; step: slots per instance).  per_inst: host array of n_instances
+ * params or NULL (cfg->defaults for all).  Validates S:43-45: quantities > 0,
+ * 0 <= gamma <= 1, beta_low <= beta_high, G_fixed < G_total, alpha >= 0.
+ * device: CUDA ordinal; cuda_stream: cudaStream_t (borrowed, not owned).
+ * Returns OK, E_INVALID, E_OOM or E_CUDA. */
+AUGSCHED_API int augsched_create(const augsched_config* cfg, const augsched_instance_params* per_inst,
+                    uint32_t n_instances, uint32_t max_active_per_instance, int device,
+                    void* cuda_stream, augsched_t** out);
+
+/* Queue n records for `instance` (step mode).  recs_on_device = 0: host
+ * arrays, copied before return; 1: device arrays that must stay valid until
+ * the handle's stream passes this call.  Host-side capacity check:
+ * E_CAPACITY if the pending queue would exceed max_active_per_instance * 4
+ * records; E_INVALID for a bad kind/id.  State violations are detected on
+ * the device and reported as E_STATE by a later synchronizing call. */
+AUGSCHED_API int augsched_enqueue(augsched_t* h, uint32_t instance, const augsched_record_soa* recs, uint32_t n,
+                     int recs_on_device);
+
+/* One scheduling step at iteration now_iter for every instance (steps 1-7
+ * above, then last = now for granted requests and the granted batch's token
+ * accounting: swap-in, recompute, prefill/assimilate, decode).  Fills `out`
+ * with device pointers.  Asynchronous. */
+AUGSCHED_API int augsched_step(augsched_t* h, uint64_t now_iter, augsched_step_out* out);
+
+/* Run every instance's simulation (Algorithm 1 + engine model + metrics) until
+ * all its requests finished or its iteration counter reaches max_iters.
+ * inst_trace_id[i] selects instance i's trace.  results: n_instances records.
+ * flags: AUGSCHED_HOST_TRACES / AUGSCHED_HOST_RESULTS / AUGSCHED_RESUME.
+ * Without HOST_RESULTS the call is asynchronous and results must be a
+ * device buffer.  E_CAPACITY if a trace is longer than the handle allows. */
+AUGSCHED_API int augsched_simulate(augsched_t* h, const augsched_trace* traces, const uint32_t* inst_trace_id,
+                      uint64_t max_iters, augsched_result* results, uint32_t flags);
+
+/* Wait for the handle's stream; returns a latched device error (E_STATE) if any. */
+AUGSCHED_API int augsched_sync(augsched_t* h);
+
+/* Number of kernel launches issued by this handle since creation. */
+AUGSCHED_API uint64_t augsched_launch_count(const augsched_t* h);
+
+/* Synchronize and free everything.  Safe on NULL. */
+AUGSCHED_API void augsched_destroy(augsched_t* h);
+
+/* Thread-local message for the last non-zero status ("" if none). */
+AUGSCHED_API const char* augsched_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* AUGSCHED_H_ */

@@ -1,0 +1,635 @@
+// augsched_simulate: persistent per-instance simulation kernel for sm_100a.
+// See sim.cuh for the design; the per-step sequence follows DESIGN.md §"Step
+// sequence" (S1..S12), i.e. Algorithm 1 plus the engine model.
+#include <cuda_runtime.h>
+#include "sim.cuh"
+
+namespace augsched {
+
+struct __align__(16) SimShm {
+  unsigned long long wbin[2][256];   // double-buffered select histograms
+  unsigned int cbin[2][256];
+  unsigned int hist_t[AUGSCHED_NBIN];
+  unsigned int hist_n[AUGSCHED_NBIN];
+  unsigned long long cnt[AUGSCHED_R_NFIELD];
+  unsigned int holes[HOLE_CAP];
+  unsigned int wtot[SIM_NW + 1];
+  // instance scalars
+  unsigned long long t, tT, min_ret, next_tick;
+  long long A, P, A_snap, B, need, freev;
+  unsigned long long freed;
+  unsigned int next_arr, n_act, n_pz, n_fin, n_holes, n_pholes, wpos;
+  unsigned int inst, n_req, r0;
+  int run, idle;
+  // selection state
+  unsigned long long sel_prefix, sel_mask, sel_wbelow, sel_k, sel_total;
+  unsigned int sel_cnt;
+  int sel_found, sel_done;
+};
+
+namespace {
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr uint32_t INVALID = 0xffffffffu;
+
+__device__ __forceinline__ void err_set(const SimParams& p, uint32_t bits) { atomicOr(p.err, bits); }
+
+// Block-wide exclusive scan of a 0/1 flag; returns this thread's prefix and
+// (in s.wtot[SIM_NW]) the block total.  Contains two __syncthreads.
+__device__ __forceinline__ uint32_t block_flag_scan(SimShm& s, bool f) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned b = __ballot_sync(FULL, f);
+  if (lane == 0) s.wtot[warp] = __popc(b);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t acc = 0;
+    for (int w = 0; w < SIM_NW; ++w) { uint32_t x = s.wtot[w]; s.wtot[w] = acc; acc += x; }
+    s.wtot[SIM_NW] = acc;
+  }
+  __syncthreads();
+  return s.wtot[warp] + __popc(b & ((1u << lane) - 1));
+}
+
+// Weighted MSD radix select.  Among items i < n for which get(i, key, w)
+// returns true (w >= 1, keys unique, key < 2^nbits) find the smallest key k*
+// with sum_{key <= k*} w >= D.  Results: s.sel_found (1 found / 0 not: then
+// s.sel_total holds the full weight), s.sel_k, s.sel_wbelow = sum_{key < k*} w.
+// Weights are clamped to D (exact: every item before k* has w < D).
+template <class Get>
+__device__ void wselect(SimShm& s, uint32_t n, uint64_t D, int nbits, Get get) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t Dc = (uint32_t)(D < (1ull << 26) ? D : (1ull << 26));
+  __syncthreads();
+  if (tid == 0) {
+    s.sel_prefix = 0; s.sel_mask = 0; s.sel_wbelow = 0; s.sel_found = 0; s.sel_done = 0;
+    s.sel_total = 0; s.sel_cnt = 0; s.sel_k = 0;
+  }
+  for (int b = tid; b < 256; b += SIM_NT) { s.wbin[0][b] = 0; s.cbin[0][b] = 0; }
+  __syncthreads();
+  int hi = nbits, pb = 0;
+  while (hi > 0) {
+    const int lo = hi > 8 ? hi - 8 : 0;
+    const uint32_t dmask = (1u << (hi - lo)) - 1;
+    const uint64_t prefix = s.sel_prefix, mask = s.sel_mask;
+    unsigned long long* wbin = s.wbin[pb];
+    unsigned int* cbin = s.cbin[pb];
+    for (int b = tid; b < 256; b += SIM_NT) { s.wbin[pb ^ 1][b] = 0; s.cbin[pb ^ 1][b] = 0; }
+    for (uint32_t base = 0; base < n; base += SIM_NT) {
+      const uint32_t i = base + tid;
+      int dig = -1;
+      uint32_t w = 0;
+      if (i < n) {
+        uint64_t key;
+        uint32_t wi;
+        if (get(i, key, wi) && (key & mask) == prefix) {
+          dig = (int)((key >> lo) & dmask);
+          w = wi < Dc ? wi : Dc;
+        }
+      }
+      const unsigned peers = __match_any_sync(FULL, dig);
+      if (dig >= 0) {
+        const unsigned sum = __reduce_add_sync(peers, w);
+        if (lane == __ffs(peers) - 1) {
+          atomicAdd(&wbin[dig], (unsigned long long)sum);
+          atomicAdd(&cbin[dig], (unsigned)__popc(peers));
+        }
+      }
+    }
+    __syncthreads();
+    if (warp == 0) {
+      unsigned long long loc = 0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) loc += wbin[lane * 8 + q];
+      unsigned long long inc = loc;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long v = __shfl_up_sync(FULL, inc, o);
+        if (lane >= o) inc += v;
+      }
+      const unsigned long long wbelow = s.sel_wbelow;
+      unsigned long long c = wbelow + (inc - loc);
+      int mybin = -1;
+      unsigned long long wb = 0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const unsigned long long w = wbin[lane * 8 + q];
+        if (mybin < 0 && w > 0 && c + w >= D) { mybin = lane * 8 + q; wb = c; }
+        c += w;
+      }
+      const unsigned bal = __ballot_sync(FULL, mybin >= 0);
+      const unsigned long long total = wbelow + __shfl_sync(FULL, inc, 31);
+      if (bal == 0) {
+        if (lane == 0) { s.sel_found = 0; s.sel_done = 1; s.sel_total = total; }
+      } else if (lane == __ffs(bal) - 1) {
+        s.sel_prefix = prefix | ((uint64_t)mybin << lo);
+        s.sel_mask = mask | ((uint64_t)dmask << lo);
+        s.sel_wbelow = wb;
+        s.sel_cnt = cbin[mybin];
+        s.sel_found = 1;
+        if (lo == 0) { s.sel_done = 1; s.sel_k = s.sel_prefix; }
+      }
+    }
+    __syncthreads();
+    if (s.sel_done) break;
+    if (s.sel_cnt == 1) {  // the crossing bucket holds one item: find it
+      const uint64_t pf = s.sel_prefix, mk = s.sel_mask;
+      for (uint32_t i = tid; i < n; i += SIM_NT) {
+        uint64_t key;
+        uint32_t wi;
+        if (get(i, key, wi) && (key & mk) == pf) s.sel_k = key;
+      }
+      __syncthreads();
+      break;
+    }
+    hi = lo;
+    pb ^= 1;
+  }
+}
+
+struct Ctx {
+  const SimParams& p;
+  SimShm& s;
+  Coef k;
+  augsched_instance_params ip;
+  // arena slices of this instance
+  int32_t *ctx, *kv, *cpu, *pend;
+  uint32_t *meta, *ft, *lastc, *ac_id, *ac_last, *ac_dem, *pz_id;
+  uint64_t* ret;
+  double* ac_V;
+  uint32_t r0, n, trace;
+};
+
+__device__ __forceinline__ uint32_t gen_total(const DevTrace& tr, uint32_t rid) {
+  const uint32_t s0 = tr.seg_off[rid], ns = tr.n_seg[rid];
+  uint32_t g = 0;
+  for (uint32_t q = 0; q < ns; ++q) g += tr.gen_true[s0 + q];
+  return g;
+}
+
+// S2: one returned call (Algorithm 1 lines 10-24).
+__device__ void do_return(Ctx& c, uint32_t id) {
+  const DevTrace& tr = c.p.tr;
+  SimShm& s = c.s;
+  const uint32_t rid = c.r0 + id;
+  const uint32_t m = c.meta[id];
+  const uint32_t kk = meta_seg(m);
+  const int pol = (int)meta_pol(m);
+  const uint32_t s0 = tr.seg_off[rid];
+  const uint32_t ns = tr.n_seg[rid];
+  const int32_t ctx = c.ctx[id], kv = c.kv[id], cpu = c.cpu[id];
+  const uint64_t R = tr.ret_len[s0 + kk];
+  const uint64_t On = tr.gen_pred[s0 + kk + 1];
+  const bool has_next = kk + 1 < ns - 1;
+  const double An = has_next ? (double)tr.dur_pred[s0 + kk + 1] : 0.0;
+  const double V = intake_stage2(c.k, c.ip.policy_mode, pol, (uint64_t)ctx, R, On, An, has_next,
+                                 (uint64_t)s.A_snap);
+  uint32_t st, tier;
+  if (pol == POL_P) {
+    st = ST_RUN; tier = 0;
+    atomicAdd((unsigned long long*)&s.P, (unsigned long long)(-(long long)kv));
+    atomicAdd((unsigned long long*)&s.A, (unsigned long long)(long long)kv);
+  } else if (pol == POL_S) { st = ST_SWAP; tier = 1; }
+  else { st = ST_WAIT; tier = 2; }
+  c.pend[id] = (int32_t)R;
+  c.meta[id] = make_meta(kk + 1, st, (uint32_t)pol, 0);
+  atomicAdd(&s.cnt[AUGSCHED_R_RETURNS], 1ull);
+  const uint32_t pos = atomicAdd(&s.n_act, 1u);
+  c.ac_id[pos] = id | (tier << 30);
+  c.ac_V[pos] = V;
+  c.ac_last[pos] = c.lastc[id];  // not reset on return (R14)
+  c.ac_dem[pos] = demand_of(ctx, kv, cpu, (int32_t)R, c.p.cfg.s_in);
+}
+
+
+// S3: arrival of request `id` at active position `pos` (Algorithm 1 lines 2-9).
+__device__ void do_arrival(Ctx& c, uint32_t id, uint32_t pos, uint64_t t) {
+  const DevTrace& tr = c.p.tr;
+  const uint32_t rid = c.r0 + id;
+  const uint32_t s0 = tr.seg_off[rid];
+  const uint64_t L = tr.l_pre[rid];
+  const uint64_t O = tr.gen_pred[s0];
+  const bool has_call = tr.n_seg[rid] > 1;
+  const double A = has_call ? (double)tr.dur_pred[s0] : 0.0;
+  const double V = intake_stage1(c.k, c.ip.policy_mode, L, O, A, has_call, (uint64_t)c.s.A_snap);
+  c.ctx[id] = 0; c.kv[id] = 0; c.cpu[id] = 0; c.pend[id] = (int32_t)L;
+  c.meta[id] = make_meta(0, ST_WAIT, POL_D, 0);
+  c.ft[id] = 0;
+  c.ac_id[pos] = id | (2u << 30);
+  c.ac_V[pos] = V;
+  c.ac_last[pos] = (uint32_t)t;           // R14, R31
+  c.ac_dem[pos] = (uint32_t)L;
+}
+
+// Remove the active entries whose ac_id was set to INVALID.
+__device__ void compact_active(Ctx& c) {
+  SimShm& s = c.s;
+  const int tid = threadIdx.x;
+  __syncthreads();
+  if (s.n_holes == 0) return;
+  if (s.n_holes <= HOLE_CAP) {
+    if (tid == 0) {
+      const uint32_t L = s.n_holes, n = s.n_act, n_new = n - L;
+      uint32_t* h = s.holes;
+      for (uint32_t a = 1; a < L; ++a) {  // insertion sort (L small)
+        uint32_t x = h[a];
+        int b = (int)a - 1;
+        while (b >= 0 && h[b] > x) { h[b + 1] = h[b]; --b; }
+        h[b + 1] = x;
+      }
+      int j = (int)L - 1;
+      int src = (int)n - 1;
+      for (uint32_t a = 0; a < L; ++a) {
+        const uint32_t hp = h[a];
+        if (hp >= n_new) break;
+        while (j >= 0 && (int)h[j] == src) { --j; --src; }
+        c.ac_id[hp] = c.ac_id[src];
+        c.ac_V[hp] = c.ac_V[src];
+        c.ac_last[hp] = c.ac_last[src];
+        c.ac_dem[hp] = c.ac_dem[src];
+        --src;
+      }
+      s.n_act = n_new;
+    }
+    __syncthreads();
+    return;
+  }
+  // many removals: in-place tiled stream compaction
+  if (tid == 0) s.wpos = 0;
+  const uint32_t n = s.n_act;
+  for (uint32_t base = 0; base < n; base += SIM_NT) {
+    const uint32_t i = base + tid;
+    uint32_t id = INVALID, last = 0, dem = 0;
+    double V = 0;
+    if (i < n) { id = c.ac_id[i]; if (id != INVALID) { V = c.ac_V[i]; last = c.ac_last[i]; dem = c.ac_dem[i]; } }
+    const bool keep = id != INVALID;
+    const uint32_t pre = block_flag_scan(s, keep);  // syncs: all reads of the tile are done
+    const uint32_t w = s.wpos + pre;
+    if (keep) { c.ac_id[w] = id; c.ac_V[w] = V; c.ac_last[w] = last; c.ac_dem[w] = dem; }
+    __syncthreads();
+    if (tid == 0) s.wpos += s.wtot[SIM_NW];
+    __syncthreads();
+  }
+  if (tid == 0) s.n_act = s.wpos;
+  __syncthreads();
+}
+
+// Remove paused entries marked INVALID (small list; tiled compaction).
+__device__ void compact_paused(Ctx& c) {
+  SimShm& s = c.s;
+  const int tid = threadIdx.x;
+  __syncthreads();
+  if (tid == 0) s.wpos = 0;
+  const uint32_t n = s.n_pz;
+  for (uint32_t base = 0; base < n; base += SIM_NT) {
+    const uint32_t i = base + tid;
+    const uint32_t id = i < n ? c.pz_id[i] : INVALID;
+    const bool keep = id != INVALID;
+    const uint32_t pre = block_flag_scan(s, keep);
+    if (keep) c.pz_id[s.wpos + pre] = id;
+    __syncthreads();
+    if (tid == 0) s.wpos += s.wtot[SIM_NW];
+    __syncthreads();
+  }
+  if (tid == 0) s.n_pz = s.wpos;
+  __syncthreads();
+}
+
+__device__ void run_instance(const SimParams& p, SimShm& s, uint64_t* Ksm, uint32_t* Wsm,
+                             uint32_t inst) {
+  const int tid = threadIdx.x;
+  const size_t off = (size_t)inst * p.max_active;
+  const Arena& a = p.ar;
+  Ctx c{p, s, {}, p.ip[inst], a.ctx + off, a.kv + off, a.cpu + off, a.pend + off, a.meta + off,
+        a.ft + off, a.lastc + off, a.ac_id + off, a.ac_last + off, a.ac_dem + off, a.pz_id + off,
+        a.ret + off, a.ac_V + off, 0, 0, 0};
+  c.k = make_coef(p.cfg, c.ip);
+  c.trace = p.inst_trace[inst];
+  c.r0 = p.tr.req_off[c.trace];
+  c.n = p.tr.req_off[c.trace + 1] - c.r0;
+  const uint64_t T = p.cfg.t_fwd_ticks;
+  const uint32_t n = c.n;
+  InstHdr& H = p.hdr[inst];
+  augsched_result& acc = p.acc[inst];
+  if (n > p.max_active) {  // trace longer than the arena
+    if (tid == 0) { err_set(p, 2u); acc.f[AUGSCHED_R_ERR] |= 2; }
+    __syncthreads();
+    if (tid == 0) p.out[inst] = acc;
+    return;
+  }
+  // ---- load (or initialise) the resumable state -------------------------
+  if (tid == 0) {
+    if (!H.started) {
+      H.t = 0; H.A = 0; H.P = 0; H.min_ret = ~0ull; H.next_arr = 0; H.n_act = 0; H.n_pz = 0;
+      H.n_fin = 0; H.started = 1;
+    }
+    s.t = H.t; s.A = H.A; s.P = H.P; s.min_ret = H.min_ret; s.next_arr = H.next_arr;
+    s.n_act = H.n_act; s.n_pz = H.n_pz; s.n_fin = H.n_fin;
+    s.next_tick = s.next_arr < n ? p.tr.arr_tick[c.r0 + s.next_arr] : ~0ull;
+  }
+  for (int f = tid; f < AUGSCHED_R_NFIELD; f += SIM_NT) s.cnt[f] = acc.f[f];
+  for (int b = tid; b < AUGSCHED_NBIN; b += SIM_NT) { s.hist_t[b] = acc.hist_ttft[b]; s.hist_n[b] = acc.hist_norm[b]; }
+  __syncthreads();
+  if (tid == 0) s.cnt[AUGSCHED_R_NREQ] = n;
+  const int64_t cap = p.cap;
+
+  for (;;) {
+    // ---- loop top: stop rule, S1 snapshot ---------------------------------
+    if (tid == 0) {
+      s.run = (s.n_fin < n) && (s.t < p.max_iters);
+      s.tT = s.t * T;
+      s.A_snap = s.A;
+      s.n_holes = 0;
+    }
+    __syncthreads();
+    if (!s.run) break;
+    const uint64_t t = s.t, tT = s.tT;
+    // ---- S2 returns ----------------------------------------------------------
+    if (tT >= s.min_ret) {
+      const uint32_t npz = s.n_pz;
+      for (uint32_t i = tid; i < npz; i += SIM_NT) {
+        const uint32_t id = c.pz_id[i];
+        if (c.ret[id] <= tT) { do_return(c, id); c.pz_id[i] = INVALID; }
+      }
+      compact_paused(c);
+      if (tid == 0) s.min_ret = ~0ull;
+      __syncthreads();
+      for (uint32_t i = tid; i < s.n_pz; i += SIM_NT) atomicMin(&s.min_ret, (unsigned long long)c.ret[c.pz_id[i]]);
+      __syncthreads();
+    }
+    // ---- S3 arrivals (ticks are sorted: the arrivals are a prefix) ------------
+    if (tT >= s.next_tick) for (;;) {
+      const uint32_t j = s.next_arr + tid;
+      const bool arrive = j < n && p.tr.arr_tick[c.r0 + j] <= tT;
+      const int cnt = __syncthreads_count(arrive);
+      if (arrive) do_arrival(c, j, s.n_act + tid, t);
+      __syncthreads();
+      if (tid == 0) {
+        s.n_act += cnt; s.next_arr += cnt; s.cnt[AUGSCHED_R_ARRIVED] += cnt;
+        if (cnt < SIM_NT) s.next_tick = s.next_arr < n ? p.tr.arr_tick[c.r0 + s.next_arr] : ~0ull;
+      }
+      __syncthreads();
+      if (cnt < SIM_NT) break;
+    }
+    // ---- idle check; S4 token limit -------------------------------------------
+    if (tid == 0) {
+      s.idle = 0;
+      if (s.n_act == 0) {
+        uint64_t te = ~0ull;
+        if (s.next_arr < n) te = (p.tr.arr_tick[c.r0 + s.next_arr] + T - 1) / T;
+        if (s.n_pz > 0) { const uint64_t tr_ = (s.min_ret + T - 1) / T; te = tr_ < te ? tr_ : te; }
+        if (te == ~0ull) s.idle = 2; else { s.t = te; s.idle = 1; }
+      } else {
+        s.B = token_limit(p.cfg, c.k, c.ip, cap, s.A, s.P);
+        s.cnt[AUGSCHED_R_BUSY_STEPS] += 1;
+        s.cnt[AUGSCHED_R_DECISIONS] += s.n_act;
+        if (s.n_act > s.cnt[AUGSCHED_R_MAXQ]) s.cnt[AUGSCHED_R_MAXQ] = s.n_act;
+      }
+    }
+    __syncthreads();
+    if (s.idle == 2) break;
+    if (s.idle == 1) continue;
+    // ---- S5 keys --------------------------------------------------------------
+    const uint32_t na = s.n_act;
+    const bool in_smem = na <= p.scap;
+    uint64_t* K = in_smem ? Ksm : a.kscr + off;
+    uint32_t* W = in_smem ? Wsm : a.wscr + off;
+    const bool fcfs = c.ip.ranking == AUGSCHED_RANK_FCFS;
+    for (uint32_t i = tid; i < na; i += SIM_NT) {
+      const uint32_t e = c.ac_id[i];
+      const uint32_t key = fcfs ? 0u : sched_key(c.k, c.ac_V[i], t, c.ac_last[i]);
+      K[i] = ((uint64_t)(e >> 30) << 48) | ((uint64_t)key << 16) | (e & 0xFFFF);
+      W[i] = c.ac_dem[i];
+    }
+    // ---- S6/S7 order + admission: weighted select of the prefix ---------------
+    const long long B = s.B;
+    if (B > 0) {
+      wselect(s, na, (uint64_t)B, KBITS, [&](uint32_t i, uint64_t& key, uint32_t& w) {
+        key = K[i]; w = W[i]; return true; });
+    } else {
+      __syncthreads();
+      if (tid == 0) { s.sel_found = 1; s.sel_k = 0; s.sel_wbelow = 0; }  // nothing admitted
+      __syncthreads();
+    }
+    const bool found = s.sel_found != 0;
+    const uint64_t kstar = B > 0 ? s.sel_k : 0;
+    const uint64_t wb = s.sel_wbelow;
+    auto grant = [&](uint64_t Ki, uint32_t dem) -> uint32_t {
+      if (Ki & KEVICT) return 0u;
+      if (B <= 0) return 0u;
+      if (!found || Ki < kstar) return dem;
+      if (Ki == kstar) return (uint32_t)((uint64_t)B - wb);
+      return 0u;
+    };
+    if (tid == 0) {
+      s.need = found ? (B > 0 ? B : 0) : (long long)s.sel_total;
+      s.freev = cap - s.A - s.P;
+      s.freed = 0;
+    }
+    __syncthreads();
+    // ---- S8 memory resolution (R20) -------------------------------------------
+    if (s.need > s.freev) {
+      // (1) demote Preserve-paused contexts, kv desc, id asc
+      const uint64_t D0 = (uint64_t)(s.need - s.freev);
+      const uint32_t npz = s.n_pz;
+      auto getp = [&](uint32_t i, uint64_t& key, uint32_t& w) {
+        const uint32_t id = c.pz_id[i];
+        const int32_t kv = c.kv[id];
+        if (meta_pol(c.meta[id]) != POL_P || kv <= 0) return false;
+        key = ((uint64_t)(0xFFFFFFFFu - (uint32_t)kv) << 16) | id;
+        w = (uint32_t)kv;
+        return true;
+      };
+      wselect(s, npz, D0, 48, getp);
+      {
+        const bool f0 = s.sel_found != 0;
+        const uint64_t k0 = s.sel_k;
+        for (uint32_t i = tid; i < npz; i += SIM_NT) {
+          uint64_t key; uint32_t w;
+          if (getp(i, key, w) && (!f0 || key <= k0)) {
+            const uint32_t id = c.pz_id[i];
+            atomicAdd(&s.freed, (unsigned long long)w);
+            c.kv[id] = 0;
+            const uint32_t m = c.meta[id];
+            c.meta[id] = make_meta(meta_seg(m), meta_st(m), POL_D, meta_gen(m));
+            atomicAdd(&s.cnt[AUGSCHED_R_DEMOTIONS], 1ull);
+          }
+        }
+      }
+      __syncthreads();
+      if (tid == 0) { s.freev += (long long)s.freed; s.P -= (long long)s.freed; s.freed = 0; }
+      __syncthreads();
+      // (2) evict from the tail of the order over entries with kv + g > 0
+      if (s.need > s.freev) {
+        const uint64_t D1 = (uint64_t)(s.need - s.freev);
+        for (uint32_t i = tid; i < na; i += SIM_NT) {
+          const uint32_t id = c.ac_id[i] & 0xFFFF;
+          W[i] = (uint32_t)c.kv[id] + grant(K[i], c.ac_dem[i]);
+        }
+        auto gete = [&](uint32_t i, uint64_t& key, uint32_t& w) {
+          w = W[i];
+          key = KMASK - K[i];
+          return w > 0;
+        };
+        wselect(s, na, D1, KBITS, gete);
+        const bool f1 = s.sel_found != 0;
+        const uint64_t k1 = s.sel_k;
+        for (uint32_t i = tid; i < na; i += SIM_NT) {
+          uint64_t key; uint32_t w;
+          if (gete(i, key, w) && (!f1 || key <= k1)) {
+            const uint32_t e = c.ac_id[i];
+            const uint32_t id = e & 0xFFFF;
+            const int32_t kv = c.kv[id];
+            atomicAdd((unsigned long long*)&s.A, (unsigned long long)(-(long long)kv));
+            c.kv[id] = 0;
+            c.cpu[id] = 0;
+            const uint32_t m = c.meta[id];
+            c.meta[id] = make_meta(meta_seg(m), ST_WAIT, meta_pol(m), meta_gen(m));
+            c.ac_id[i] = id | (2u << 30);
+            c.ac_dem[i] = demand_of(c.ctx[id], 0, 0, c.pend[id], p.cfg.s_in);
+            K[i] |= KEVICT;
+            atomicAdd(&s.cnt[AUGSCHED_R_EVICTIONS], 1ull);
+          }
+        }
+        __syncthreads();
+      }
+    }
+    // ---- S9 last = t for granted entries; S10 engine advance -------------------
+    {
+      uint32_t my_tok = 0, my_adm = 0;
+      for (uint32_t i = tid; i < na; i += SIM_NT) {
+        const uint32_t g = grant(K[i], c.ac_dem[i]);
+        if (g == 0) continue;
+        my_tok += g; my_adm += 1;
+        const uint32_t id = c.ac_id[i] & 0xFFFF;
+        const uint32_t rid = c.r0 + id;
+        int32_t ctx = c.ctx[id], kv = c.kv[id], cpu = c.cpu[id], pend = c.pend[id];
+        const int32_t kv_snap = kv;
+        uint32_t m = c.meta[id];
+        uint32_t seg = meta_seg(m), gen = meta_gen(m), pol = meta_pol(m);
+        long long dA = 0, dP = 0;
+        bool leave = false;
+        if (cpu > 0) {                                   // swap-in
+          cpu -= (int32_t)g; kv += (int32_t)g; dA += g;
+        } else if ((ctx - kv) + pend > 0) {              // recompute, then prefill/assimilate
+          const int32_t rc = (int32_t)g < ctx - kv ? (int32_t)g : ctx - kv;
+          kv += rc;
+          const int32_t pp = (int32_t)g - rc;
+          pend -= pp; ctx += pp; kv += pp;
+          dA += g;
+        } else {                                         // decode one token
+          ctx += 1; kv += 1; dA += 1; gen += 1;
+          if (c.ft[id] == 0) c.ft[id] = (uint32_t)(t + 1);  // R22
+          const uint32_t s0 = p.tr.seg_off[rid];
+          const uint32_t ns = p.tr.n_seg[rid];
+          if (gen == p.tr.gen_true[s0 + seg]) {
+            leave = true;
+            if (seg + 1 == ns) {                         // finish
+              dA -= kv; kv = 0;
+              m = make_meta(seg, ST_DONE, pol, gen);
+              const uint64_t arr = p.tr.arr_tick[rid];
+              const uint64_t fin = t + 1;
+              const uint64_t ttft = (uint64_t)c.ft[id] * T - arr;
+              const uint64_t e2e = fin * T - arr;
+              const uint64_t gt = gen_total(p.tr, rid);
+              const bool ok = ttft < c.ip.slo_ttft_ticks &&
+                              e2e * c.ip.slo_norm_den < (uint64_t)c.ip.slo_norm_num * T * gt;
+              const bool ok5 = ttft < 5 * c.ip.slo_ttft_ticks &&
+                               e2e * c.ip.slo_norm_den < 5 * (uint64_t)c.ip.slo_norm_num * T * gt;
+              atomicAdd(&s.n_fin, 1u);
+              atomicAdd(&s.cnt[AUGSCHED_R_COMPLETED], 1ull);
+              if (ok) atomicAdd(&s.cnt[AUGSCHED_R_SLO_OK], 1ull);
+              if (ok5) atomicAdd(&s.cnt[AUGSCHED_R_SLO_OK_5X], 1ull);
+              atomicMax(&s.cnt[AUGSCHED_R_MAKESPAN], (unsigned long long)fin);
+              atomicAdd(&s.cnt[AUGSCHED_R_SUM_TTFT], (unsigned long long)ttft);
+              atomicAdd(&s.cnt[AUGSCHED_R_SUM_E2E], (unsigned long long)e2e);
+              atomicAdd(&s.cnt[AUGSCHED_R_SUM_GEN], (unsigned long long)gt);
+              atomicAdd(&s.hist_t[hist_bin(ttft)], 1u);
+              atomicAdd(&s.hist_n[hist_bin(e2e / gt)], 1u);
+            } else {                                     // issue call `seg` (R13, R21)
+              const double Ti = (double)p.tr.dur_pred[s0 + seg];
+              const int np = select_policy(c.k, (uint64_t)ctx, Ti,
+                                           (uint64_t)(s.A_snap - (long long)kv_snap),
+                                           c.ip.policy_mode);
+              const uint64_t rt = (t + 1) * T + p.tr.dur_true[s0 + seg];
+              c.ret[id] = rt;
+              c.lastc[id] = (uint32_t)t;
+              dA -= kv;
+              if (np == POL_P) { dP += kv; atomicAdd(&s.cnt[AUGSCHED_R_CALLS_PRESERVE], 1ull); }
+              else if (np == POL_S) { cpu = ctx; kv = 0; atomicAdd(&s.cnt[AUGSCHED_R_CALLS_SWAP], 1ull); }
+              else { kv = 0; atomicAdd(&s.cnt[AUGSCHED_R_CALLS_DISCARD], 1ull); }
+              m = make_meta(seg, ST_PAUSED, (uint32_t)np, gen);
+              const uint32_t q = atomicAdd(&s.n_pz, 1u);
+              c.pz_id[q] = id;
+              atomicMin(&s.min_ret, (unsigned long long)rt);
+            }
+          }
+        }
+        if (!leave) m = make_meta(seg, ST_RUN, pol, gen);
+        c.ctx[id] = ctx; c.kv[id] = kv; c.cpu[id] = cpu; c.pend[id] = pend; c.meta[id] = m;
+        if (dA) atomicAdd((unsigned long long*)&s.A, (unsigned long long)dA);
+        if (dP) atomicAdd((unsigned long long*)&s.P, (unsigned long long)dP);
+        if (leave) {
+          c.ac_id[i] = INVALID;
+          const uint32_t hslot = atomicAdd(&s.n_holes, 1u);
+          if (hslot < HOLE_CAP) s.holes[hslot] = i;
+        } else {
+          c.ac_id[i] = id;                               // tier 0: running (R16)
+          c.ac_last[i] = (uint32_t)t;                    // R14
+          c.ac_dem[i] = demand_of(ctx, kv, cpu, pend, p.cfg.s_in);
+        }
+      }
+      if (my_tok) atomicAdd(&s.cnt[AUGSCHED_R_TOKENS], (unsigned long long)my_tok);
+      if (my_adm) atomicAdd(&s.cnt[AUGSCHED_R_ADMITTED], (unsigned long long)my_adm);
+    }
+    compact_active(c);  // syncs
+    if (tid == 0) {
+      if (s.A < 0 || s.P < 0 || s.A + s.P > cap) s.cnt[AUGSCHED_R_ERR] |= 1;
+      s.t = t + 1;                                       // S12
+    }
+    __syncthreads();
+  }
+  // ---- save state and results ------------------------------------------------
+  __syncthreads();
+  if (tid == 0) {
+    H.t = s.t; H.A = s.A; H.P = s.P; H.min_ret = s.min_ret; H.next_arr = s.next_arr;
+    H.n_act = s.n_act; H.n_pz = s.n_pz; H.n_fin = s.n_fin;
+    s.cnt[AUGSCHED_R_FINAL_T] = s.t;
+  }
+  __syncthreads();
+  augsched_result& out = p.out[inst];
+  for (int f = tid; f < AUGSCHED_R_NFIELD; f += SIM_NT) { acc.f[f] = s.cnt[f]; out.f[f] = s.cnt[f]; }
+  for (int b = tid; b < AUGSCHED_NBIN; b += SIM_NT) {
+    acc.hist_ttft[b] = s.hist_t[b]; out.hist_ttft[b] = s.hist_t[b];
+    acc.hist_norm[b] = s.hist_n[b]; out.hist_norm[b] = s.hist_n[b];
+  }
+}
+
+__global__ void __launch_bounds__(SIM_NT, SIM_MINB) sim_kernel(SimParams p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  SimShm& s = *reinterpret_cast<SimShm*>(smem_raw);
+  uint64_t* Ksm = reinterpret_cast<uint64_t*>(smem_raw + ((sizeof(SimShm) + 15) & ~size_t(15)));
+  uint32_t* Wsm = reinterpret_cast<uint32_t*>(Ksm + p.scap);
+  for (;;) {
+    if (threadIdx.x == 0) s.inst = atomicAdd(p.work, 1u);
+    __syncthreads();
+    const uint32_t inst = s.inst;
+    if (inst >= p.n_inst) return;
+    run_instance(p, s, Ksm, Wsm, inst);
+    __syncthreads();
+  }
+}
+
+}  // namespace
+
+size_t sim_smem_bytes(uint32_t scap) {
+  return ((sizeof(SimShm) + 15) & ~size_t(15)) + (size_t)scap * (sizeof(uint64_t) + sizeof(uint32_t));
+}
+
+const void* sim_kernel_ptr() { return reinterpret_cast<const void*>(&sim_kernel); }
+
+cudaError_t launch_sim(const SimParams& p, int grid, size_t smem, cudaStream_t st) {
+  sim_kernel<<<grid, SIM_NT, smem, st>>>(p);
+  return cudaGetLastError();
+}
+
+}  // namespace augsched

@@ -1,0 +1,103 @@
+// Persistent per-instance simulation kernel (K8 of SURVEY §2.4), fusing
+// intake (Stage I/II), the token-limit update, scoring, ordering, admission,
+// memory resolution, engine advance and metrics for one instance per CTA.
+//
+// Ordering without a sort: the per-step outputs that feed the simulation only
+// depend on WHICH entries fall in the admitted prefix of the (tier, key, id)
+// order and on the single partially-granted entry (R17), and, under memory
+// pressure, on which tail entries are evicted (R20).  Both are weighted
+// order statistics: the admitted prefix ends at the first entry whose
+// cumulative demand reaches the limit B, the evicted tail at the first entry
+// (from the back) whose cumulative kv+grant reaches the deficit.  They are
+// found exactly by an MSD radix select over the unique 50-bit composite key
+// (tier << 48 | key << 16 | id) with demand-weighted shared-memory
+// histograms (warp-aggregated with __match_any_sync / __reduce_add_sync).
+// augsched_step, whose API returns the full order, uses the sort kernels.
+#pragma once
+#include <cstdint>
+#include "augsched.h"
+#include "model.cuh"
+
+namespace augsched {
+
+constexpr int SIM_NT = 128;
+constexpr int SIM_MINB = 8;              // CTAs per SM the kernel is register-bounded for
+constexpr int SIM_NW = SIM_NT / 32;
+constexpr int KBITS = 50;                 // tier(2) | key(32) | id(16)
+constexpr uint64_t KMASK = (1ull << KBITS) - 1;
+constexpr uint64_t KEVICT = 1ull << 63;   // marks an evicted entry in the K array
+constexpr int HOLE_CAP = 64;              // serial hole filling up to this many removals
+
+// Trace set as the kernel sees it (device pointers).
+struct DevTrace {
+  const uint32_t* req_off;
+  const uint64_t* arr_tick;
+  const uint32_t* l_pre;
+  const uint32_t* seg_off;
+  const uint32_t* n_seg;
+  const uint32_t* gen_true;
+  const uint32_t* gen_pred;
+  const uint32_t* dur_true;
+  const float* dur_pred;
+  const uint32_t* ret_len;
+};
+
+// Per-instance persistent header (resumable simulation).
+struct InstHdr {
+  uint64_t t;
+  int64_t A, P;           // KV ledger in tokens: active, Preserve-paused
+  uint64_t min_ret;       // min return tick over the paused list
+  uint32_t next_arr, n_act, n_pz, n_fin;
+  uint32_t started, pad;
+};
+
+// Handle-owned per-instance arena (stride = max_active entries per instance).
+struct Arena {
+  // cold state by request id
+  int32_t* ctx;
+  int32_t* kv;
+  int32_t* cpu;
+  int32_t* pend;
+  uint32_t* meta;      // seg:8 | status:4 | pol:4 | gen_done:16
+  uint64_t* ret;       // return tick of the outstanding call
+  uint32_t* ft;        // first-token iteration (t+1 >= 1; 0 = none)
+  uint32_t* lastc;     // last-scheduled iteration while paused (R14)
+  // active list by position
+  uint32_t* ac_id;     // id | tier << 30  (tier 0 running, 1 swapped, 2 waiting)
+  double* ac_V;
+  uint32_t* ac_last;
+  uint32_t* ac_dem;
+  // paused list by position
+  uint32_t* pz_id;
+  // scratch for steps whose queue exceeds the shared-memory capacity
+  uint64_t* kscr;
+  uint32_t* wscr;
+  uint64_t* kscr2;     // secondary selections (demotion)
+  uint32_t* wscr2;
+};
+
+struct SimParams {
+  augsched_config cfg;
+  int64_t cap;                               // floor((G_total - G_fixed)/M)
+  DevTrace tr;
+  const augsched_instance_params* ip;        // [n_inst]
+  const uint32_t* inst_trace;                // [n_inst]
+  Arena ar;
+  InstHdr* hdr;                              // [n_inst]
+  augsched_result* acc;                      // [n_inst] handle-owned accumulators
+  augsched_result* out;                      // [n_inst] caller's results (device)
+  uint64_t max_iters;
+  uint32_t n_inst, max_active, scap;
+  uint32_t* work;                            // work-stealing counter
+  uint32_t* err;                             // device error word
+};
+
+__device__ __forceinline__ uint32_t meta_seg(uint32_t m) { return m & 0xFF; }
+__device__ __forceinline__ uint32_t meta_st(uint32_t m) { return (m >> 8) & 0xF; }
+__device__ __forceinline__ uint32_t meta_pol(uint32_t m) { return (m >> 12) & 0xF; }
+__device__ __forceinline__ uint32_t meta_gen(uint32_t m) { return m >> 16; }
+__device__ __forceinline__ uint32_t make_meta(uint32_t seg, uint32_t st, uint32_t pol, uint32_t gen) {
+  return (seg & 0xFF) | (st << 8) | (pol << 12) | (gen << 16);
+}
+
+}  // namespace augsched
