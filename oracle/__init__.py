@@ -259,6 +259,14 @@ class Step:
         return dict(rc=rc, B=B, n_active=na, admitted=adm, order=order.reshape(n, m),
                     grant=grant.reshape(n, m), keys=keys.reshape(n, m))
 
+    def slots(self, inst: int) -> np.ndarray:
+        """[max_active, 6] int32: status, policy, ctx, kv, cpu, pend."""
+        self.L.oracle_step_slot.argtypes = [C.c_void_p, C.c_uint32, C.c_uint32, C.c_void_p]
+        out = np.zeros((self.max_active, 6), np.int32)
+        for j in range(self.max_active):
+            self.L.oracle_step_slot(self.h, inst, j, out[j].ctypes.data)
+        return out
+
     def ledger(self, inst: int):
         A = C.c_int64()
         P = C.c_int64()

@@ -569,8 +569,10 @@ int step_one(OStep& S, uint32_t i, uint64_t now, int64_t* B_out, uint32_t* n_out
   // S7 admission
   std::vector<int64_t> g(ord.size(), 0);
   int64_t Pj = 0;
+  uint32_t n_prefix = 0;  // admission prefix length (entries with P_{j-1} < B)
   for (size_t j = 0; j < ord.size(); ++j) {
     if (Pj >= B) break;
+    ++n_prefix;
     int64_t d;
     const SSlot& s = I.s[ord[j].id];
     if (s.cpu > 0) d = std::min<int64_t>(s.cpu, cfg.s_in);
@@ -604,13 +606,11 @@ int step_one(OStep& S, uint32_t i, uint64_t now, int64_t* B_out, uint32_t* n_out
     }
   }
   // S9 + token accounting of the granted batch
-  uint32_t adm = 0;
   for (size_t j = 0; j < ord.size(); ++j) {
     order[j] = ord[j].id;
     keys[j] = ord[j].key;
     grant[j] = (uint32_t)g[j];
     if (g[j] <= 0) continue;
-    ++adm;
     SSlot& s = I.s[ord[j].id];
     int64_t x = g[j];
     s.last = now;
@@ -625,7 +625,7 @@ int step_one(OStep& S, uint32_t i, uint64_t now, int64_t* B_out, uint32_t* n_out
   }
   *B_out = B;
   *n_out = (uint32_t)ord.size();
-  *adm_out = adm;
+  *adm_out = n_prefix;
   return err;
 }
 
@@ -737,6 +737,12 @@ int oracle_step(void* h, uint64_t now, int64_t* B, uint32_t* n_active, uint32_t*
     if (e) err = e;
   }
   return err;
+}
+// slot state: status (0 empty, 1 run, 2 swap, 3 wait, 4 paused), policy, token counts
+void oracle_step_slot(void* h, uint32_t inst, uint32_t id, int32_t* out6) {
+  const SSlot& s = ((OStep*)h)->inst[inst].s[id];
+  out6[0] = s.status; out6[1] = s.pol; out6[2] = (int32_t)s.ctx; out6[3] = (int32_t)s.kv;
+  out6[4] = (int32_t)s.cpu; out6[5] = (int32_t)s.pend;
 }
 void oracle_step_ledger(void* h, uint32_t inst, int64_t* A, int64_t* P) {
   OStep* S = (OStep*)h;

@@ -9,7 +9,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libaugsched.so")
 SOURCES = ["sim.cu", "step.cu", "api.cu"]
-HEADERS = ["model.cuh", "sim.cuh", "step.cuh"]
+HEADERS = ["model.cuh", "sim.cuh", "step.cuh", "select.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

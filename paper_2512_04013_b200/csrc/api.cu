@@ -320,15 +320,15 @@ int augsched_enqueue(augsched_t* h, uint32_t instance, const augsched_record_soa
   if (!h || !recs) return fail(AUGSCHED_E_INVALID, "enqueue: NULL argument");
   if (instance >= h->n_inst) return fail(AUGSCHED_E_INVALID, "enqueue: bad instance %u", instance);
   CUDA_TRY(cudaSetDevice(h->device));
-  int rc = step_ensure(h->st, h->n_inst, h->max_active, h->stream);
+  int rc = step_ensure(h->st, h->n_inst, h->max_active, h->stream, h->cfg, h->d_ip, &h->launches);
   if (rc) return rc;
-  return step_enqueue(h->st, instance, recs, n, recs_on_device, h->stream, &h->launches);
+  return step_enqueue(h->st, instance, recs, n, recs_on_device, h->stream, h->d_err, &h->launches);
 }
 
 int augsched_step(augsched_t* h, uint64_t now_iter, augsched_step_out* out) {
   if (!h || !out) return fail(AUGSCHED_E_INVALID, "step: NULL argument");
   CUDA_TRY(cudaSetDevice(h->device));
-  int rc = step_ensure(h->st, h->n_inst, h->max_active, h->stream);
+  int rc = step_ensure(h->st, h->n_inst, h->max_active, h->stream, h->cfg, h->d_ip, &h->launches);
   if (rc) return rc;
   return step_run(h->st, h->cfg, h->cap, h->d_ip, h->d_err, now_iter, out, h->stream, &h->launches);
 }

@@ -1,0 +1,120 @@
+// Block-wide weighted MSD radix select (shared by the simulate and step paths).
+//
+// Among items i < n for which get(i, key, w) returns true (w >= 1, keys
+// unique, key < 2^nbits), find the smallest key k* with
+//     sum_{key <= k*} w >= D.
+// This is the last entry of the admitted prefix of Algorithm 1's fill loop
+// (P:1221-1229 with the chunked last entry of R17) when keys are the
+// (tier, score key, id) order and weights the demands; with keys taken from
+// the back of the order and weights kv + grant it is the eviction cut of R20.
+//
+// 8-bit digits from the top; demand-weighted shared-memory histograms built
+// with warp-aggregated atomics (__match_any_sync + __reduce_add_sync), double
+// buffered so each pass costs two barriers; a per-bin witness key ends the
+// search as soon as the crossing bucket holds a single item.  Weights are
+// clamped to D, which is exact: every item before k* has w < D.
+#pragma once
+#include <cstdint>
+
+namespace augsched {
+
+struct SelShm {
+  unsigned long long wbin[2][256];
+  unsigned int cbin[2][256];
+  unsigned long long wkey[2][256];
+  unsigned long long prefix, mask, wbelow, k, total;
+  unsigned int cnt;
+  int found, done;
+};
+
+// Results: s.found (0: total weight < D, s.total holds it), s.k = k*,
+// s.wbelow = sum of weights with key < k*.  Must be called by all NT threads.
+template <int NT, class Get>
+__device__ void wselect(SelShm& s, uint32_t n, uint64_t D, int nbits, Get get) {
+  constexpr unsigned FULL = 0xffffffffu;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t Dc = (uint32_t)(D < (1ull << 26) ? D : (1ull << 26));
+  __syncthreads();
+  if (tid == 0) {
+    s.prefix = 0; s.mask = 0; s.wbelow = 0; s.found = 0; s.done = 0; s.total = 0; s.cnt = 0;
+    s.k = 0;
+  }
+  for (int b = tid; b < 256; b += NT) { s.wbin[0][b] = 0; s.cbin[0][b] = 0; }
+  __syncthreads();
+  int hi = nbits, pb = 0;
+  while (hi > 0) {
+    const int lo = hi > 8 ? hi - 8 : 0;
+    const uint32_t dmask = (1u << (hi - lo)) - 1;
+    const uint64_t prefix = s.prefix, mask = s.mask;
+    unsigned long long* wbin = s.wbin[pb];
+    unsigned int* cbin = s.cbin[pb];
+    unsigned long long* wkey = s.wkey[pb];
+    for (int b = tid; b < 256; b += NT) { s.wbin[pb ^ 1][b] = 0; s.cbin[pb ^ 1][b] = 0; }
+    for (uint32_t base = 0; base < n; base += NT) {
+      const uint32_t i = base + tid;
+      int dig = -1;
+      uint32_t w = 0;
+      uint64_t key = 0;
+      if (i < n) {
+        uint32_t wi;
+        if (get(i, key, wi) && (key & mask) == prefix) {
+          dig = (int)((key >> lo) & dmask);
+          w = wi < Dc ? wi : Dc;
+        }
+      }
+      const unsigned peers = __match_any_sync(FULL, dig);
+      if (dig >= 0) {
+        const unsigned sum = __reduce_add_sync(peers, w);
+        if (lane == __ffs(peers) - 1) {
+          atomicAdd(&wbin[dig], (unsigned long long)sum);
+          atomicAdd(&cbin[dig], (unsigned)__popc(peers));
+          wkey[dig] = key;
+        }
+      }
+    }
+    __syncthreads();
+    if (warp == 0) {
+      unsigned long long run = s.wbelow;
+      int bin = -1;
+      unsigned long long wb = 0;
+#pragma unroll 1
+      for (int q = 0; q < 8; ++q) {
+        const int b = q * 32 + lane;
+        const unsigned long long w = wbin[b];
+        unsigned long long inc = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const unsigned long long v = __shfl_up_sync(FULL, inc, o);
+          if (lane >= o) inc += v;
+        }
+        const unsigned bal = __ballot_sync(FULL, w > 0 && run + inc >= D);
+        if (bal) {
+          const int f = __ffs(bal) - 1;
+          bin = q * 32 + f;
+          wb = run + __shfl_sync(FULL, inc - w, f);
+          break;
+        }
+        run += __shfl_sync(FULL, inc, 31);
+      }
+      if (lane == 0) {
+        if (bin < 0) {
+          s.found = 0; s.done = 1; s.total = run;
+        } else {
+          s.prefix = prefix | ((uint64_t)bin << lo);
+          s.mask = mask | ((uint64_t)dmask << lo);
+          s.wbelow = wb;
+          s.cnt = cbin[bin];
+          s.found = 1;
+          if (lo == 0) { s.done = 1; s.k = s.prefix; }
+          else if (s.cnt == 1) { s.done = 1; s.k = wkey[bin]; }
+        }
+      }
+    }
+    __syncthreads();
+    if (s.done) break;
+    hi = lo;
+    pb ^= 1;
+  }
+}
+
+}  // namespace augsched

@@ -3,12 +3,12 @@
 // sequence" (S1..S12), i.e. Algorithm 1 plus the engine model.
 #include <cuda_runtime.h>
 #include "sim.cuh"
+#include "select.cuh"
 
 namespace augsched {
 
 struct __align__(16) SimShm {
-  unsigned long long wbin[2][256];   // double-buffered select histograms
-  unsigned int cbin[2][256];
+  SelShm sel;
   unsigned int hist_t[AUGSCHED_NBIN];
   unsigned int hist_n[AUGSCHED_NBIN];
   unsigned long long cnt[AUGSCHED_R_NFIELD];
@@ -21,10 +21,6 @@ struct __align__(16) SimShm {
   unsigned int next_arr, n_act, n_pz, n_fin, n_holes, n_pholes, wpos;
   unsigned int inst, n_req, r0;
   int run, idle;
-  // selection state
-  unsigned long long sel_prefix, sel_mask, sel_wbelow, sel_k, sel_total;
-  unsigned int sel_cnt;
-  int sel_found, sel_done;
 };
 
 namespace {
@@ -52,100 +48,9 @@ __device__ __forceinline__ uint32_t block_flag_scan(SimShm& s, bool f) {
 
 // Weighted MSD radix select.  Among items i < n for which get(i, key, w)
 // returns true (w >= 1, keys unique, key < 2^nbits) find the smallest key k*
-// with sum_{key <= k*} w >= D.  Results: s.sel_found (1 found / 0 not: then
-// s.sel_total holds the full weight), s.sel_k, s.sel_wbelow = sum_{key < k*} w.
+// with sum_{key <= k*} w >= D.  Results: s.sel.found (1 found / 0 not: then
+// s.sel.total holds the full weight), s.sel.k, s.sel.wbelow = sum_{key < k*} w.
 // Weights are clamped to D (exact: every item before k* has w < D).
-template <class Get>
-__device__ void wselect(SimShm& s, uint32_t n, uint64_t D, int nbits, Get get) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const uint32_t Dc = (uint32_t)(D < (1ull << 26) ? D : (1ull << 26));
-  __syncthreads();
-  if (tid == 0) {
-    s.sel_prefix = 0; s.sel_mask = 0; s.sel_wbelow = 0; s.sel_found = 0; s.sel_done = 0;
-    s.sel_total = 0; s.sel_cnt = 0; s.sel_k = 0;
-  }
-  for (int b = tid; b < 256; b += SIM_NT) { s.wbin[0][b] = 0; s.cbin[0][b] = 0; }
-  __syncthreads();
-  int hi = nbits, pb = 0;
-  while (hi > 0) {
-    const int lo = hi > 8 ? hi - 8 : 0;
-    const uint32_t dmask = (1u << (hi - lo)) - 1;
-    const uint64_t prefix = s.sel_prefix, mask = s.sel_mask;
-    unsigned long long* wbin = s.wbin[pb];
-    unsigned int* cbin = s.cbin[pb];
-    for (int b = tid; b < 256; b += SIM_NT) { s.wbin[pb ^ 1][b] = 0; s.cbin[pb ^ 1][b] = 0; }
-    for (uint32_t base = 0; base < n; base += SIM_NT) {
-      const uint32_t i = base + tid;
-      int dig = -1;
-      uint32_t w = 0;
-      if (i < n) {
-        uint64_t key;
-        uint32_t wi;
-        if (get(i, key, wi) && (key & mask) == prefix) {
-          dig = (int)((key >> lo) & dmask);
-          w = wi < Dc ? wi : Dc;
-        }
-      }
-      const unsigned peers = __match_any_sync(FULL, dig);
-      if (dig >= 0) {
-        const unsigned sum = __reduce_add_sync(peers, w);
-        if (lane == __ffs(peers) - 1) {
-          atomicAdd(&wbin[dig], (unsigned long long)sum);
-          atomicAdd(&cbin[dig], (unsigned)__popc(peers));
-        }
-      }
-    }
-    __syncthreads();
-    if (warp == 0) {
-      unsigned long long loc = 0;
-#pragma unroll
-      for (int q = 0; q < 8; ++q) loc += wbin[lane * 8 + q];
-      unsigned long long inc = loc;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const unsigned long long v = __shfl_up_sync(FULL, inc, o);
-        if (lane >= o) inc += v;
-      }
-      const unsigned long long wbelow = s.sel_wbelow;
-      unsigned long long c = wbelow + (inc - loc);
-      int mybin = -1;
-      unsigned long long wb = 0;
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const unsigned long long w = wbin[lane * 8 + q];
-        if (mybin < 0 && w > 0 && c + w >= D) { mybin = lane * 8 + q; wb = c; }
-        c += w;
-      }
-      const unsigned bal = __ballot_sync(FULL, mybin >= 0);
-      const unsigned long long total = wbelow + __shfl_sync(FULL, inc, 31);
-      if (bal == 0) {
-        if (lane == 0) { s.sel_found = 0; s.sel_done = 1; s.sel_total = total; }
-      } else if (lane == __ffs(bal) - 1) {
-        s.sel_prefix = prefix | ((uint64_t)mybin << lo);
-        s.sel_mask = mask | ((uint64_t)dmask << lo);
-        s.sel_wbelow = wb;
-        s.sel_cnt = cbin[mybin];
-        s.sel_found = 1;
-        if (lo == 0) { s.sel_done = 1; s.sel_k = s.sel_prefix; }
-      }
-    }
-    __syncthreads();
-    if (s.sel_done) break;
-    if (s.sel_cnt == 1) {  // the crossing bucket holds one item: find it
-      const uint64_t pf = s.sel_prefix, mk = s.sel_mask;
-      for (uint32_t i = tid; i < n; i += SIM_NT) {
-        uint64_t key;
-        uint32_t wi;
-        if (get(i, key, wi) && (key & mk) == pf) s.sel_k = key;
-      }
-      __syncthreads();
-      break;
-    }
-    hi = lo;
-    pb ^= 1;
-  }
-}
-
 struct Ctx {
   const SimParams& p;
   SimShm& s;
@@ -403,16 +308,16 @@ __device__ void run_instance(const SimParams& p, SimShm& s, uint64_t* Ksm, uint3
     // ---- S6/S7 order + admission: weighted select of the prefix ---------------
     const long long B = s.B;
     if (B > 0) {
-      wselect(s, na, (uint64_t)B, KBITS, [&](uint32_t i, uint64_t& key, uint32_t& w) {
+      wselect<SIM_NT>(s.sel, na, (uint64_t)B, KBITS, [&](uint32_t i, uint64_t& key, uint32_t& w) {
         key = K[i]; w = W[i]; return true; });
     } else {
       __syncthreads();
-      if (tid == 0) { s.sel_found = 1; s.sel_k = 0; s.sel_wbelow = 0; }  // nothing admitted
+      if (tid == 0) { s.sel.found = 1; s.sel.k = 0; s.sel.wbelow = 0; }  // nothing admitted
       __syncthreads();
     }
-    const bool found = s.sel_found != 0;
-    const uint64_t kstar = B > 0 ? s.sel_k : 0;
-    const uint64_t wb = s.sel_wbelow;
+    const bool found = s.sel.found != 0;
+    const uint64_t kstar = B > 0 ? s.sel.k : 0;
+    const uint64_t wb = s.sel.wbelow;
     auto grant = [&](uint64_t Ki, uint32_t dem) -> uint32_t {
       if (Ki & KEVICT) return 0u;
       if (B <= 0) return 0u;
@@ -421,7 +326,7 @@ __device__ void run_instance(const SimParams& p, SimShm& s, uint64_t* Ksm, uint3
       return 0u;
     };
     if (tid == 0) {
-      s.need = found ? (B > 0 ? B : 0) : (long long)s.sel_total;
+      s.need = found ? (B > 0 ? B : 0) : (long long)s.sel.total;
       s.freev = cap - s.A - s.P;
       s.freed = 0;
     }
@@ -439,10 +344,10 @@ __device__ void run_instance(const SimParams& p, SimShm& s, uint64_t* Ksm, uint3
         w = (uint32_t)kv;
         return true;
       };
-      wselect(s, npz, D0, 48, getp);
+      wselect<SIM_NT>(s.sel, npz, D0, 48, getp);
       {
-        const bool f0 = s.sel_found != 0;
-        const uint64_t k0 = s.sel_k;
+        const bool f0 = s.sel.found != 0;
+        const uint64_t k0 = s.sel.k;
         for (uint32_t i = tid; i < npz; i += SIM_NT) {
           uint64_t key; uint32_t w;
           if (getp(i, key, w) && (!f0 || key <= k0)) {
@@ -470,9 +375,9 @@ __device__ void run_instance(const SimParams& p, SimShm& s, uint64_t* Ksm, uint3
           key = KMASK - K[i];
           return w > 0;
         };
-        wselect(s, na, D1, KBITS, gete);
-        const bool f1 = s.sel_found != 0;
-        const uint64_t k1 = s.sel_k;
+        wselect<SIM_NT>(s.sel, na, D1, KBITS, gete);
+        const bool f1 = s.sel.found != 0;
+        const uint64_t k1 = s.sel.k;
         for (uint32_t i = tid; i < na; i += SIM_NT) {
           uint64_t key; uint32_t w;
           if (gete(i, key, w) && (!f1 || key <= k1)) {

@@ -1,14 +1,718 @@
+// augsched_step kernels (see step.cuh).  sm_100a, compiled with -fmad=false.
+#include <cuda_runtime.h>
+#include <cstdio>
 #include "step.cuh"
+#include "select.cuh"
+
 namespace augsched {
-int step_ensure(StepState& st, uint32_t n_inst, uint32_t max_active, cudaStream_t) {
-  st.n_inst = n_inst; st.max_active = max_active; return AUGSCHED_OK;
+
+namespace {
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr int SNT = 256;              // sort / per-instance kernels
+constexpr int SITEMS = 16;            // items per thread per sort tile
+constexpr int STILE = SNT * SITEMS;   // 4096 elements per tile
+constexpr int SW = SNT / 32;
+
+__device__ __forceinline__ void flag_err(uint32_t* e, uint32_t bits) { atomicOr(e, bits); }
+
+__device__ __forceinline__ long long ld_ll(const long long* p) { return *(volatile const long long*)p; }
+
+// ------------------------------------------------------------------ setup
+__global__ void coef_kernel(augsched_config cfg, const augsched_instance_params* ip, Coef* coef,
+                            uint32_t n) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) coef[i] = make_coef(cfg, ip[i]);
 }
-int step_enqueue(StepState&, uint32_t, const augsched_record_soa*, uint32_t, int, cudaStream_t, uint64_t*) {
-  return set_error(AUGSCHED_E_UNIMPLEMENTED, "step mode not built yet");
+
+// convert per-instance ids to global slot indices and validate kinds/ids
+__global__ void rec_fix_kernel(const uint32_t* kind, uint32_t* id, uint32_t n, uint32_t inst,
+                               uint32_t MA, uint32_t* err) {
+  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const uint32_t k = kind[j], x = id[j];
+  if (k < AUGSCHED_K_NEW || k > AUGSCHED_K_IMPORT || x >= MA) {
+    flag_err(err, 1u);
+    id[j] = 0xffffffffu;
+    return;
+  }
+  id[j] = inst * MA + x;
 }
-int step_run(StepState&, const augsched_config&, int64_t, const augsched_instance_params*, uint32_t*,
-             uint64_t, augsched_step_out*, cudaStream_t, uint64_t*) {
-  return set_error(AUGSCHED_E_UNIMPLEMENTED, "step mode not built yet");
+
+struct Rec {
+  const uint32_t *kind, *id, *la, *lb, *lc, *flags, *last, *ctx, *kv, *cpu, *pend;
+  const float* ta;
+};
+
+struct Slots {
+  uint32_t* st;
+  double* V;
+  uint32_t* last;
+  int32_t *ctx, *kv, *cpu, *pend;
+  long long *A, *P, *Aevt, *Asnap;
+  const Coef* coef;
+  const augsched_instance_params* ip;
+  uint32_t MA;
+};
+
+__device__ __forceinline__ void ledger_add(long long* x, long long d) {
+  atomicAdd(reinterpret_cast<unsigned long long*>(x), (unsigned long long)d);
 }
-void step_free(StepState&) {}
+
+// engine events of the previous forward: CALL (issue, S~ by Eq.4-8 with the
+// actual context, R13) and FINISH
+__global__ void rec_phaseA(Rec r, uint32_t n, Slots S, uint32_t* err) {
+  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const uint32_t k = r.kind[j], g = r.id[j];
+  if (g == 0xffffffffu || (k != AUGSCHED_K_CALL && k != AUGSCHED_K_FINISH)) return;
+  const uint32_t inst = g / S.MA;
+  const uint32_t st = S.st[g] & 15;
+  if (k == AUGSCHED_K_FINISH) {
+    if (st < ST_RUN || st > ST_WAIT) { flag_err(err, 1u); return; }
+    ledger_add(&S.A[inst], -(long long)S.kv[g]);
+    S.st[g] = ST_NONE; S.kv[g] = 0; S.ctx[g] = 0; S.cpu[g] = 0; S.pend[g] = 0;
+    return;
+  }
+  const int32_t ctx = S.ctx[g], kv = S.kv[g];
+  if (st != ST_RUN || S.cpu[g] != 0 || kv != ctx || S.pend[g] != 0) { flag_err(err, 1u); return; }
+  const Coef& c = S.coef[inst];
+  const int pol = select_policy(c, (uint64_t)ctx, (double)r.ta[j],
+                                (uint64_t)(S.Aevt[inst] - (long long)kv), S.ip[inst].policy_mode);
+  ledger_add(&S.A[inst], -(long long)kv);
+  if (pol == POL_P) ledger_add(&S.P[inst], kv);
+  else if (pol == POL_S) { S.cpu[g] = ctx; S.kv[g] = 0; }
+  else S.kv[g] = 0;
+  S.st[g] = ST_PAUSED | ((uint32_t)pol << 4);
+}
+
+__global__ void snap_kernel(const long long* A, long long* Asnap, uint32_t n) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) Asnap[i] = A[i];
+}
+
+// RETURN (Stage II + final value, routing), NEW (Stage I), IMPORT (restore)
+__global__ void rec_phaseBC(Rec r, uint32_t n, Slots S, uint64_t now, uint32_t* err) {
+  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const uint32_t k = r.kind[j], g = r.id[j];
+  if (g == 0xffffffffu || k == AUGSCHED_K_CALL || k == AUGSCHED_K_FINISH) return;
+  const uint32_t inst = g / S.MA;
+  const Coef& c = S.coef[inst];
+  const uint32_t pm = S.ip[inst].policy_mode;
+  const uint64_t Asnap = (uint64_t)S.Asnap[inst];
+  const uint32_t stv = S.st[g] & 15;
+  const bool flag1 = (r.flags[j] & 1u) != 0;
+  if (k == AUGSCHED_K_RETURN) {
+    if (stv != ST_PAUSED) { flag_err(err, 1u); return; }
+    const int pol = (int)((S.st[g] >> 4) & 3);
+    const int32_t kv = S.kv[g];
+    S.V[g] = intake_stage2(c, pm, pol, (uint64_t)S.ctx[g], r.la[j], r.lb[j], (double)r.ta[j], flag1, Asnap);
+    uint32_t ns;
+    if (pol == POL_P) { ns = ST_RUN; ledger_add(&S.P[inst], -(long long)kv); ledger_add(&S.A[inst], kv); }
+    else if (pol == POL_S) ns = ST_SWAP;
+    else ns = ST_WAIT;
+    S.pend[g] = (int32_t)r.la[j];
+    S.st[g] = ns | ((uint32_t)pol << 4);
+    return;
+  }
+  if (stv != ST_NONE) { flag_err(err, 1u); return; }
+  if (k == AUGSCHED_K_NEW) {
+    S.V[g] = intake_stage1(c, pm, r.la[j], r.lb[j], (double)r.ta[j], flag1, Asnap);
+    S.st[g] = ST_WAIT | ((uint32_t)POL_D << 4);
+    S.ctx[g] = 0; S.kv[g] = 0; S.cpu[g] = 0; S.pend[g] = (int32_t)r.la[j];
+    S.last[g] = (uint32_t)now;
+    return;
+  }
+  // IMPORT
+  const uint32_t f = r.flags[j];
+  const uint32_t ns = (f >> 4) & 7, pol = (f >> 8) & 3;
+  const bool st2 = (f >> 12) & 1;
+  if (ns < ST_RUN || ns > ST_PAUSED || pol > 2) { flag_err(err, 1u); return; }
+  S.V[g] = st2 ? intake_stage2(c, pm, (int)pol, r.la[j], r.lb[j], r.lc[j], (double)r.ta[j], flag1, Asnap)
+               : intake_stage1(c, pm, r.la[j], r.lb[j], (double)r.ta[j], flag1, Asnap);
+  S.st[g] = ns | (pol << 4);
+  S.last[g] = r.last[j];
+  S.ctx[g] = (int32_t)r.ctx[j]; S.kv[g] = (int32_t)r.kv[j]; S.cpu[g] = (int32_t)r.cpu[j];
+  S.pend[g] = (int32_t)r.pend[j];
+  if (ns == ST_PAUSED && pol == POL_P) ledger_add(&S.P[inst], (long long)r.kv[j]);
+  else ledger_add(&S.A[inst], (long long)r.kv[j]);
+}
+
+// ------------------------------------------------------------------ keys
+struct KeyArgs {
+  Slots S;
+  augsched_config cfg;
+  int64_t cap;
+  uint64_t now;
+  uint32_t* k0;
+  uint32_t* v0;
+  uint32_t* ghist;
+  uint32_t* n_active;
+  long long* budget;
+  int npass;
+  PassDesc passes[STEP_MAX_PASS];
+  size_t N;
+};
+
+__device__ __forceinline__ int digit_of(uint32_t k, uint32_t v, const PassDesc& d, uint32_t MA) {
+  if (d.src == 0) return (int)((k >> d.shift) & 255u);
+  if (d.src == 1) return (int)(v >> 30);
+  return (int)((((v & 0x3FFFFFFFu) / MA) >> d.shift) & 255u);
+}
+
+// Score every slot (a4): key = orderable u32 of fp32(V - alpha*wait) for
+// queued slots (tier 0 running, 1 swapped, 2 waiting); empty / paused slots get
+// tier 3 and sort behind.  Payload = global slot | tier << 30.  Also the token
+// limit of each instance (a3) and the digit histograms of every sort pass.
+__global__ void __launch_bounds__(SNT) keys_kernel(KeyArgs a) {
+  __shared__ uint32_t h[STEP_MAX_PASS][256];
+  const int tid = threadIdx.x, lane = tid & 31;
+  for (int p = 0; p < a.npass; ++p) h[p][tid] = 0;
+  __syncthreads();
+  const uint32_t MA = a.S.MA;
+  for (size_t base = (size_t)blockIdx.x * SNT; base < a.N; base += (size_t)gridDim.x * SNT) {
+    const size_t s = base + tid;
+    bool valid = s < a.N;
+    uint32_t inst = 0, tier = 3, key = 0, v = 0;
+    if (valid) {
+      inst = (uint32_t)(s / MA);
+      const uint32_t stv = a.S.st[s] & 15;
+      tier = (stv >= ST_RUN && stv <= ST_WAIT) ? stv - ST_RUN : 3u;
+      if (tier < 3 && a.S.ip[inst].ranking != AUGSCHED_RANK_FCFS)
+        key = sched_key(a.S.coef[inst], a.S.V[s], a.now, a.S.last[s]);
+      v = (uint32_t)s | (tier << 30);
+      a.k0[s] = key;
+      a.v0[s] = v;
+      if (s % MA == 0)
+        a.budget[inst] = token_limit(a.cfg, a.S.coef[inst], a.S.ip[inst], a.cap,
+                                     ld_ll(&a.S.A[inst]), ld_ll(&a.S.P[inst]));
+    }
+    // queued count per instance (warp-aggregated)
+    const bool q = valid && tier < 3;
+    const int gi = q ? (int)inst : -1;
+    const unsigned peers = __match_any_sync(FULL, gi);
+    if (q && lane == __ffs(peers) - 1) atomicAdd(&a.n_active[inst], (unsigned)__popc(peers));
+    for (int p = 0; p < a.npass; ++p) {
+      const int d = valid ? digit_of(key, v, a.passes[p], MA) : -1;
+      const unsigned pe = __match_any_sync(FULL, d);
+      if (d >= 0 && lane == __ffs(pe) - 1) atomicAdd(&h[p][d], (unsigned)__popc(pe));
+    }
+  }
+  __syncthreads();
+  for (int p = 0; p < a.npass; ++p)
+    if (h[p][tid]) atomicAdd(&a.ghist[p * 256 + tid], h[p][tid]);
+}
+
+// ------------------------------------------------------------------ sort pass
+struct SortArgs {
+  const uint32_t* kin;
+  const uint32_t* vin;
+  uint32_t* kout;
+  uint32_t* vout;
+  size_t n;
+  PassDesc d;
+  uint32_t MA;
+  const uint32_t* ghist;        // this pass's 256 bins
+  unsigned long long* status;   // [tiles][256] look-back words
+  unsigned long long epoch;
+  uint32_t* tile_ctr;
+  int final_;                   // last pass: write order (local slot) and key
+  uint32_t* order;
+  uint32_t* keyout;
+};
+
+// One stable LSD counting-sort pass over an 8-bit digit.  Tile = 4,096
+// elements; each warp ranks its contiguous 512-element segment with
+// __match_any_sync and warp-private digit counters, one barrier combines
+// warps, and the tile's digit offsets come from a decoupled look-back over
+// preceding tiles (tile ids handed out in launch order by an atomic counter).
+__global__ void __launch_bounds__(SNT) sort_pass_kernel(SortArgs a) {
+  __shared__ uint32_t bin_off[256];
+  __shared__ uint32_t wcnt[SW][256];
+  __shared__ uint32_t tbase[256];
+  __shared__ uint32_t wtot[SW];
+  __shared__ uint32_t tile_s;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) tile_s = atomicAdd(a.tile_ctr, 1u);
+  for (int w = 0; w < SW; ++w) wcnt[w][tid] = 0;
+  // exclusive scan of the global digit histogram (256 bins, one per thread)
+  {
+    const uint32_t x = a.ghist[tid];
+    uint32_t inc = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(FULL, inc, o);
+      if (lane >= o) inc += y;
+    }
+    if (lane == 31) wtot[warp] = inc;
+    __syncthreads();
+    uint32_t wb = 0;
+    for (int w = 0; w < warp; ++w) wb += wtot[w];
+    bin_off[tid] = wb + inc - x;
+  }
+  const size_t tile = tile_s;
+  const size_t seg = tile * STILE + (size_t)warp * (32 * SITEMS);
+  uint32_t kk[SITEMS], vv[SITEMS], rk[SITEMS];
+  int dg[SITEMS];
+#pragma unroll
+  for (int r = 0; r < SITEMS; ++r) {
+    const size_t idx = seg + (size_t)r * 32 + lane;
+    if (idx < a.n) {
+      kk[r] = a.kin[idx];
+      vv[r] = a.vin[idx];
+      dg[r] = digit_of(kk[r], vv[r], a.d, a.MA);
+    } else {
+      kk[r] = 0; vv[r] = 0; dg[r] = -1;
+    }
+  }
+  __syncthreads();  // wcnt cleared, bin_off ready
+  const unsigned lt = (1u << lane) - 1;
+#pragma unroll
+  for (int r = 0; r < SITEMS; ++r) {
+    const unsigned peers = __match_any_sync(FULL, dg[r]);
+    if (dg[r] >= 0) {
+      rk[r] = wcnt[warp][dg[r]] + __popc(peers & lt);
+    }
+    __syncwarp();
+    if (dg[r] >= 0 && lane == __ffs(peers) - 1) wcnt[warp][dg[r]] += __popc(peers);
+    __syncwarp();
+  }
+  __syncthreads();
+  // per digit (thread tid): exclusive offsets of the warps, tile count
+  uint32_t cnt = 0;
+  for (int w = 0; w < SW; ++w) {
+    const uint32_t c = wcnt[w][tid];
+    wcnt[w][tid] = cnt;
+    cnt += c;
+  }
+  // decoupled look-back: flag 1 = tile aggregate, 2 = inclusive prefix
+  volatile unsigned long long* st = a.status;
+  const unsigned long long ep = a.epoch << 34;
+  if (tile == 0) {
+    st[tid] = ep | (2ull << 32) | cnt;
+    tbase[tid] = 0;
+  } else {
+    st[tile * 256 + tid] = ep | (1ull << 32) | cnt;
+    uint32_t excl = 0;
+    size_t t = tile - 1;
+    for (;;) {
+      const unsigned long long w = st[t * 256 + tid];
+      if ((w >> 34) != a.epoch) continue;
+      excl += (uint32_t)w;
+      if (((w >> 32) & 3ull) == 2ull) break;
+      --t;
+    }
+    tbase[tid] = excl;
+    st[tile * 256 + tid] = ep | (2ull << 32) | (excl + cnt);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < SITEMS; ++r) {
+    if (dg[r] < 0) continue;
+    const uint32_t d = (uint32_t)dg[r];
+    const size_t pos = (size_t)bin_off[d] + tbase[d] + wcnt[warp][d] + rk[r];
+    if (a.final_) {
+      const uint32_t gsl = vv[r] & 0x3FFFFFFFu;
+      a.order[pos] = gsl - (gsl / a.MA) * a.MA;
+      a.keyout[pos] = kk[r];
+    } else {
+      a.kout[pos] = kk[r];
+      a.vout[pos] = vv[r];
+    }
+  }
+}
+
+// ------------------------------------------------------------------ block scan helpers
+__device__ __forceinline__ unsigned long long block_incl_scan_u64(unsigned long long x,
+                                                                  unsigned long long* wsum,
+                                                                  unsigned long long* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned long long inc = x;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long y = __shfl_up_sync(FULL, inc, o);
+    if (lane >= o) inc += y;
+  }
+  if (lane == 31) wsum[warp] = inc;
+  __syncthreads();
+  unsigned long long base = 0, tot = 0;
+  for (int w = 0; w < SW; ++w) {
+    if (w < warp) base += wsum[w];
+    tot += wsum[w];
+  }
+  *total = tot;
+  __syncthreads();
+  return base + inc;
+}
+
+__device__ __forceinline__ uint32_t slot_demand(const Slots& S, uint32_t g, uint32_t s_in) {
+  return demand_of(S.ctx[g], S.kv[g], S.cpu[g], S.pend[g], s_in);
+}
+
+// a6: per instance, grants of the admitted prefix (P_{j-1} < B, partial last)
+__global__ void __launch_bounds__(SNT) admit_kernel(Slots S, augsched_config cfg, int64_t cap,
+                                                    const long long* budget, const uint32_t* n_active,
+                                                    const uint32_t* order, uint32_t* grant,
+                                                    uint32_t* admitted, long long* need, uint32_t* flag) {
+  __shared__ unsigned long long wsum[SW];
+  const uint32_t i = blockIdx.x;
+  const uint32_t MA = S.MA;
+  const size_t base = (size_t)i * MA;
+  const long long B = budget[i];
+  const uint32_t n = n_active[i];
+  unsigned long long Prun = 0, gsum = 0;
+  uint32_t adm = 0;
+  for (uint32_t j0 = 0; j0 < n && (long long)Prun < B; j0 += SNT) {
+    const uint32_t j = j0 + threadIdx.x;
+    unsigned long long d = 0;
+    if (j < n) d = slot_demand(S, (uint32_t)(base + order[base + j]), cfg.s_in);
+    unsigned long long tot;
+    const unsigned long long inc = block_incl_scan_u64(d, wsum, &tot);
+    const unsigned long long ex = Prun + inc - d;
+    if (j < n && (long long)ex < B) {
+      const unsigned long long g = d < (unsigned long long)B - ex ? d : (unsigned long long)B - ex;
+      grant[base + j] = (uint32_t)g;
+      gsum += g;
+    }
+    const uint32_t c = __syncthreads_count(j < n && (long long)ex < B);
+    adm += c;
+    Prun += tot;
+  }
+  // block-reduce the granted tokens
+  unsigned long long tot;
+  block_incl_scan_u64(gsum, wsum, &tot);
+  if (threadIdx.x == 0) {
+    admitted[i] = adm;
+    need[i] = (long long)tot;
+    const long long fr = cap - ld_ll(&S.A[i]) - ld_ll(&S.P[i]);
+    flag[i] = (long long)tot > fr ? 1u : 0u;
+  }
+}
+
+// a7 (rare): demote Preserve-paused KV (kv desc, slot asc), then evict from
+// the tail of the order over entries with kv + g > 0, until the grants fit.
+__global__ void __launch_bounds__(SNT) resolve_kernel(Slots S, int64_t cap, const uint32_t* n_active,
+                                                      const uint32_t* order, uint32_t* grant,
+                                                      const uint32_t* admitted, const long long* need,
+                                                      const uint32_t* flag) {
+  __shared__ SelShm sel;
+  __shared__ unsigned long long freed;
+  const uint32_t i = blockIdx.x;
+  if (!flag[i]) return;
+  const uint32_t MA = S.MA;
+  const size_t base = (size_t)i * MA;
+  const long long nd = need[i];
+  long long fr = cap - ld_ll(&S.A[i]) - ld_ll(&S.P[i]);
+  if (threadIdx.x == 0) freed = 0;
+  // (1) demotion
+  auto getp = [&](uint32_t x, uint64_t& key, uint32_t& w) {
+    const size_t g = base + x;
+    const uint32_t stv = S.st[g];
+    const int32_t kv = S.kv[g];
+    if ((stv & 15) != ST_PAUSED || ((stv >> 4) & 3) != POL_P || kv <= 0) return false;
+    key = ((uint64_t)(0xFFFFFFFFu - (uint32_t)kv) << 24) | x;
+    w = (uint32_t)kv;
+    return true;
+  };
+  wselect<SNT>(sel, MA, (uint64_t)(nd - fr), 56, getp);
+  {
+    const bool f0 = sel.found != 0;
+    const uint64_t k0 = sel.k;
+    for (uint32_t x = threadIdx.x; x < MA; x += SNT) {
+      uint64_t key;
+      uint32_t w;
+      if (getp(x, key, w) && (!f0 || key <= k0)) {
+        const size_t g = base + x;
+        atomicAdd(&freed, (unsigned long long)w);
+        S.kv[g] = 0;
+        S.st[g] = ST_PAUSED | ((uint32_t)POL_D << 4);
+      }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) ledger_add(&S.P[i], -(long long)freed);
+  fr += (long long)freed;
+  __syncthreads();
+  if (nd <= fr) return;
+  // (2) tail eviction
+  const uint32_t n = n_active[i], adm = admitted[i];
+  auto gete = [&](uint32_t j, uint64_t& key, uint32_t& w) {
+    const size_t g = base + order[base + j];
+    w = (uint32_t)S.kv[g] + (j < adm ? grant[base + j] : 0u);
+    key = (uint64_t)(n - 1 - j);
+    return w > 0;
+  };
+  wselect<SNT>(sel, n, (uint64_t)(nd - fr), 24, gete);
+  const bool f1 = sel.found != 0;
+  const uint64_t k1 = sel.k;
+  long long dA = 0;
+  for (uint32_t j = threadIdx.x; j < n; j += SNT) {
+    uint64_t key;
+    uint32_t w;
+    if (gete(j, key, w) && (!f1 || key <= k1)) {
+      const size_t g = base + order[base + j];
+      dA -= S.kv[g];
+      S.kv[g] = 0;
+      S.cpu[g] = 0;
+      S.st[g] = ST_WAIT | (S.st[g] & 0x30u);
+      if (j < adm) grant[base + j] = 0;
+    }
+  }
+  if (dA) ledger_add(&S.A[i], dA);
+}
+
+// S9 + token accounting of the granted batch (decode adds one token; the
+// engine reports segment ends with CALL / FINISH records).
+__global__ void __launch_bounds__(SNT) apply_kernel(Slots S, uint64_t now, const uint32_t* order,
+                                                    const uint32_t* grant, const uint32_t* admitted) {
+  __shared__ unsigned long long wsum[SW];
+  const uint32_t i = blockIdx.x;
+  const size_t base = (size_t)i * S.MA;
+  const uint32_t adm = admitted[i];
+  unsigned long long dA = 0;
+  for (uint32_t j = threadIdx.x; j < adm; j += SNT) {
+    const uint32_t gr = grant[base + j];
+    if (gr == 0) continue;
+    const size_t g = base + order[base + j];
+    int32_t ctx = S.ctx[g], kv = S.kv[g], cpu = S.cpu[g], pend = S.pend[g];
+    if (cpu > 0) { cpu -= (int32_t)gr; kv += (int32_t)gr; }
+    else if ((ctx - kv) + pend > 0) {
+      const int32_t rc = (int32_t)gr < ctx - kv ? (int32_t)gr : ctx - kv;
+      kv += rc;
+      const int32_t pp = (int32_t)gr - rc;
+      pend -= pp; ctx += pp; kv += pp;
+    } else { ctx += 1; kv += 1; }
+    dA += gr;
+    S.ctx[g] = ctx; S.kv[g] = kv; S.cpu[g] = cpu; S.pend[g] = pend;
+    S.last[g] = (uint32_t)now;
+    S.st[g] = ST_RUN | (S.st[g] & 0x30u);
+  }
+  unsigned long long tot;
+  block_incl_scan_u64(dA, wsum, &tot);
+  if (threadIdx.x == 0) {
+    const long long a = ld_ll(&S.A[i]) + (long long)tot;
+    S.A[i] = a;
+    S.Aevt[i] = a;
+  }
+}
+
+}  // namespace
+
+// ====================================================================== host
+namespace {
+
+template <class T>
+int salloc(StepState& st, T** p, size_t n) {
+  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(p), (n ? n : 1) * sizeof(T));
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return set_error(e == cudaErrorMemoryAllocation ? AUGSCHED_E_OOM : AUGSCHED_E_CUDA,
+                     "step: device allocation failed");
+  }
+  st.alloc_list[st.n_alloc++] = *p;
+  return AUGSCHED_OK;
+}
+
+int cuda_check(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return AUGSCHED_OK;
+  char buf[256];
+  snprintf(buf, sizeof(buf), "%s: %s", what, cudaGetErrorString(e));
+  return set_error(AUGSCHED_E_CUDA, buf);
+}
+
+int grow_records(StepState& st, uint32_t need, cudaStream_t s) {
+  if (need <= st.r_cap) return AUGSCHED_OK;
+  uint32_t cap = st.r_cap ? st.r_cap : 1024;
+  while (cap < need) cap *= 2;
+  uint32_t** u[] = {&st.r_kind, &st.r_id, &st.r_la, &st.r_lb, &st.r_lc, &st.r_flags, &st.r_last,
+                    &st.r_ctx, &st.r_kv, &st.r_cpu, &st.r_pend};
+  for (auto pp : u) {
+    uint32_t* np = nullptr;
+    if (cudaMalloc(&np, sizeof(uint32_t) * cap) != cudaSuccess) {
+      cudaGetLastError();
+      return set_error(AUGSCHED_E_OOM, "step: record buffer allocation failed");
+    }
+    if (*pp) {
+      cudaMemcpyAsync(np, *pp, sizeof(uint32_t) * st.r_n, cudaMemcpyDeviceToDevice, s);
+      cudaStreamSynchronize(s);
+      cudaFree(*pp);
+    }
+    *pp = np;
+  }
+  float* nt = nullptr;
+  if (cudaMalloc(&nt, sizeof(float) * cap) != cudaSuccess) {
+    cudaGetLastError();
+    return set_error(AUGSCHED_E_OOM, "step: record buffer allocation failed");
+  }
+  if (st.r_ta) {
+    cudaMemcpyAsync(nt, st.r_ta, sizeof(float) * st.r_n, cudaMemcpyDeviceToDevice, s);
+    cudaStreamSynchronize(s);
+    cudaFree(st.r_ta);
+  }
+  st.r_ta = nt;
+  st.r_cap = cap;
+  return AUGSCHED_OK;
+}
+
+Slots slots_of(StepState& st, const augsched_instance_params* d_ip) {
+  return Slots{st.st, st.V, st.last, st.ctx, st.kv, st.cpu, st.pend, st.A, st.P, st.Aevt, st.Asnap,
+               st.coef, d_ip, st.max_active};
+}
+
+}  // namespace
+
+int step_ensure(StepState& st, uint32_t n_inst, uint32_t max_active, cudaStream_t s,
+                const augsched_config& cfg, const augsched_instance_params* d_ip, uint64_t* launches) {
+  if (st.ready) return AUGSCHED_OK;
+  const size_t N = (size_t)n_inst * max_active;
+  if (N >= (1ull << 30)) return set_error(AUGSCHED_E_CAPACITY, "step: n_instances * max_active must be < 2^30");
+  if (max_active >= (1u << 24)) return set_error(AUGSCHED_E_CAPACITY, "step: max_active must be < 2^24");
+  st.n_inst = n_inst;
+  st.max_active = max_active;
+  st.N = N;
+  st.n_tiles = (uint32_t)((N + STILE - 1) / STILE);
+  int rc;
+  if ((rc = salloc(st, &st.st, N)) || (rc = salloc(st, &st.V, N)) || (rc = salloc(st, &st.last, N)) ||
+      (rc = salloc(st, &st.ctx, N)) || (rc = salloc(st, &st.kv, N)) || (rc = salloc(st, &st.cpu, N)) ||
+      (rc = salloc(st, &st.pend, N)) || (rc = salloc(st, &st.A, n_inst)) ||
+      (rc = salloc(st, &st.P, n_inst)) || (rc = salloc(st, &st.Aevt, n_inst)) ||
+      (rc = salloc(st, &st.Asnap, n_inst)) || (rc = salloc(st, &st.need, n_inst)) ||
+      (rc = salloc(st, &st.coef, n_inst)) || (rc = salloc(st, &st.budget, n_inst)) ||
+      (rc = salloc(st, &st.n_active, n_inst)) || (rc = salloc(st, &st.admitted, n_inst)) ||
+      (rc = salloc(st, &st.flag, n_inst)) || (rc = salloc(st, &st.order, N)) ||
+      (rc = salloc(st, &st.grant, N)) || (rc = salloc(st, &st.key, N)) ||
+      (rc = salloc(st, &st.k0, N)) || (rc = salloc(st, &st.v0, N)) || (rc = salloc(st, &st.k1, N)) ||
+      (rc = salloc(st, &st.v1, N)) ||
+      (rc = salloc(st, &st.lb_status, (size_t)st.n_tiles * 256)) ||
+      (rc = salloc(st, &st.ghist, STEP_MAX_PASS * 256)) ||
+      (rc = salloc(st, &st.tile_ctr, STEP_MAX_PASS)))
+    return rc;
+  cudaMemsetAsync(st.st, 0, sizeof(uint32_t) * N, s);
+  cudaMemsetAsync(st.ctx, 0, sizeof(int32_t) * N, s);
+  cudaMemsetAsync(st.kv, 0, sizeof(int32_t) * N, s);
+  cudaMemsetAsync(st.cpu, 0, sizeof(int32_t) * N, s);
+  cudaMemsetAsync(st.pend, 0, sizeof(int32_t) * N, s);
+  cudaMemsetAsync(st.A, 0, sizeof(long long) * n_inst, s);
+  cudaMemsetAsync(st.P, 0, sizeof(long long) * n_inst, s);
+  cudaMemsetAsync(st.Aevt, 0, sizeof(long long) * n_inst, s);
+  cudaMemsetAsync(st.lb_status, 0, sizeof(unsigned long long) * st.n_tiles * 256, s);
+  coef_kernel<<<(n_inst + 255) / 256, 256, 0, s>>>(cfg, d_ip, st.coef, n_inst);
+  *launches += 1;
+  // digit passes: 4 key bytes, the tier, then the instance bytes (LSD)
+  st.npass = 0;
+  for (int b = 0; b < 4; ++b) st.passes[st.npass++] = PassDesc{0, 8 * b};
+  st.passes[st.npass++] = PassDesc{1, 0};
+  for (uint32_t x = n_inst - 1, b = 0; x > 0; x >>= 8, ++b) st.passes[st.npass++] = PassDesc{2, (int)(8 * b)};
+  st.epoch = 0;
+  st.ready = true;
+  return cuda_check(cudaGetLastError(), "step_ensure");
+}
+
+int step_enqueue(StepState& st, uint32_t inst, const augsched_record_soa* r, uint32_t n, int on_dev,
+                 cudaStream_t s, uint32_t* d_err, uint64_t* launches) {
+  if (n == 0) return AUGSCHED_OK;
+  if ((uint64_t)st.r_n + n > 4ull * st.N + 1024)
+    return set_error(AUGSCHED_E_CAPACITY, "enqueue: too many pending records");
+  const void* srcs[] = {r->kind, r->id, r->la, r->lb, r->lc, r->flags, r->last, r->ctx, r->kv, r->cpu,
+                        r->pend, r->ta};
+  for (const void* p : srcs)
+    if (!p) return set_error(AUGSCHED_E_INVALID, "enqueue: every record column must be non-NULL");
+  if (!on_dev) {
+    for (uint32_t j = 0; j < n; ++j)
+      if (r->kind[j] < AUGSCHED_K_NEW || r->kind[j] > AUGSCHED_K_IMPORT || r->id[j] >= st.max_active)
+        return set_error(AUGSCHED_E_INVALID, "enqueue: bad record kind or id");
+  }
+  int rc = grow_records(st, st.r_n + n, s);
+  if (rc) return rc;
+  const cudaMemcpyKind kind = on_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  uint32_t* dst[] = {st.r_kind, st.r_id, st.r_la, st.r_lb, st.r_lc, st.r_flags, st.r_last, st.r_ctx,
+                     st.r_kv, st.r_cpu, st.r_pend};
+  for (int c = 0; c < 11; ++c) {
+    cudaError_t e = cudaMemcpyAsync(dst[c] + st.r_n, srcs[c], sizeof(uint32_t) * n, kind, s);
+    if (e != cudaSuccess) return cuda_check(e, "enqueue copy");
+  }
+  cudaError_t e = cudaMemcpyAsync(st.r_ta + st.r_n, r->ta, sizeof(float) * n, kind, s);
+  if (e != cudaSuccess) return cuda_check(e, "enqueue copy");
+  rec_fix_kernel<<<(n + 255) / 256, 256, 0, s>>>(st.r_kind + st.r_n, st.r_id + st.r_n, n, inst,
+                                                 st.max_active, d_err);
+  *launches += 1;
+  st.r_n += n;
+  if (!on_dev) {
+    // host arrays must be consumed before returning (pageable copies are
+    // staged by the driver; a pinned source would not be)
+    e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return cuda_check(e, "enqueue sync");
+  }
+  return cuda_check(cudaGetLastError(), "enqueue");
+}
+
+int step_run(StepState& st, const augsched_config& cfg, int64_t cap,
+             const augsched_instance_params* d_ip, uint32_t* d_err, uint64_t now,
+             augsched_step_out* out, cudaStream_t s, uint64_t* launches) {
+  Slots S = slots_of(st, d_ip);
+  const uint32_t ni = st.n_inst;
+  if (st.r_n) {
+    Rec r{st.r_kind, st.r_id, st.r_la, st.r_lb, st.r_lc, st.r_flags, st.r_last, st.r_ctx, st.r_kv,
+          st.r_cpu, st.r_pend, st.r_ta};
+    const uint32_t g = (st.r_n + 255) / 256;
+    rec_phaseA<<<g, 256, 0, s>>>(r, st.r_n, S, d_err);
+    snap_kernel<<<(ni + 255) / 256, 256, 0, s>>>(st.A, st.Asnap, ni);
+    rec_phaseBC<<<g, 256, 0, s>>>(r, st.r_n, S, now, d_err);
+    *launches += 3;
+    st.r_n = 0;
+  }
+  cudaMemsetAsync(st.n_active, 0, sizeof(uint32_t) * ni, s);
+  cudaMemsetAsync(st.ghist, 0, sizeof(uint32_t) * STEP_MAX_PASS * 256, s);
+  cudaMemsetAsync(st.tile_ctr, 0, sizeof(uint32_t) * STEP_MAX_PASS, s);
+  KeyArgs ka;
+  ka.S = S; ka.cfg = cfg; ka.cap = cap; ka.now = now; ka.k0 = st.k0; ka.v0 = st.v0;
+  ka.ghist = st.ghist; ka.n_active = st.n_active; ka.budget = st.budget; ka.npass = st.npass;
+  for (int p = 0; p < st.npass; ++p) ka.passes[p] = st.passes[p];
+  ka.N = st.N;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const size_t kblocks = (st.N + SNT - 1) / SNT;
+  const int kgrid = (int)(kblocks < (size_t)sms * 8 ? kblocks : (size_t)sms * 8);
+  keys_kernel<<<kgrid, SNT, 0, s>>>(ka);
+  *launches += 1;
+  uint32_t *kin = st.k0, *vin = st.v0, *kout = st.k1, *vout = st.v1;
+  for (int p = 0; p < st.npass; ++p) {
+    SortArgs sa;
+    sa.kin = kin; sa.vin = vin; sa.kout = kout; sa.vout = vout; sa.n = st.N; sa.d = st.passes[p];
+    sa.MA = st.max_active; sa.ghist = st.ghist + p * 256; sa.status = st.lb_status;
+    sa.epoch = ++st.epoch; sa.tile_ctr = st.tile_ctr + p; sa.final_ = p == st.npass - 1;
+    sa.order = st.order; sa.keyout = st.key;
+    sort_pass_kernel<<<st.n_tiles, SNT, 0, s>>>(sa);
+    *launches += 1;
+    uint32_t* t = kin; kin = kout; kout = t;
+    t = vin; vin = vout; vout = t;
+  }
+  admit_kernel<<<ni, SNT, 0, s>>>(S, cfg, cap, st.budget, st.n_active, st.order, st.grant,
+                                  st.admitted, st.need, st.flag);
+  resolve_kernel<<<ni, SNT, 0, s>>>(S, cap, st.n_active, st.order, st.grant, st.admitted, st.need,
+                                    st.flag);
+  apply_kernel<<<ni, SNT, 0, s>>>(S, now, st.order, st.grant, st.admitted);
+  *launches += 3;
+  out->budget = reinterpret_cast<const int64_t*>(st.budget);
+  out->n_active = st.n_active;
+  out->admitted = st.admitted;
+  out->order = st.order;
+  out->grant = st.grant;
+  out->key = st.key;
+  return cuda_check(cudaGetLastError(), "step");
+}
+
+void step_free(StepState& st) {
+  for (int i = 0; i < st.n_alloc; ++i) cudaFree(st.alloc_list[i]);
+  st.n_alloc = 0;
+  uint32_t* u[] = {st.r_kind, st.r_id, st.r_la, st.r_lb, st.r_lc, st.r_flags, st.r_last, st.r_ctx,
+                   st.r_kv, st.r_cpu, st.r_pend};
+  for (auto p : u)
+    if (p) cudaFree(p);
+  if (st.r_ta) cudaFree(st.r_ta);
+  st = StepState();
+}
+
 }  // namespace augsched

@@ -1,0 +1,129 @@
+"""GPU parity of augsched_step (record intake, keys, device-wide LSD radix
+sort, admission, resolution, grant accounting) against the oracle's step
+mode: token limits, queue sizes, the full order, every key and every grant
+must be identical, step after step."""
+import numpy as np
+import pytest
+
+import oracle
+import tracegen
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_2512_04013_b200 as aug  # noqa: E402
+
+
+def compare(g, o, n_inst, label):
+    assert np.array_equal(g["B"], o["B"]), f"{label}: budget {g['B'][:4]} vs {o['B'][:4]}"
+    assert np.array_equal(g["n_active"], o["n_active"]), f"{label}: n_active"
+    assert np.array_equal(g["admitted"], o["admitted"]), f"{label}: admitted {g['admitted']} vs {o['admitted']}"
+    for i in range(n_inst):
+        n, a = int(o["n_active"][i]), int(o["admitted"][i])
+        assert np.array_equal(g["order"][i, :n], o["order"][i, :n]), f"{label}: order inst {i}"
+        assert np.array_equal(g["keys"][i, :n], o["keys"][i, :n]), f"{label}: keys inst {i}"
+        assert np.array_equal(g["grant"][i, :a], o["grant"][i, :a]), f"{label}: grant inst {i}"
+        assert not o["grant"][i, a:n].any()
+
+
+def test_G3_gpu():
+    cfg = dict(tracegen.PRESET_G0, g_total=1000 + 10**6, g_model=1000)
+    for rk in (0, 1):
+        ip = tracegen.inst_params(1, base=tracegen.INST_G0, l_static=100, ranking=rk)
+        rec = oracle.records(4, kind=oracle.K_NEW, id=[0, 1, 2, 3], la=[100, 20, 100, 20],
+                             lb=[10, 10, 10, 10], ta=[0.0, 0.0, 2.0, 0.0], flags=[0, 0, 1, 1])
+        st = oracle.Step(cfg, ip, 4)
+        st.enqueue(0, rec)
+        o = st.step(0)
+        s = aug.Scheduler(cfg, ip, 1, 4)
+        s.enqueue(0, rec)
+        g = s.step_result(s.step(0))
+        s.close()
+        compare(g, o, 1, f"G3 ranking {rk}")
+        want = [1, 3, 0, 2] if rk == 0 else [0, 1, 2, 3]
+        assert list(g["order"][0]) == want
+
+
+def random_events(rng, slots, now, p_new=0.3):
+    """Valid engine events for one instance given its slot states."""
+    recs = []
+    for j, (stv, pol, ctx, kv, cpu, pend) in enumerate(slots):
+        u = rng.random()
+        if stv == 0 and u < p_new:
+            recs.append(dict(kind=oracle.K_NEW, id=j, la=int(rng.integers(1, 300)),
+                             lb=int(rng.integers(1, 80)), ta=float(rng.choice([0.0, 0.05, 1.0, 8.0])),
+                             flags=int(rng.integers(0, 2))))
+        elif stv == 1 and cpu == 0 and kv == ctx and pend == 0 and u < 0.3:
+            if rng.random() < 0.6:
+                recs.append(dict(kind=oracle.K_CALL, id=j, ta=float(rng.choice([0.0, 0.2, 3.0]))))
+            else:
+                recs.append(dict(kind=oracle.K_FINISH, id=j))
+        elif stv == 4 and u < 0.35:
+            recs.append(dict(kind=oracle.K_RETURN, id=j, la=int(rng.integers(1, 120)),
+                             lb=int(rng.integers(1, 60)), ta=float(rng.choice([0.0, 0.5, 4.0])),
+                             flags=int(rng.integers(0, 2))))
+        elif stv in (2, 3) and u < 0.02:
+            recs.append(dict(kind=oracle.K_FINISH, id=j))
+    if not recs:
+        return None
+    cols = {k: [r.get(k, 0) for r in recs] for k in oracle.REC_FIELDS}
+    return oracle.records(len(recs), **cols)
+
+
+@pytest.mark.parametrize("seed,cap", [(1, 10**6), (2, 900), (3, 400)])
+def test_random_event_stream(seed, cap):
+    """3 instances x 64 slots, 40 steps of random NEW/CALL/RETURN/FINISH
+    events; small caps force demotion and tail eviction every few steps."""
+    rng = np.random.default_rng(seed)
+    n_inst, MA = 3, 64
+    cfg = dict(tracegen.PRESET_G0, g_total=1000 + cap, g_model=1000)
+    ip = tracegen.inst_params(n_inst, base=tracegen.INST_G0, ranking=[0, 1, 0], budget_mode=[1, 0, 0],
+                              l_static=150, target_max=[50, 200, 120], alpha=[0.0, 0.0, 3.0],
+                              policy_mode=[0, 0, 0])
+    st = oracle.Step(cfg, ip, MA)
+    s = aug.Scheduler(cfg, ip, n_inst, MA)
+    for t in range(40):
+        for i in range(n_inst):
+            rec = random_events(rng, st.slots(i), t)
+            if rec is not None:
+                assert st.enqueue(i, rec) == 0
+                s.enqueue(i, rec)
+        o = st.step(t)
+        assert o["rc"] == 0
+        g = s.step_result(s.step(t))
+        compare(g, o, n_inst, f"seed {seed} step {t}")
+    s.close()
+
+
+def test_state_violation_is_reported():
+    cfg = dict(tracegen.PRESET_G0)
+    ip = tracegen.inst_params(1, base=tracegen.INST_G0)
+    s = aug.Scheduler(cfg, ip, 1, 8)
+    s.enqueue(0, oracle.records(1, kind=oracle.K_RETURN, id=[3], la=[5], lb=[5]))  # slot 3 not paused
+    s.step(0)
+    with pytest.raises(aug.AugschedError) as e:
+        s.sync()
+    assert e.value.code == aug.E_STATE
+    s.close()
+
+
+def test_cfg4_one_million_queue():
+    """Config 4: one queue of 1,000,000 requests (512 running, 512 swapped,
+    waiting 80% Stage I / 20% Stage II), 3 consecutive steps, full order."""
+    n = 1_000_000
+    rec = tracegen.cfg4_records(n)
+    cfg = tracegen.PRESET_CFG4
+    ip = tracegen.inst_params(1)
+    st = oracle.Step(cfg, ip, n)
+    assert st.enqueue(0, rec) == 0
+    s = aug.Scheduler(cfg, ip, 1, n)
+    s.enqueue(0, rec)
+    t0 = 65536
+    for k in range(3):
+        o = st.step(t0 + k)
+        g = s.step_result(s.step(t0 + k))
+        compare(g, o, 1, f"cfg4 step {k}")
+        assert int(g["B"][0]) == 750 and int(g["n_active"][0]) == n - 16
+    s.close()

@@ -339,3 +339,63 @@ def cfg5_params(n_inst: int = 65536):
 
 def cfg5_trace_ids(n_inst: int = 65536):
     return (np.arange(n_inst) // 16).astype(np.uint32)
+
+
+# --------------------------------------------------------------------------
+# Config 4: one huge queue, as IMPORT records of augsched_step (input state)
+# --------------------------------------------------------------------------
+
+# Ample KV memory for the 1M-request queue (cap ~ 2.2e9 tokens), so the
+# limit stays at the clamp hi = 1.5 * 500 = 750 over the benchmark's steps.
+PRESET_CFG4 = dict(PRESET_7B, g_total=2**60)
+
+K_IMPORT = 5
+ST_RUN, ST_SWAP, ST_WAIT, ST_PAUSED = 1, 2, 3, 4
+POL_P, POL_S, POL_D = 0, 1, 2
+
+
+def cfg4_records(n: int = 1_000_000, seed: int = 4, t0: int = 65536, n_running: int = 512,
+                 n_swapped: int = 512, n_paused: int = 16, stage2_share: float = 0.2) -> dict:
+    """SoA IMPORT records for a single queue of n slots:
+    `n_running` running (Preserve returns, decode-ready: demand 1),
+    `n_swapped` swapped (Swap returns: swap-in pending), `n_paused`
+    Preserve-paused (hold the ledger's P), and waiting requests: 80% fresh
+    (Stage I, prefill pending) and 20% returned Discard (Stage II, recompute
+    + assimilation pending).  last = t0 - U{0..65535}.  Features come from
+    the W2 generator; the applied policies are assigned, not computed."""
+    rng = np.random.Generator(np.random.PCG64(np.random.SeedSequence([seed, 4])))
+    arr, lpre, nseg, gt, gp, dt, dp, ret = gen_trace_arrays(n, 4.0, seed, 0)
+    s0 = np.concatenate([[0], np.cumsum(nseg)[:-1]])
+    L = lpre.astype(np.int64)
+    g0, gp0, dp0, r0 = gt[s0].astype(np.int64), gp[s0], dp[s0], ret[s0].astype(np.int64)
+    has2 = nseg >= 2
+    gp1 = np.where(has2, gp[np.minimum(s0 + 1, len(gp) - 1)], 0)
+    dp1 = np.where(nseg >= 3, dp[np.minimum(s0 + 1, len(dp) - 1)], 0.0).astype(np.float32)
+    Lt = L + g0
+    kind = np.full(n, K_IMPORT, np.uint32)
+    status = np.full(n, ST_WAIT, np.int64)
+    pol = np.full(n, POL_D, np.int64)
+    stage2 = np.zeros(n, np.int64)
+    la, lb, lc = L.copy(), gp0.astype(np.int64), np.zeros(n, np.int64)
+    ta = dp0.astype(np.float32)
+    flag0 = (nseg > 1).astype(np.int64)
+    ctx = np.zeros(n, np.int64); kv = np.zeros(n, np.int64)
+    cpu = np.zeros(n, np.int64); pend = L.copy()
+    idx = rng.permutation(n)
+    a, b, c = n_running, n_running + n_swapped, n_running + n_swapped + n_paused
+    run, swp, psd, rest = idx[:a], idx[a:b], idx[b:c], idx[c:]
+    st2 = rest[rng.random(rest.shape[0]) < stage2_share]
+    for grp, st, pl in ((run, ST_RUN, POL_P), (swp, ST_SWAP, POL_S), (psd, ST_PAUSED, POL_P), (st2, ST_WAIT, POL_D)):
+        status[grp] = st; pol[grp] = pl; stage2[grp] = 1
+        la[grp], lb[grp], lc[grp] = Lt[grp], r0[grp], gp1[grp]
+        ta[grp] = dp1[grp]
+        flag0[grp] = (nseg[grp] >= 3).astype(np.int64)
+    ctx[run] = kv[run] = Lt[run] + r0[run]; pend[run] = 0
+    ctx[swp] = Lt[swp]; cpu[swp] = Lt[swp]; pend[swp] = r0[swp]
+    ctx[psd] = kv[psd] = Lt[psd]; pend[psd] = 0
+    ctx[st2] = Lt[st2]; pend[st2] = r0[st2]
+    last = t0 - rng.integers(0, 65536, n)
+    flags = flag0 | (status << 4) | (pol << 8) | (stage2 << 12)
+    u = lambda x: np.ascontiguousarray(x, np.uint32)
+    return dict(kind=kind, id=u(np.arange(n)), la=u(la), lb=u(lb), lc=u(lc), ta=np.ascontiguousarray(ta),
+                flags=u(flags), last=u(last), ctx=u(ctx), kv=u(kv), cpu=u(cpu), pend=u(pend))
