@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=0, help="oracle sample size (instances)")
+    ap.add_argument("--no-step", action="store_true", help="skip the cfg4 1M-queue step measurement")
+    ap.add_argument("--step-n", type=int, default=1_000_000)
     return ap.parse_args()
 
 
@@ -161,6 +163,48 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+# ----------------------------------------------------------------------------- cfg4 step
+def step_bench(args, dev, stream, peak):
+    """Config 4: augsched_step over one 1,000,000-request queue (scores, full
+    stable order, admission, grant accounting), K consecutive steps, each
+    timed with CUDA events after an L2 flush (working set ~60 MB < L2)."""
+    import torch
+    import paper_2512_04013_b200 as aug
+    n = args.step_n
+    rec = tracegen.cfg4_records(n)
+    s = aug.Scheduler(tracegen.PRESET_CFG4, tracegen.inst_params(1), 1, n, device=dev, stream=stream)
+    s.enqueue(0, rec)
+    flush = torch.empty(512 * 2**20, dtype=torch.uint8, device=f"cuda:{dev}")
+    t = 65536
+    for _ in range(args.warmup):
+        s.step(t); t += 1
+    torch.cuda.synchronize()
+    l0 = s.launches
+    cold, warm = [], []
+    for _ in range(args.steps):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream); s.step(t); b.record(stream); t += 1
+        torch.cuda.synchronize()
+        cold.append(a.elapsed_time(b))
+    for _ in range(args.steps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream); s.step(t); b.record(stream); t += 1
+        torch.cuda.synchronize()
+        warm.append(a.elapsed_time(b))
+    launches = (s.launches - l0) // (2 * args.steps)
+    s.close()
+    ms = float(np.median(cold))
+    ach = 32.0 * n / (ms / 1e3) / 1e9
+    return {"workload": f"cfg4: one queue of {n} requests (512 running, 512 swapped, rest waiting "
+                        "80% Stage I / 20% Stage II), full stable order + admission per step",
+            "value": n / (ms / 1e3), "unit": UNIT, "ms_per_step_cold_l2": ms,
+            "ms_per_step_warm_l2": float(np.median(warm)), "launches_per_step": launches,
+            "roofline": {"bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(ach / peak, 4), "traffic": None,
+                         "note": "whole step (keys + 5 sort passes + admit/resolve/apply), 32 B/decision"}}
+
+
 # ----------------------------------------------------------------------------- GPU arm
 def run_gpu(args):
     import torch
@@ -229,11 +273,12 @@ def run_gpu(args):
         dist.all_reduce(tm[1:], op=dist.ReduceOp.SUM)
         tm[0] = mx[0]
         # final NCCL all-gather of the per-instance result records (north star)
-        gathered = torch.empty(world * out.numel(), dtype=torch.uint8, device=out.device)
+        from paper_2512_04013_b200 import dist as adist
         g0 = time.perf_counter()
-        dist.all_gather_into_tensor(gathered, out)
+        gathered = adist.all_gather_records(out, world)
         torch.cuda.synchronize()
         gather_ms = 1e3 * (time.perf_counter() - g0)
+        assert gathered.numel() == world * out.numel()
     else:
         gather_ms = 0.0
     total_ms, dec_all, isteps_all = float(tm[0]), float(tm[1]), float(tm[2])
@@ -300,6 +345,8 @@ def run_gpu(args):
                        "h2d_bytes_per_step": pinned.nbytes + 4 * n_inst,
                        "d2h_bytes_per_step": n_inst * aug.RESULT_DTYPE.itemsize}
         s2.close()
+    if rank == 0 and not args.no_step:
+        line["step_1m"] = step_bench(args, dev, stream, peak)
     if rank == 0 and world == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline(args, tr, ip, tid, W * (args.warmup + args.steps),
                                             sample=args.cpu_sample or None)

@@ -18,19 +18,28 @@
 
 namespace augsched {
 
-struct SelShm {
+struct SelBins {
   unsigned long long wbin[2][256];
   unsigned int cbin[2][256];
   unsigned long long wkey[2][256];
+};
+
+struct SelRes {
   unsigned long long prefix, mask, wbelow, k, total;
   unsigned int cnt;
   int found, done;
 };
 
-// Results: s.found (0: total weight < D, s.total holds it), s.k = k*,
-// s.wbelow = sum of weights with key < k*.  Must be called by all NT threads.
+// convenience for kernels that only need one select
+struct SelShm {
+  SelBins b;
+  SelRes r;
+};
+
+// Results: r.found (0: total weight < D, r.total holds it), r.k = k*,
+// r.wbelow = sum of weights with key < k*.  Must be called by all NT threads.
 template <int NT, class Get>
-__device__ void wselect(SelShm& s, uint32_t n, uint64_t D, int nbits, Get get) {
+__device__ void wselect(SelBins& sb, SelRes& s, uint32_t n, uint64_t D, int nbits, Get get) {
   constexpr unsigned FULL = 0xffffffffu;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t Dc = (uint32_t)(D < (1ull << 26) ? D : (1ull << 26));
@@ -39,17 +48,17 @@ __device__ void wselect(SelShm& s, uint32_t n, uint64_t D, int nbits, Get get) {
     s.prefix = 0; s.mask = 0; s.wbelow = 0; s.found = 0; s.done = 0; s.total = 0; s.cnt = 0;
     s.k = 0;
   }
-  for (int b = tid; b < 256; b += NT) { s.wbin[0][b] = 0; s.cbin[0][b] = 0; }
+  for (int b = tid; b < 256; b += NT) { sb.wbin[0][b] = 0; sb.cbin[0][b] = 0; }
   __syncthreads();
   int hi = nbits, pb = 0;
   while (hi > 0) {
     const int lo = hi > 8 ? hi - 8 : 0;
     const uint32_t dmask = (1u << (hi - lo)) - 1;
     const uint64_t prefix = s.prefix, mask = s.mask;
-    unsigned long long* wbin = s.wbin[pb];
-    unsigned int* cbin = s.cbin[pb];
-    unsigned long long* wkey = s.wkey[pb];
-    for (int b = tid; b < 256; b += NT) { s.wbin[pb ^ 1][b] = 0; s.cbin[pb ^ 1][b] = 0; }
+    unsigned long long* wbin = sb.wbin[pb];
+    unsigned int* cbin = sb.cbin[pb];
+    unsigned long long* wkey = sb.wkey[pb];
+    for (int b = tid; b < 256; b += NT) { sb.wbin[pb ^ 1][b] = 0; sb.cbin[pb ^ 1][b] = 0; }
     for (uint32_t base = 0; base < n; base += NT) {
       const uint32_t i = base + tid;
       int dig = -1;
@@ -115,6 +124,67 @@ __device__ void wselect(SelShm& s, uint32_t n, uint64_t D, int nbits, Get get) {
     hi = lo;
     pb ^= 1;
   }
+}
+
+template <int NT, class Get>
+__device__ __forceinline__ void wselect(SelShm& s, uint32_t n, uint64_t D, int nbits, Get get) {
+  wselect<NT>(s.b, s.r, n, D, nbits, get);
+}
+
+// Small-candidate variant: m <= 256 (key, weight) pairs in shared memory.
+// Each candidate's rank is counted against all others (keys unique), pairs
+// are scattered to rank order, and one warp scans the weights for the
+// crossing.  Results in r as for wselect, with wbelow offset by w0 (the
+// weight of everything ordered before the candidate set).
+struct CandShm {
+  unsigned long long ck[2][256];
+  unsigned int cw[2][256];
+  unsigned long long rk[256];
+  unsigned int rw[256];
+};
+
+template <int NT>
+__device__ void rank_select(CandShm& c, int list, SelRes& r, int m, uint64_t D, uint64_t w0) {
+  constexpr unsigned FULL = 0xffffffffu;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const unsigned long long* ck = c.ck[list];
+  const unsigned int* cw = c.cw[list];
+  for (int a = tid; a < m; a += NT) {
+    const unsigned long long key = ck[a];
+    int rk = 0;
+    for (int j = 0; j < m; ++j) rk += ck[j] < key;
+    c.rk[rk] = key;
+    c.rw[rk] = cw[a];
+  }
+  __syncthreads();
+  if (tid < 32) {
+    unsigned long long run = w0;
+    int hit = -1;
+    unsigned long long wb = 0;
+    for (int q = 0; q < m; q += 32) {
+      const int j = q + lane;
+      const unsigned long long w = j < m ? c.rw[j] : 0ull;
+      unsigned long long inc = w;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long v = __shfl_up_sync(FULL, inc, o);
+        if (lane >= o) inc += v;
+      }
+      const unsigned bal = __ballot_sync(FULL, j < m && run + inc >= D);
+      if (bal) {
+        const int f = __ffs(bal) - 1;
+        hit = q + f;
+        wb = run + __shfl_sync(FULL, inc - w, f);
+        break;
+      }
+      run += __shfl_sync(FULL, inc, 31);
+    }
+    if (lane == 0) {
+      if (hit < 0) { r.found = 0; r.total = run; }
+      else { r.found = 1; r.k = c.rk[hit]; r.wbelow = wb; }
+    }
+  }
+  __syncthreads();
 }
 
 }  // namespace augsched

@@ -8,7 +8,16 @@
 namespace augsched {
 
 struct __align__(16) SimShm {
-  SelShm sel;
+  union {
+    SelBins b;                       // radix-select histograms (fallback path)
+    CandShm c;                       // small candidate lists (fast path)
+  } u;
+  SelRes res;
+  unsigned long long tw[3];          // per-tier demand (clamped to B) of the step
+  unsigned int tc[3];                // per-tier queue counts of the step
+  unsigned long long amin[2];        // argmin rounds over the waiting tier
+  unsigned int aw;
+  int due;                           // intake or idle handling needed this iteration
   unsigned int hist_t[AUGSCHED_NBIN];
   unsigned int hist_n[AUGSCHED_NBIN];
   unsigned long long cnt[AUGSCHED_R_NFIELD];
@@ -237,87 +246,170 @@ __device__ void run_instance(const SimParams& p, SimShm& s, uint64_t* Ksm, uint3
   if (tid == 0) s.cnt[AUGSCHED_R_NREQ] = n;
   const int64_t cap = p.cap;
 
+  // thread 0 prepares iteration s.t: stop rule, S1 snapshot, whether intake
+  // or the idle jump must run, and (when no intake is due) the token limit.
+  auto prep = [&]() {
+    s.run = (s.n_fin < n) && (s.t < p.max_iters);
+    s.tT = s.t * T;
+    s.A_snap = s.A;
+    s.n_holes = 0;
+    s.due = s.n_act == 0 || s.tT >= s.min_ret || s.tT >= s.next_tick;
+    if (!s.due) s.B = token_limit(p.cfg, c.k, c.ip, cap, s.A, s.P);
+    s.tw[0] = s.tw[1] = s.tw[2] = 0;
+    s.tc[0] = s.tc[1] = s.tc[2] = 0;
+    s.amin[0] = ~0ull;
+  };
+  if (tid == 0) prep();
+  __syncthreads();
+
   for (;;) {
-    // ---- loop top: stop rule, S1 snapshot ---------------------------------
-    if (tid == 0) {
-      s.run = (s.n_fin < n) && (s.t < p.max_iters);
-      s.tT = s.t * T;
-      s.A_snap = s.A;
-      s.n_holes = 0;
-    }
-    __syncthreads();
     if (!s.run) break;
     const uint64_t t = s.t, tT = s.tT;
-    // ---- S2 returns ----------------------------------------------------------
-    if (tT >= s.min_ret) {
-      const uint32_t npz = s.n_pz;
-      for (uint32_t i = tid; i < npz; i += SIM_NT) {
-        const uint32_t id = c.pz_id[i];
-        if (c.ret[id] <= tT) { do_return(c, id); c.pz_id[i] = INVALID; }
+    if (s.due) {
+      // ---- S2 returns --------------------------------------------------------
+      if (tT >= s.min_ret) {
+        const uint32_t npz = s.n_pz;
+        for (uint32_t i = tid; i < npz; i += SIM_NT) {
+          const uint32_t id = c.pz_id[i];
+          if (c.ret[id] <= tT) { do_return(c, id); c.pz_id[i] = INVALID; }
+        }
+        compact_paused(c);
+        if (tid == 0) s.min_ret = ~0ull;
+        __syncthreads();
+        for (uint32_t i = tid; i < s.n_pz; i += SIM_NT) atomicMin(&s.min_ret, (unsigned long long)c.ret[c.pz_id[i]]);
+        __syncthreads();
       }
-      compact_paused(c);
-      if (tid == 0) s.min_ret = ~0ull;
-      __syncthreads();
-      for (uint32_t i = tid; i < s.n_pz; i += SIM_NT) atomicMin(&s.min_ret, (unsigned long long)c.ret[c.pz_id[i]]);
-      __syncthreads();
-    }
-    // ---- S3 arrivals (ticks are sorted: the arrivals are a prefix) ------------
-    if (tT >= s.next_tick) for (;;) {
-      const uint32_t j = s.next_arr + tid;
-      const bool arrive = j < n && p.tr.arr_tick[c.r0 + j] <= tT;
-      const int cnt = __syncthreads_count(arrive);
-      if (arrive) do_arrival(c, j, s.n_act + tid, t);
-      __syncthreads();
+      // ---- S3 arrivals (ticks are sorted: the arrivals are a prefix) ----------
+      if (tT >= s.next_tick) for (;;) {
+        const uint32_t j = s.next_arr + tid;
+        const bool arrive = j < n && p.tr.arr_tick[c.r0 + j] <= tT;
+        const int cnt = __syncthreads_count(arrive);
+        if (arrive) do_arrival(c, j, s.n_act + tid, t);
+        __syncthreads();
+        if (tid == 0) {
+          s.n_act += cnt; s.next_arr += cnt; s.cnt[AUGSCHED_R_ARRIVED] += cnt;
+          if (cnt < SIM_NT) s.next_tick = s.next_arr < n ? p.tr.arr_tick[c.r0 + s.next_arr] : ~0ull;
+        }
+        __syncthreads();
+        if (cnt < SIM_NT) break;
+      }
+      // ---- idle jump (not counted) or S4 token limit ---------------------------
       if (tid == 0) {
-        s.n_act += cnt; s.next_arr += cnt; s.cnt[AUGSCHED_R_ARRIVED] += cnt;
-        if (cnt < SIM_NT) s.next_tick = s.next_arr < n ? p.tr.arr_tick[c.r0 + s.next_arr] : ~0ull;
+        s.idle = 0;
+        if (s.n_act == 0) {
+          uint64_t te = ~0ull;
+          if (s.next_arr < n) te = (p.tr.arr_tick[c.r0 + s.next_arr] + T - 1) / T;
+          if (s.n_pz > 0) { const uint64_t tr_ = (s.min_ret + T - 1) / T; te = tr_ < te ? tr_ : te; }
+          if (te == ~0ull) { s.idle = 2; s.run = 0; }
+          else { s.t = te; s.idle = 1; prep(); }
+        } else {
+          s.B = token_limit(p.cfg, c.k, c.ip, cap, s.A, s.P);
+        }
       }
       __syncthreads();
-      if (cnt < SIM_NT) break;
+      if (s.idle) continue;
     }
-    // ---- idle check; S4 token limit -------------------------------------------
-    if (tid == 0) {
-      s.idle = 0;
-      if (s.n_act == 0) {
-        uint64_t te = ~0ull;
-        if (s.next_arr < n) te = (p.tr.arr_tick[c.r0 + s.next_arr] + T - 1) / T;
-        if (s.n_pz > 0) { const uint64_t tr_ = (s.min_ret + T - 1) / T; te = tr_ < te ? tr_ : te; }
-        if (te == ~0ull) s.idle = 2; else { s.t = te; s.idle = 1; }
-      } else {
-        s.B = token_limit(p.cfg, c.k, c.ip, cap, s.A, s.P);
-        s.cnt[AUGSCHED_R_BUSY_STEPS] += 1;
-        s.cnt[AUGSCHED_R_DECISIONS] += s.n_act;
-        if (s.n_act > s.cnt[AUGSCHED_R_MAXQ]) s.cnt[AUGSCHED_R_MAXQ] = s.n_act;
-      }
-    }
-    __syncthreads();
-    if (s.idle == 2) break;
-    if (s.idle == 1) continue;
-    // ---- S5 keys --------------------------------------------------------------
+    // ---- S5 keys, per-tier demand, running/swapped candidate lists -----------
     const uint32_t na = s.n_act;
+    const long long B = s.B;
+    const uint32_t Bc = B > 0 ? (uint32_t)B : 0u;
     const bool in_smem = na <= p.scap;
     uint64_t* K = in_smem ? Ksm : a.kscr + off;
     uint32_t* W = in_smem ? Wsm : a.wscr + off;
     const bool fcfs = c.ip.ranking == AUGSCHED_RANK_FCFS;
-    for (uint32_t i = tid; i < na; i += SIM_NT) {
-      const uint32_t e = c.ac_id[i];
-      const uint32_t key = fcfs ? 0u : sched_key(c.k, c.ac_V[i], t, c.ac_last[i]);
-      K[i] = ((uint64_t)(e >> 30) << 48) | ((uint64_t)key << 16) | (e & 0xFFFF);
-      W[i] = c.ac_dem[i];
+    {
+      unsigned long long tw0 = 0, tw1 = 0, tw2 = 0;
+      for (uint32_t i = tid; i < na; i += SIM_NT) {
+        const uint32_t e = c.ac_id[i];
+        const uint32_t tier = e >> 30;
+        const uint32_t key = fcfs ? 0u : sched_key(c.k, c.ac_V[i], t, c.ac_last[i]);
+        const uint64_t Ki = ((uint64_t)tier << 48) | ((uint64_t)key << 16) | (e & 0xFFFF);
+        const uint32_t d = c.ac_dem[i];
+        K[i] = Ki;
+        W[i] = d;
+        const uint32_t dc = d < Bc ? d : Bc;
+        if (tier == 2) { tw2 += dc; continue; }
+        const uint32_t q = atomicAdd(&s.tc[tier], 1u);
+        if (q < 256) { s.u.c.ck[tier][q] = Ki; s.u.c.cw[tier][q] = d; }
+        if (tier == 0) tw0 += dc; else tw1 += dc;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        tw0 += __shfl_xor_sync(FULL, tw0, o);
+        tw1 += __shfl_xor_sync(FULL, tw1, o);
+        tw2 += __shfl_xor_sync(FULL, tw2, o);
+      }
+      if ((tid & 31) == 0) {
+        if (tw0) atomicAdd(&s.tw[0], tw0);
+        if (tw1) atomicAdd(&s.tw[1], tw1);
+        if (tw2) atomicAdd(&s.tw[2], tw2);
+      }
+      if (tid == 0) {
+        s.cnt[AUGSCHED_R_BUSY_STEPS] += 1;
+        s.cnt[AUGSCHED_R_DECISIONS] += na;
+        if (na > s.cnt[AUGSCHED_R_MAXQ]) s.cnt[AUGSCHED_R_MAXQ] = na;
+      }
     }
-    // ---- S6/S7 order + admission: weighted select of the prefix ---------------
-    const long long B = s.B;
-    if (B > 0) {
-      wselect<SIM_NT>(s.sel, na, (uint64_t)B, KBITS, [&](uint32_t i, uint64_t& key, uint32_t& w) {
-        key = K[i]; w = W[i]; return true; });
-    } else {
-      __syncthreads();
-      if (tid == 0) { s.sel.found = 1; s.sel.k = 0; s.sel.wbelow = 0; }  // nothing admitted
+    __syncthreads();
+    // ---- S6/S7 order + admission: find the last admitted entry k* --------------
+    // Tiers are ordered running < swapped < waiting, so the crossing tier follows
+    // from the per-tier totals; within it the crossing comes from a rank select
+    // over the (small) candidate list, or from argmin rounds over the waiting
+    // tier; the radix select over the whole queue is the fallback.
+    {
+      const unsigned long long w0 = s.tw[0], w1 = s.tw[1], w2 = s.tw[2];
+      const unsigned long long Bu = (unsigned long long)Bc;
+      bool done = false;
+      if (B <= 0) {
+        if (tid == 0) { s.res.found = 1; s.res.k = 0; s.res.wbelow = 0; }  // nothing admitted
+        done = true;
+      } else if (w0 + w1 + w2 < Bu) {
+        if (tid == 0) { s.res.found = 0; s.res.total = w0 + w1 + w2; }    // everything admitted
+        done = true;
+      } else if (w0 >= Bu) {
+        if (s.tc[0] <= 256) { rank_select<SIM_NT>(s.u.c, 0, s.res, (int)s.tc[0], Bu, 0); done = true; }
+      } else if (w0 + w1 >= Bu) {
+        if (s.tc[1] <= 256) { rank_select<SIM_NT>(s.u.c, 1, s.res, (int)s.tc[1], Bu, w0); done = true; }
+      } else {
+        // waiting tier: take the smallest remaining waiting keys one at a time
+        unsigned long long wb = w0 + w1;
+        uint64_t lastK = (2ull << 48) - 1;
+        for (int r = 0; r < 4 && !done; ++r) {
+          unsigned long long mk = ~0ull;
+          for (uint32_t i = tid; i < na; i += SIM_NT) {
+            const uint64_t Ki = K[i];
+            if (Ki > lastK && Ki < mk) mk = Ki;
+          }
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            const unsigned long long y = __shfl_xor_sync(FULL, mk, o);
+            mk = y < mk ? y : mk;
+          }
+          if ((tid & 31) == 0 && mk != ~0ull) atomicMin(&s.amin[r & 1], mk);
+          if (tid == 0) s.amin[(r + 1) & 1] = ~0ull;
+          __syncthreads();
+          const uint64_t km = s.amin[r & 1];
+          for (uint32_t i = tid; i < na; i += SIM_NT)
+            if (K[i] == km) s.aw = W[i];
+          __syncthreads();
+          const unsigned long long w = s.aw;
+          if (wb + w >= Bu) {
+            if (tid == 0) { s.res.found = 1; s.res.k = km; s.res.wbelow = wb; }
+            done = true;
+          }
+          wb += w;
+          lastK = km;
+        }
+      }
+      if (!done) {
+        wselect<SIM_NT>(s.u.b, s.res, na, Bu, KBITS, [&](uint32_t i, uint64_t& key, uint32_t& w) {
+          key = K[i]; w = W[i]; return true; });
+      }
       __syncthreads();
     }
-    const bool found = s.sel.found != 0;
-    const uint64_t kstar = B > 0 ? s.sel.k : 0;
-    const uint64_t wb = s.sel.wbelow;
+    const bool found = s.res.found != 0;
+    const uint64_t kstar = B > 0 ? s.res.k : 0;
+    const uint64_t wb = s.res.wbelow;
     auto grant = [&](uint64_t Ki, uint32_t dem) -> uint32_t {
       if (Ki & KEVICT) return 0u;
       if (B <= 0) return 0u;
@@ -325,16 +417,12 @@ __device__ void run_instance(const SimParams& p, SimShm& s, uint64_t* Ksm, uint3
       if (Ki == kstar) return (uint32_t)((uint64_t)B - wb);
       return 0u;
     };
-    if (tid == 0) {
-      s.need = found ? (B > 0 ? B : 0) : (long long)s.sel.total;
-      s.freev = cap - s.A - s.P;
-      s.freed = 0;
-    }
-    __syncthreads();
+    const long long need = B <= 0 ? 0 : (found ? B : (long long)s.res.total);
+    long long freev = cap - s.A - s.P;
     // ---- S8 memory resolution (R20) -------------------------------------------
-    if (s.need > s.freev) {
+    if (need > freev) {
       // (1) demote Preserve-paused contexts, kv desc, id asc
-      const uint64_t D0 = (uint64_t)(s.need - s.freev);
+      const uint64_t D0 = (uint64_t)(need - freev);
       const uint32_t npz = s.n_pz;
       auto getp = [&](uint32_t i, uint64_t& key, uint32_t& w) {
         const uint32_t id = c.pz_id[i];
@@ -344,10 +432,21 @@ __device__ void run_instance(const SimParams& p, SimShm& s, uint64_t* Ksm, uint3
         w = (uint32_t)kv;
         return true;
       };
-      wselect<SIM_NT>(s.sel, npz, D0, 48, getp);
+      if (tid == 0) { s.tc[0] = 0; s.freed = 0; }
+      __syncthreads();
+      for (uint32_t i = tid; i < npz; i += SIM_NT) {
+        uint64_t key; uint32_t w;
+        if (getp(i, key, w)) {
+          const uint32_t q = atomicAdd(&s.tc[0], 1u);
+          if (q < 256) { s.u.c.ck[0][q] = key; s.u.c.cw[0][q] = w; }
+        }
+      }
+      __syncthreads();
+      if (s.tc[0] <= 256) rank_select<SIM_NT>(s.u.c, 0, s.res, (int)s.tc[0], D0, 0);
+      else wselect<SIM_NT>(s.u.b, s.res, npz, D0, 48, getp);
       {
-        const bool f0 = s.sel.found != 0;
-        const uint64_t k0 = s.sel.k;
+        const bool f0 = s.res.found != 0;
+        const uint64_t k0 = s.res.k;
         for (uint32_t i = tid; i < npz; i += SIM_NT) {
           uint64_t key; uint32_t w;
           if (getp(i, key, w) && (!f0 || key <= k0)) {
@@ -361,23 +460,31 @@ __device__ void run_instance(const SimParams& p, SimShm& s, uint64_t* Ksm, uint3
         }
       }
       __syncthreads();
-      if (tid == 0) { s.freev += (long long)s.freed; s.P -= (long long)s.freed; s.freed = 0; }
+      freev += (long long)s.freed;
+      if (tid == 0) { s.P -= (long long)s.freed; s.tc[1] = 0; }
       __syncthreads();
       // (2) evict from the tail of the order over entries with kv + g > 0
-      if (s.need > s.freev) {
-        const uint64_t D1 = (uint64_t)(s.need - s.freev);
+      if (need > freev) {
+        const uint64_t D1 = (uint64_t)(need - freev);
         for (uint32_t i = tid; i < na; i += SIM_NT) {
           const uint32_t id = c.ac_id[i] & 0xFFFF;
-          W[i] = (uint32_t)c.kv[id] + grant(K[i], c.ac_dem[i]);
+          const uint32_t w = (uint32_t)c.kv[id] + grant(K[i], c.ac_dem[i]);
+          W[i] = w;
+          if (w > 0) {
+            const uint32_t q = atomicAdd(&s.tc[1], 1u);
+            if (q < 256) { s.u.c.ck[1][q] = KMASK - K[i]; s.u.c.cw[1][q] = w; }
+          }
         }
+        __syncthreads();
         auto gete = [&](uint32_t i, uint64_t& key, uint32_t& w) {
           w = W[i];
           key = KMASK - K[i];
           return w > 0;
         };
-        wselect<SIM_NT>(s.sel, na, D1, KBITS, gete);
-        const bool f1 = s.sel.found != 0;
-        const uint64_t k1 = s.sel.k;
+        if (s.tc[1] <= 256) rank_select<SIM_NT>(s.u.c, 1, s.res, (int)s.tc[1], D1, 0);
+        else wselect<SIM_NT>(s.u.b, s.res, na, D1, KBITS, gete);
+        const bool f1 = s.res.found != 0;
+        const uint64_t k1 = s.res.k;
         for (uint32_t i = tid; i < na; i += SIM_NT) {
           uint64_t key; uint32_t w;
           if (gete(i, key, w) && (!f1 || key <= k1)) {
@@ -490,6 +597,7 @@ __device__ void run_instance(const SimParams& p, SimShm& s, uint64_t* Ksm, uint3
     if (tid == 0) {
       if (s.A < 0 || s.P < 0 || s.A + s.P > cap) s.cnt[AUGSCHED_R_ERR] |= 1;
       s.t = t + 1;                                       // S12
+      prep();
     }
     __syncthreads();
   }

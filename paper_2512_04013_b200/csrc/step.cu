@@ -417,8 +417,8 @@ __global__ void __launch_bounds__(SNT) resolve_kernel(Slots S, int64_t cap, cons
   };
   wselect<SNT>(sel, MA, (uint64_t)(nd - fr), 56, getp);
   {
-    const bool f0 = sel.found != 0;
-    const uint64_t k0 = sel.k;
+    const bool f0 = sel.r.found != 0;
+    const uint64_t k0 = sel.r.k;
     for (uint32_t x = threadIdx.x; x < MA; x += SNT) {
       uint64_t key;
       uint32_t w;
@@ -444,8 +444,8 @@ __global__ void __launch_bounds__(SNT) resolve_kernel(Slots S, int64_t cap, cons
     return w > 0;
   };
   wselect<SNT>(sel, n, (uint64_t)(nd - fr), 24, gete);
-  const bool f1 = sel.found != 0;
-  const uint64_t k1 = sel.k;
+  const bool f1 = sel.r.found != 0;
+  const uint64_t k1 = sel.r.k;
   long long dA = 0;
   for (uint32_t j = threadIdx.x; j < n; j += SNT) {
     uint64_t key;
