@@ -115,7 +115,7 @@ typedef struct augsched_trace {
   const uint64_t* arr_tick;  /* [n_req] arrival time, µs */
   const uint32_t* l_pre;     /* [n_req] prompt tokens L^pre (>= 1) */
   const uint32_t* seg_off;   /* [n_req] */
-  const uint32_t* n_seg;     /* [n_req] >= 1 */
+  const uint32_t* n_seg;     /* [n_req] in [1, 255] (simulate reports E_INVALID otherwise) */
   const uint32_t* gen_true;  /* [n_seg_total] */
   const uint32_t* gen_pred;  /* [n_seg_total] predicted L^out */
   const uint32_t* dur_true;  /* [n_seg_total] call duration µs (ignored for last segment) */

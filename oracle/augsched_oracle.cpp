@@ -14,8 +14,7 @@
 // contraction: every double op is one IEEE round-to-nearest operation, R3).
 //
 // Pins (tests/test_oracle_*.py): SPEC worked examples,
-// the hand-worked schedules G3-G8 of SURVEY §8(c).3, Proposition 1 in exact
-// integers, brute force over all n! orders / 2^n subsets for
+// the hand-worked schedules G3-G8 of SURVEY §8(c).3, brute force over all n! orders / 2^n subsets for
 // n <= 7, and the invariants of SURVEY §8(c).4.
 // ============================================================================
 #include <algorithm>

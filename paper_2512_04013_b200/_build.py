@@ -38,7 +38,8 @@ def stale() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not stale():
         return LIB
-    cmd = [_nvcc(), *NVCC_FLAGS, "-shared", "-I", os.path.join(ROOT, "include"),
+    extra = os.environ.get("AUGSCHED_NVCC_EXTRA", "").split()  # tuning experiments only
+    cmd = [_nvcc(), *NVCC_FLAGS, *extra, "-shared", "-I", os.path.join(ROOT, "include"),
            *[os.path.join(CSRC, s) for s in SOURCES], "-o", LIB + ".tmp"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:

@@ -124,9 +124,7 @@ int ensure_sim(augsched_t* h) {
   const size_t N = (size_t)h->n_inst * h->max_active;
   Arena& a = h->ar;
   int rc;
-  if ((rc = h->alloc(&a.ctx, N)) || (rc = h->alloc(&a.kv, N)) || (rc = h->alloc(&a.cpu, N)) ||
-      (rc = h->alloc(&a.pend, N)) || (rc = h->alloc(&a.meta, N)) || (rc = h->alloc(&a.ret, N)) ||
-      (rc = h->alloc(&a.ft, N)) || (rc = h->alloc(&a.lastc, N)) || (rc = h->alloc(&a.ac_id, N)) ||
+  if ((rc = h->alloc(&a.rs, N)) || (rc = h->alloc(&a.ret, N)) || (rc = h->alloc(&a.ac_id, N)) ||
       (rc = h->alloc(&a.ac_V, N)) || (rc = h->alloc(&a.ac_last, N)) ||
       (rc = h->alloc(&a.ac_dem, N)) || (rc = h->alloc(&a.pz_id, N)) ||
       (rc = h->alloc(&a.kscr, N)) || (rc = h->alloc(&a.wscr, N)) ||
@@ -135,7 +133,7 @@ int ensure_sim(augsched_t* h) {
   a.kscr2 = nullptr;
   a.wscr2 = nullptr;
   // shared-memory queue capacity and persistent grid
-  h->scap = h->max_active < 1536 ? h->max_active : 1536;
+  h->scap = h->max_active < SIM_SCAP ? h->max_active : SIM_SCAP;
   h->sim_smem = sim_smem_bytes(h->scap);
   CUDA_TRY(cudaFuncSetAttribute(sim_kernel_ptr(), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)h->sim_smem));
@@ -222,6 +220,7 @@ int augsched_sync(augsched_t* h) {
   CUDA_TRY(cudaMemcpy(&err, h->d_err, sizeof(err), cudaMemcpyDeviceToHost));
   if (err & 1u) return fail(AUGSCHED_E_STATE, "a record violated the request state machine");
   if (err & 2u) return fail(AUGSCHED_E_CAPACITY, "a trace is longer than max_active_per_instance");
+  if (err & 4u) return fail(AUGSCHED_E_INVALID, "a request has n_seg outside [1, 255]");
   return AUGSCHED_OK;
 }
 

@@ -8,7 +8,8 @@
 // (tier, score key, id) order and weights the demands; with keys taken from
 // the back of the order and weights kv + grant it is the eviction cut of R20.
 //
-// 8-bit digits from the top; demand-weighted shared-memory histograms built
+// RB-bit digits from the top (8 for the 256-thread step kernels, 5 = one bin
+// per lane for the one-warp simulate CTAs); demand-weighted shared-memory histograms built
 // with warp-aggregated atomics (__match_any_sync + __reduce_add_sync), double
 // buffered so each pass costs two barriers; a per-bin witness key ends the
 // search as soon as the crossing bucket holds a single item.  Weights are
@@ -18,11 +19,14 @@
 
 namespace augsched {
 
-struct SelBins {
-  unsigned long long wbin[2][256];
-  unsigned int cbin[2][256];
-  unsigned long long wkey[2][256];
+template <int RB>
+struct SelBinsT {
+  static constexpr int NB = 1 << RB;
+  unsigned long long wbin[2][NB];
+  unsigned int cbin[2][NB];
+  unsigned long long wkey[2][NB];
 };
+using SelBins = SelBinsT<8>;
 
 struct SelRes {
   unsigned long long prefix, mask, wbelow, k, total;
@@ -38,9 +42,11 @@ struct SelShm {
 
 // Results: r.found (0: total weight < D, r.total holds it), r.k = k*,
 // r.wbelow = sum of weights with key < k*.  Must be called by all NT threads.
-template <int NT, class Get>
-__device__ void wselect(SelBins& sb, SelRes& s, uint32_t n, uint64_t D, int nbits, Get get) {
+template <int NT, int RB, class Get>
+__device__ void wselect(SelBinsT<RB>& sb, SelRes& s, uint32_t n, uint64_t D, int nbits, Get get) {
   constexpr unsigned FULL = 0xffffffffu;
+  constexpr int NB = 1 << RB;
+  static_assert(NB >= 32 && NB % 32 == 0, "one warp scans the bins in 32-wide chunks");
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t Dc = (uint32_t)(D < (1ull << 26) ? D : (1ull << 26));
   __syncthreads();
@@ -48,17 +54,17 @@ __device__ void wselect(SelBins& sb, SelRes& s, uint32_t n, uint64_t D, int nbit
     s.prefix = 0; s.mask = 0; s.wbelow = 0; s.found = 0; s.done = 0; s.total = 0; s.cnt = 0;
     s.k = 0;
   }
-  for (int b = tid; b < 256; b += NT) { sb.wbin[0][b] = 0; sb.cbin[0][b] = 0; }
+  for (int b = tid; b < NB; b += NT) { sb.wbin[0][b] = 0; sb.cbin[0][b] = 0; }
   __syncthreads();
   int hi = nbits, pb = 0;
   while (hi > 0) {
-    const int lo = hi > 8 ? hi - 8 : 0;
+    const int lo = hi > RB ? hi - RB : 0;
     const uint32_t dmask = (1u << (hi - lo)) - 1;
     const uint64_t prefix = s.prefix, mask = s.mask;
     unsigned long long* wbin = sb.wbin[pb];
     unsigned int* cbin = sb.cbin[pb];
     unsigned long long* wkey = sb.wkey[pb];
-    for (int b = tid; b < 256; b += NT) { sb.wbin[pb ^ 1][b] = 0; sb.cbin[pb ^ 1][b] = 0; }
+    for (int b = tid; b < NB; b += NT) { sb.wbin[pb ^ 1][b] = 0; sb.cbin[pb ^ 1][b] = 0; }
     for (uint32_t base = 0; base < n; base += NT) {
       const uint32_t i = base + tid;
       int dig = -1;
@@ -87,7 +93,7 @@ __device__ void wselect(SelBins& sb, SelRes& s, uint32_t n, uint64_t D, int nbit
       int bin = -1;
       unsigned long long wb = 0;
 #pragma unroll 1
-      for (int q = 0; q < 8; ++q) {
+      for (int q = 0; q < NB / 32; ++q) {
         const int b = q * 32 + lane;
         const unsigned long long w = wbin[b];
         unsigned long long inc = w;
@@ -128,23 +134,25 @@ __device__ void wselect(SelBins& sb, SelRes& s, uint32_t n, uint64_t D, int nbit
 
 template <int NT, class Get>
 __device__ __forceinline__ void wselect(SelShm& s, uint32_t n, uint64_t D, int nbits, Get get) {
-  wselect<NT>(s.b, s.r, n, D, nbits, get);
+  wselect<NT, 8>(s.b, s.r, n, D, nbits, get);
 }
 
-// Small-candidate variant: m <= 256 (key, weight) pairs in shared memory.
+// Small-candidate variant: m <= C (key, weight) pairs in shared memory.
 // Each candidate's rank is counted against all others (keys unique), pairs
 // are scattered to rank order, and one warp scans the weights for the
 // crossing.  Results in r as for wselect, with wbelow offset by w0 (the
 // weight of everything ordered before the candidate set).
-struct CandShm {
-  unsigned long long ck[2][256];
-  unsigned int cw[2][256];
-  unsigned long long rk[256];
-  unsigned int rw[256];
+template <int C>
+struct CandShmT {
+  static constexpr int CAP = C;
+  unsigned long long ck[2][C];
+  unsigned int cw[2][C];
+  unsigned long long rk[C];
+  unsigned int rw[C];
 };
 
-template <int NT>
-__device__ void rank_select(CandShm& c, int list, SelRes& r, int m, uint64_t D, uint64_t w0) {
+template <int NT, int C>
+__device__ void rank_select(CandShmT<C>& c, int list, SelRes& r, int m, uint64_t D, uint64_t w0) {
   constexpr unsigned FULL = 0xffffffffu;
   const int tid = threadIdx.x, lane = tid & 31;
   const unsigned long long* ck = c.ck[list];

@@ -9,17 +9,15 @@ namespace augsched {
 
 struct __align__(16) SimShm {
   union {
-    SelBins b;                       // radix-select histograms (fallback path)
-    CandShm c;                       // small candidate lists (fast path)
+    SelBinsT<SIM_RB> b;              // radix-select histograms (fallback path)
+    CandShmT<SIM_CAND> c;            // small candidate lists (fast path)
   } u;
   SelRes res;
   unsigned long long tw[3];          // per-tier demand (clamped to B) of the step
   unsigned int tc[3];                // per-tier queue counts of the step
-  unsigned long long amin[2];        // argmin rounds over the waiting tier
-  unsigned int aw;
+  unsigned long long rk[2][SIM_NW];  // waiting-tier pop rounds: per-warp smallest key
+  unsigned int rw[2][SIM_NW];        //   and its demand (double-buffered by round parity)
   int due;                           // intake or idle handling needed this iteration
-  unsigned int hist_t[AUGSCHED_NBIN];
-  unsigned int hist_n[AUGSCHED_NBIN];
   unsigned long long cnt[AUGSCHED_R_NFIELD];
   unsigned int holes[HOLE_CAP];
   unsigned int wtot[SIM_NW + 1];
@@ -66,8 +64,8 @@ struct Ctx {
   Coef k;
   augsched_instance_params ip;
   // arena slices of this instance
-  int32_t *ctx, *kv, *cpu, *pend;
-  uint32_t *meta, *ft, *lastc, *ac_id, *ac_last, *ac_dem, *pz_id;
+  ReqState* rs;
+  uint32_t *ac_id, *ac_last, *ac_dem, *pz_id;
   uint64_t* ret;
   double* ac_V;
   uint32_t r0, n, trace;
@@ -85,12 +83,13 @@ __device__ void do_return(Ctx& c, uint32_t id) {
   const DevTrace& tr = c.p.tr;
   SimShm& s = c.s;
   const uint32_t rid = c.r0 + id;
-  const uint32_t m = c.meta[id];
+  ReqState r = c.rs[id];
+  const uint32_t m = r.meta;
   const uint32_t kk = meta_seg(m);
   const int pol = (int)meta_pol(m);
   const uint32_t s0 = tr.seg_off[rid];
-  const uint32_t ns = tr.n_seg[rid];
-  const int32_t ctx = c.ctx[id], kv = c.kv[id], cpu = c.cpu[id];
+  const uint32_t ns = meta_nseg(m);
+  const int32_t ctx = r.ctx, kv = r.kv, cpu = r.cpu;
   const uint64_t R = tr.ret_len[s0 + kk];
   const uint64_t On = tr.gen_pred[s0 + kk + 1];
   const bool has_next = kk + 1 < ns - 1;
@@ -104,13 +103,15 @@ __device__ void do_return(Ctx& c, uint32_t id) {
     atomicAdd((unsigned long long*)&s.A, (unsigned long long)(long long)kv);
   } else if (pol == POL_S) { st = ST_SWAP; tier = 1; }
   else { st = ST_WAIT; tier = 2; }
-  c.pend[id] = (int32_t)R;
-  c.meta[id] = make_meta(kk + 1, st, (uint32_t)pol, 0);
+  r.pend = (int32_t)R;
+  r.meta = make_meta(kk + 1, st, (uint32_t)pol, ns);
+  r.left = tr.gen_true[s0 + kk + 1];
+  c.rs[id] = r;
   atomicAdd(&s.cnt[AUGSCHED_R_RETURNS], 1ull);
   const uint32_t pos = atomicAdd(&s.n_act, 1u);
   c.ac_id[pos] = id | (tier << 30);
   c.ac_V[pos] = V;
-  c.ac_last[pos] = c.lastc[id];  // not reset on return (R14)
+  c.ac_last[pos] = r.lastc;  // not reset on return (R14)
   c.ac_dem[pos] = demand_of(ctx, kv, cpu, (int32_t)R, c.p.cfg.s_in);
 }
 
@@ -125,9 +126,14 @@ __device__ void do_arrival(Ctx& c, uint32_t id, uint32_t pos, uint64_t t) {
   const bool has_call = tr.n_seg[rid] > 1;
   const double A = has_call ? (double)tr.dur_pred[s0] : 0.0;
   const double V = intake_stage1(c.k, c.ip.policy_mode, L, O, A, has_call, (uint64_t)c.s.A_snap);
-  c.ctx[id] = 0; c.kv[id] = 0; c.cpu[id] = 0; c.pend[id] = (int32_t)L;
-  c.meta[id] = make_meta(0, ST_WAIT, POL_D, 0);
-  c.ft[id] = 0;
+  const uint32_t ns = tr.n_seg[rid];
+  if (ns == 0 || ns > 255) { err_set(c.p, 4u); c.s.cnt[AUGSCHED_R_ERR] |= 4; }  // meta holds 8 bits
+  ReqState r;
+  r.ctx = 0; r.kv = 0; r.cpu = 0; r.pend = (int32_t)L;
+  r.meta = make_meta(0, ST_WAIT, POL_D, ns);
+  r.ft = 0; r.lastc = 0;
+  r.left = tr.gen_true[s0];
+  c.rs[id] = r;
   c.ac_id[pos] = id | (2u << 30);
   c.ac_V[pos] = V;
   c.ac_last[pos] = (uint32_t)t;           // R14, R31
@@ -213,8 +219,7 @@ __device__ void run_instance(const SimParams& p, SimShm& s, uint64_t* Ksm, uint3
   const int tid = threadIdx.x;
   const size_t off = (size_t)inst * p.max_active;
   const Arena& a = p.ar;
-  Ctx c{p, s, {}, p.ip[inst], a.ctx + off, a.kv + off, a.cpu + off, a.pend + off, a.meta + off,
-        a.ft + off, a.lastc + off, a.ac_id + off, a.ac_last + off, a.ac_dem + off, a.pz_id + off,
+  Ctx c{p, s, {}, p.ip[inst], a.rs + off, a.ac_id + off, a.ac_last + off, a.ac_dem + off, a.pz_id + off,
         a.ret + off, a.ac_V + off, 0, 0, 0};
   c.k = make_coef(p.cfg, c.ip);
   c.trace = p.inst_trace[inst];
@@ -241,7 +246,6 @@ __device__ void run_instance(const SimParams& p, SimShm& s, uint64_t* Ksm, uint3
     s.next_tick = s.next_arr < n ? p.tr.arr_tick[c.r0 + s.next_arr] : ~0ull;
   }
   for (int f = tid; f < AUGSCHED_R_NFIELD; f += SIM_NT) s.cnt[f] = acc.f[f];
-  for (int b = tid; b < AUGSCHED_NBIN; b += SIM_NT) { s.hist_t[b] = acc.hist_ttft[b]; s.hist_n[b] = acc.hist_norm[b]; }
   __syncthreads();
   if (tid == 0) s.cnt[AUGSCHED_R_NREQ] = n;
   const int64_t cap = p.cap;
@@ -257,7 +261,6 @@ __device__ void run_instance(const SimParams& p, SimShm& s, uint64_t* Ksm, uint3
     if (!s.due) s.B = token_limit(p.cfg, c.k, c.ip, cap, s.A, s.P);
     s.tw[0] = s.tw[1] = s.tw[2] = 0;
     s.tc[0] = s.tc[1] = s.tc[2] = 0;
-    s.amin[0] = ~0ull;
   };
   if (tid == 0) prep();
   __syncthreads();
@@ -317,21 +320,59 @@ __device__ void run_instance(const SimParams& p, SimShm& s, uint64_t* Ksm, uint3
     uint64_t* K = in_smem ? Ksm : a.kscr + off;
     uint32_t* W = in_smem ? Wsm : a.wscr + off;
     const bool fcfs = c.ip.ranking == AUGSCHED_RANK_FCFS;
+    // This thread's two smallest waiting-tier keys (and demands): the first
+    // candidates of the pop rounds below.
+    uint64_t c1 = ~0ull, c2 = ~0ull;
+    uint32_t cw1 = 0, cw2 = 0;
     {
       unsigned long long tw0 = 0, tw1 = 0, tw2 = 0;
-      for (uint32_t i = tid; i < na; i += SIM_NT) {
-        const uint32_t e = c.ac_id[i];
-        const uint32_t tier = e >> 30;
-        const uint32_t key = fcfs ? 0u : sched_key(c.k, c.ac_V[i], t, c.ac_last[i]);
-        const uint64_t Ki = ((uint64_t)tier << 48) | ((uint64_t)key << 16) | (e & 0xFFFF);
-        const uint32_t d = c.ac_dem[i];
-        K[i] = Ki;
-        W[i] = d;
-        const uint32_t dc = d < Bc ? d : Bc;
-        if (tier == 2) { tw2 += dc; continue; }
-        const uint32_t q = atomicAdd(&s.tc[tier], 1u);
-        if (q < 256) { s.u.c.ck[tier][q] = Ki; s.u.c.cw[tier][q] = d; }
-        if (tier == 0) tw0 += dc; else tw1 += dc;
+      constexpr int U = SIM_UNROLL;  // entries in flight per thread (independent L2 loads)
+      const int lane = tid & 31;
+      const unsigned lt = (1u << lane) - 1;
+      // warp-uniform trip count (the candidate lists use warp ballots)
+      for (uint32_t b0 = 0; b0 < na; b0 += SIM_NT * U) {
+        uint32_t e[U], l[U], d[U];
+        double V[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const uint32_t i = b0 + u * SIM_NT + tid;
+          if (i < na) { e[u] = c.ac_id[i]; V[u] = c.ac_V[i]; l[u] = c.ac_last[i]; d[u] = c.ac_dem[i]; }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const uint32_t i = b0 + u * SIM_NT + tid;
+          uint32_t tier = 3;
+          uint64_t Ki = 0;
+          if (i < na) {
+            tier = e[u] >> 30;
+            const uint32_t key = fcfs ? 0u : sched_key(c.k, V[u], t, l[u]);
+            Ki = ((uint64_t)tier << 48) | ((uint64_t)key << 16) | (e[u] & 0xFFFF);
+            K[i] = Ki;
+            W[i] = d[u];
+            const uint32_t dc = d[u] < Bc ? d[u] : Bc;
+            if (tier == 2) {
+              tw2 += dc;
+              if (Ki < c2) {
+                if (Ki < c1) { c2 = c1; cw2 = cw1; c1 = Ki; cw1 = d[u]; }
+                else { c2 = Ki; cw2 = d[u]; }
+              }
+            } else if (tier == 0) tw0 += dc;
+            else tw1 += dc;
+          }
+          // running / swapped candidate lists, one shared atomic per warp and tier
+#pragma unroll
+          for (uint32_t tt = 0; tt < 2; ++tt) {
+            const unsigned m = __ballot_sync(FULL, tier == tt);
+            if (m) {
+              const int leader = __ffs(m) - 1;
+              uint32_t q0 = 0;
+              if (lane == leader) q0 = atomicAdd(&s.tc[tt], (unsigned)__popc(m));
+              q0 = __shfl_sync(FULL, q0, leader);
+              const uint32_t q = q0 + __popc(m & lt);
+              if (tier == tt && q < SIM_CAND) { s.u.c.ck[tt][q] = Ki; s.u.c.cw[tt][q] = d[u]; }
+            }
+          }
+        }
       }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
@@ -367,42 +408,59 @@ __device__ void run_instance(const SimParams& p, SimShm& s, uint64_t* Ksm, uint3
         if (tid == 0) { s.res.found = 0; s.res.total = w0 + w1 + w2; }    // everything admitted
         done = true;
       } else if (w0 >= Bu) {
-        if (s.tc[0] <= 256) { rank_select<SIM_NT>(s.u.c, 0, s.res, (int)s.tc[0], Bu, 0); done = true; }
+        if (s.tc[0] <= SIM_CAND) { rank_select<SIM_NT, SIM_CAND>(s.u.c, 0, s.res, (int)s.tc[0], Bu, 0); done = true; }
       } else if (w0 + w1 >= Bu) {
-        if (s.tc[1] <= 256) { rank_select<SIM_NT>(s.u.c, 1, s.res, (int)s.tc[1], Bu, w0); done = true; }
+        if (s.tc[1] <= SIM_CAND) { rank_select<SIM_NT, SIM_CAND>(s.u.c, 1, s.res, (int)s.tc[1], Bu, w0); done = true; }
       } else {
-        // waiting tier: take the smallest remaining waiting keys one at a time
+        // waiting tier: pop the smallest remaining waiting keys in order, one
+        // per round (one barrier each).  Every thread offers its smallest
+        // unconsumed waiting key (c1, then c2, then a rescan of its own
+        // entries); the block minimum is the next entry of the order.
+        const int lane = tid & 31, warp = tid >> 5;
         unsigned long long wb = w0 + w1;
-        uint64_t lastK = (2ull << 48) - 1;
-        for (int r = 0; r < 4 && !done; ++r) {
-          unsigned long long mk = ~0ull;
-          for (uint32_t i = tid; i < na; i += SIM_NT) {
-            const uint64_t Ki = K[i];
-            if (Ki > lastK && Ki < mk) mk = Ki;
-          }
+        uint64_t myk = c1;
+        uint32_t myw = cw1;
+        int cons = 0;
+        for (int r = 0; r < 32; ++r) {
+          uint64_t mk = myk;
 #pragma unroll
           for (int o = 16; o > 0; o >>= 1) {
-            const unsigned long long y = __shfl_xor_sync(FULL, mk, o);
+            const uint64_t y = __shfl_xor_sync(FULL, mk, o);
             mk = y < mk ? y : mk;
           }
-          if ((tid & 31) == 0 && mk != ~0ull) atomicMin(&s.amin[r & 1], mk);
-          if (tid == 0) s.amin[(r + 1) & 1] = ~0ull;
+          const unsigned own = __ballot_sync(FULL, myk == mk);
+          if (lane == __ffs(own) - 1) { s.rk[r & 1][warp] = mk; s.rw[r & 1][warp] = myw; }
           __syncthreads();
-          const uint64_t km = s.amin[r & 1];
-          for (uint32_t i = tid; i < na; i += SIM_NT)
-            if (K[i] == km) s.aw = W[i];
-          __syncthreads();
-          const unsigned long long w = s.aw;
-          if (wb + w >= Bu) {
-            if (tid == 0) { s.res.found = 1; s.res.k = km; s.res.wbelow = wb; }
-            done = true;
+          uint64_t bk = s.rk[r & 1][0];
+          uint32_t bw = s.rw[r & 1][0];
+#pragma unroll
+          for (int w = 1; w < SIM_NW; ++w) {
+            const uint64_t x = s.rk[r & 1][w];
+            if (x < bk) { bk = x; bw = s.rw[r & 1][w]; }
           }
-          wb += w;
-          lastK = km;
+          if (bk == ~0ull) break;  // not reachable: w0 + w1 + w2 >= B
+          if (wb + bw >= Bu) {
+            if (tid == 0) { s.res.found = 1; s.res.k = bk; s.res.wbelow = wb; }
+            done = true;
+            break;
+          }
+          wb += bw;
+          if (myk == bk) {
+            if (++cons == 1) { myk = c2; myw = cw2; }
+            else {
+              uint64_t nk = ~0ull;
+              uint32_t nw = 0;
+              for (uint32_t i = tid; i < na; i += SIM_NT) {
+                const uint64_t Ki = K[i];
+                if ((Ki >> 48) == 2 && Ki > bk && Ki < nk) { nk = Ki; nw = W[i]; }
+              }
+              myk = nk; myw = nw;
+            }
+          }
         }
       }
       if (!done) {
-        wselect<SIM_NT>(s.u.b, s.res, na, Bu, KBITS, [&](uint32_t i, uint64_t& key, uint32_t& w) {
+        wselect<SIM_NT, SIM_RB>(s.u.b, s.res, na, Bu, KBITS, [&](uint32_t i, uint64_t& key, uint32_t& w) {
           key = K[i]; w = W[i]; return true; });
       }
       __syncthreads();
@@ -426,8 +484,8 @@ __device__ void run_instance(const SimParams& p, SimShm& s, uint64_t* Ksm, uint3
       const uint32_t npz = s.n_pz;
       auto getp = [&](uint32_t i, uint64_t& key, uint32_t& w) {
         const uint32_t id = c.pz_id[i];
-        const int32_t kv = c.kv[id];
-        if (meta_pol(c.meta[id]) != POL_P || kv <= 0) return false;
+        const int32_t kv = c.rs[id].kv;
+        if (meta_pol(c.rs[id].meta) != POL_P || kv <= 0) return false;
         key = ((uint64_t)(0xFFFFFFFFu - (uint32_t)kv) << 16) | id;
         w = (uint32_t)kv;
         return true;
@@ -438,12 +496,12 @@ __device__ void run_instance(const SimParams& p, SimShm& s, uint64_t* Ksm, uint3
         uint64_t key; uint32_t w;
         if (getp(i, key, w)) {
           const uint32_t q = atomicAdd(&s.tc[0], 1u);
-          if (q < 256) { s.u.c.ck[0][q] = key; s.u.c.cw[0][q] = w; }
+          if (q < SIM_CAND) { s.u.c.ck[0][q] = key; s.u.c.cw[0][q] = w; }
         }
       }
       __syncthreads();
-      if (s.tc[0] <= 256) rank_select<SIM_NT>(s.u.c, 0, s.res, (int)s.tc[0], D0, 0);
-      else wselect<SIM_NT>(s.u.b, s.res, npz, D0, 48, getp);
+      if (s.tc[0] <= SIM_CAND) rank_select<SIM_NT, SIM_CAND>(s.u.c, 0, s.res, (int)s.tc[0], D0, 0);
+      else wselect<SIM_NT, SIM_RB>(s.u.b, s.res, npz, D0, 48, getp);
       {
         const bool f0 = s.res.found != 0;
         const uint64_t k0 = s.res.k;
@@ -452,9 +510,8 @@ __device__ void run_instance(const SimParams& p, SimShm& s, uint64_t* Ksm, uint3
           if (getp(i, key, w) && (!f0 || key <= k0)) {
             const uint32_t id = c.pz_id[i];
             atomicAdd(&s.freed, (unsigned long long)w);
-            c.kv[id] = 0;
-            const uint32_t m = c.meta[id];
-            c.meta[id] = make_meta(meta_seg(m), meta_st(m), POL_D, meta_gen(m));
+            c.rs[id].kv = 0;
+            c.rs[id].meta = meta_with(c.rs[id].meta, meta_st(c.rs[id].meta), POL_D);
             atomicAdd(&s.cnt[AUGSCHED_R_DEMOTIONS], 1ull);
           }
         }
@@ -468,11 +525,11 @@ __device__ void run_instance(const SimParams& p, SimShm& s, uint64_t* Ksm, uint3
         const uint64_t D1 = (uint64_t)(need - freev);
         for (uint32_t i = tid; i < na; i += SIM_NT) {
           const uint32_t id = c.ac_id[i] & 0xFFFF;
-          const uint32_t w = (uint32_t)c.kv[id] + grant(K[i], c.ac_dem[i]);
+          const uint32_t w = (uint32_t)c.rs[id].kv + grant(K[i], c.ac_dem[i]);
           W[i] = w;
           if (w > 0) {
             const uint32_t q = atomicAdd(&s.tc[1], 1u);
-            if (q < 256) { s.u.c.ck[1][q] = KMASK - K[i]; s.u.c.cw[1][q] = w; }
+            if (q < SIM_CAND) { s.u.c.ck[1][q] = KMASK - K[i]; s.u.c.cw[1][q] = w; }
           }
         }
         __syncthreads();
@@ -481,8 +538,8 @@ __device__ void run_instance(const SimParams& p, SimShm& s, uint64_t* Ksm, uint3
           key = KMASK - K[i];
           return w > 0;
         };
-        if (s.tc[1] <= 256) rank_select<SIM_NT>(s.u.c, 1, s.res, (int)s.tc[1], D1, 0);
-        else wselect<SIM_NT>(s.u.b, s.res, na, D1, KBITS, gete);
+        if (s.tc[1] <= SIM_CAND) rank_select<SIM_NT, SIM_CAND>(s.u.c, 1, s.res, (int)s.tc[1], D1, 0);
+        else wselect<SIM_NT, SIM_RB>(s.u.b, s.res, na, D1, KBITS, gete);
         const bool f1 = s.res.found != 0;
         const uint64_t k1 = s.res.k;
         for (uint32_t i = tid; i < na; i += SIM_NT) {
@@ -490,14 +547,14 @@ __device__ void run_instance(const SimParams& p, SimShm& s, uint64_t* Ksm, uint3
           if (gete(i, key, w) && (!f1 || key <= k1)) {
             const uint32_t e = c.ac_id[i];
             const uint32_t id = e & 0xFFFF;
-            const int32_t kv = c.kv[id];
-            atomicAdd((unsigned long long*)&s.A, (unsigned long long)(-(long long)kv));
-            c.kv[id] = 0;
-            c.cpu[id] = 0;
-            const uint32_t m = c.meta[id];
-            c.meta[id] = make_meta(meta_seg(m), ST_WAIT, meta_pol(m), meta_gen(m));
+            ReqState r = c.rs[id];
+            atomicAdd((unsigned long long*)&s.A, (unsigned long long)(-(long long)r.kv));
+            r.kv = 0;
+            r.cpu = 0;
+            r.meta = meta_with(r.meta, ST_WAIT, meta_pol(r.meta));
+            c.rs[id] = r;
             c.ac_id[i] = id | (2u << 30);
-            c.ac_dem[i] = demand_of(c.ctx[id], 0, 0, c.pend[id], p.cfg.s_in);
+            c.ac_dem[i] = demand_of(r.ctx, 0, 0, r.pend, p.cfg.s_in);
             K[i] |= KEVICT;
             atomicAdd(&s.cnt[AUGSCHED_R_EVICTIONS], 1ull);
           }
@@ -508,16 +565,20 @@ __device__ void run_instance(const SimParams& p, SimShm& s, uint64_t* Ksm, uint3
     // ---- S9 last = t for granted entries; S10 engine advance -------------------
     {
       uint32_t my_tok = 0, my_adm = 0;
+      long long accA = 0, accP = 0;
       for (uint32_t i = tid; i < na; i += SIM_NT) {
-        const uint32_t g = grant(K[i], c.ac_dem[i]);
+        const uint64_t Ki = K[i];
+        const uint32_t dem = c.ac_dem[i], e = c.ac_id[i];  // independent loads, issued together
+        const uint32_t g = grant(Ki, dem);
         if (g == 0) continue;
         my_tok += g; my_adm += 1;
-        const uint32_t id = c.ac_id[i] & 0xFFFF;
+        const uint32_t id = e & 0xFFFF;
         const uint32_t rid = c.r0 + id;
-        int32_t ctx = c.ctx[id], kv = c.kv[id], cpu = c.cpu[id], pend = c.pend[id];
+        ReqState r = c.rs[id];
+        int32_t ctx = r.ctx, kv = r.kv, cpu = r.cpu, pend = r.pend;
         const int32_t kv_snap = kv;
-        uint32_t m = c.meta[id];
-        uint32_t seg = meta_seg(m), gen = meta_gen(m), pol = meta_pol(m);
+        uint32_t m = r.meta;
+        const uint32_t seg = meta_seg(m), pol = meta_pol(m);
         long long dA = 0, dP = 0;
         bool leave = false;
         if (cpu > 0) {                                   // swap-in
@@ -529,18 +590,16 @@ __device__ void run_instance(const SimParams& p, SimShm& s, uint64_t* Ksm, uint3
           pend -= pp; ctx += pp; kv += pp;
           dA += g;
         } else {                                         // decode one token
-          ctx += 1; kv += 1; dA += 1; gen += 1;
-          if (c.ft[id] == 0) c.ft[id] = (uint32_t)(t + 1);  // R22
-          const uint32_t s0 = p.tr.seg_off[rid];
-          const uint32_t ns = p.tr.n_seg[rid];
-          if (gen == p.tr.gen_true[s0 + seg]) {
+          ctx += 1; kv += 1; dA += 1;
+          if (r.ft == 0) r.ft = (uint32_t)(t + 1);      // R22
+          if (--r.left == 0) {                           // segment end
             leave = true;
-            if (seg + 1 == ns) {                         // finish
+            if (seg + 1 == meta_nseg(m)) {               // finish
               dA -= kv; kv = 0;
-              m = make_meta(seg, ST_DONE, pol, gen);
+              m = meta_with(m, ST_DONE, pol);
               const uint64_t arr = p.tr.arr_tick[rid];
               const uint64_t fin = t + 1;
-              const uint64_t ttft = (uint64_t)c.ft[id] * T - arr;
+              const uint64_t ttft = (uint64_t)r.ft * T - arr;
               const uint64_t e2e = fin * T - arr;
               const uint64_t gt = gen_total(p.tr, rid);
               const bool ok = ttft < c.ip.slo_ttft_ticks &&
@@ -555,31 +614,33 @@ __device__ void run_instance(const SimParams& p, SimShm& s, uint64_t* Ksm, uint3
               atomicAdd(&s.cnt[AUGSCHED_R_SUM_TTFT], (unsigned long long)ttft);
               atomicAdd(&s.cnt[AUGSCHED_R_SUM_E2E], (unsigned long long)e2e);
               atomicAdd(&s.cnt[AUGSCHED_R_SUM_GEN], (unsigned long long)gt);
-              atomicAdd(&s.hist_t[hist_bin(ttft)], 1u);
-              atomicAdd(&s.hist_n[hist_bin(e2e / gt)], 1u);
+              atomicAdd(&acc.hist_ttft[hist_bin(ttft)], 1u);   // rare: global atomics
+              atomicAdd(&acc.hist_norm[hist_bin(e2e / gt)], 1u);
             } else {                                     // issue call `seg` (R13, R21)
+              const uint32_t s0 = p.tr.seg_off[rid];
               const double Ti = (double)p.tr.dur_pred[s0 + seg];
               const int np = select_policy(c.k, (uint64_t)ctx, Ti,
                                            (uint64_t)(s.A_snap - (long long)kv_snap),
                                            c.ip.policy_mode);
               const uint64_t rt = (t + 1) * T + p.tr.dur_true[s0 + seg];
               c.ret[id] = rt;
-              c.lastc[id] = (uint32_t)t;
+              r.lastc = (uint32_t)t;
               dA -= kv;
               if (np == POL_P) { dP += kv; atomicAdd(&s.cnt[AUGSCHED_R_CALLS_PRESERVE], 1ull); }
               else if (np == POL_S) { cpu = ctx; kv = 0; atomicAdd(&s.cnt[AUGSCHED_R_CALLS_SWAP], 1ull); }
               else { kv = 0; atomicAdd(&s.cnt[AUGSCHED_R_CALLS_DISCARD], 1ull); }
-              m = make_meta(seg, ST_PAUSED, (uint32_t)np, gen);
+              m = meta_with(m, ST_PAUSED, (uint32_t)np);
               const uint32_t q = atomicAdd(&s.n_pz, 1u);
               c.pz_id[q] = id;
               atomicMin(&s.min_ret, (unsigned long long)rt);
             }
           }
         }
-        if (!leave) m = make_meta(seg, ST_RUN, pol, gen);
-        c.ctx[id] = ctx; c.kv[id] = kv; c.cpu[id] = cpu; c.pend[id] = pend; c.meta[id] = m;
-        if (dA) atomicAdd((unsigned long long*)&s.A, (unsigned long long)dA);
-        if (dP) atomicAdd((unsigned long long*)&s.P, (unsigned long long)dP);
+        if (!leave) m = meta_with(m, ST_RUN, pol);
+        r.ctx = ctx; r.kv = kv; r.cpu = cpu; r.pend = pend; r.meta = m;
+        c.rs[id] = r;
+        accA += dA;
+        accP += dP;
         if (leave) {
           c.ac_id[i] = INVALID;
           const uint32_t hslot = atomicAdd(&s.n_holes, 1u);
@@ -590,8 +651,20 @@ __device__ void run_instance(const SimParams& p, SimShm& s, uint64_t* Ksm, uint3
           c.ac_dem[i] = demand_of(ctx, kv, cpu, pend, p.cfg.s_in);
         }
       }
-      if (my_tok) atomicAdd(&s.cnt[AUGSCHED_R_TOKENS], (unsigned long long)my_tok);
-      if (my_adm) atomicAdd(&s.cnt[AUGSCHED_R_ADMITTED], (unsigned long long)my_adm);
+      // one shared atomic per warp (64-bit shared atomicAdd is a CAS loop)
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        my_tok += __shfl_xor_sync(FULL, my_tok, o);
+        my_adm += __shfl_xor_sync(FULL, my_adm, o);
+        accA += __shfl_xor_sync(FULL, accA, o);
+        accP += __shfl_xor_sync(FULL, accP, o);
+      }
+      if ((tid & 31) == 0) {
+        if (my_tok) atomicAdd(&s.cnt[AUGSCHED_R_TOKENS], (unsigned long long)my_tok);
+        if (my_adm) atomicAdd(&s.cnt[AUGSCHED_R_ADMITTED], (unsigned long long)my_adm);
+        if (accA) atomicAdd((unsigned long long*)&s.A, (unsigned long long)accA);
+        if (accP) atomicAdd((unsigned long long*)&s.P, (unsigned long long)accP);
+      }
     }
     compact_active(c);  // syncs
     if (tid == 0) {
@@ -612,8 +685,8 @@ __device__ void run_instance(const SimParams& p, SimShm& s, uint64_t* Ksm, uint3
   augsched_result& out = p.out[inst];
   for (int f = tid; f < AUGSCHED_R_NFIELD; f += SIM_NT) { acc.f[f] = s.cnt[f]; out.f[f] = s.cnt[f]; }
   for (int b = tid; b < AUGSCHED_NBIN; b += SIM_NT) {
-    acc.hist_ttft[b] = s.hist_t[b]; out.hist_ttft[b] = s.hist_t[b];
-    acc.hist_norm[b] = s.hist_n[b]; out.hist_norm[b] = s.hist_n[b];
+    out.hist_ttft[b] = __ldcg(&acc.hist_ttft[b]);   // written by L2 atomics above
+    out.hist_norm[b] = __ldcg(&acc.hist_norm[b]);
   }
 }
 

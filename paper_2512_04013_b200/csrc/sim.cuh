@@ -20,8 +20,29 @@
 
 namespace augsched {
 
-constexpr int SIM_NT = 128;
-constexpr int SIM_MINB = 8;              // CTAs per SM the kernel is register-bounded for
+#ifndef AUGSCHED_SIM_NT
+#define AUGSCHED_SIM_NT 32
+#endif
+// One warp per CTA by default: an instance's per-step barriers are then
+// warp-local, and many more instances are resident per SM.
+constexpr int SIM_NT = AUGSCHED_SIM_NT;
+constexpr int SIM_RB = SIM_NT >= 256 ? 8 : 5;   // radix bits of the fallback select
+#ifndef AUGSCHED_SIM_CAND
+#define AUGSCHED_SIM_CAND 64
+#endif
+constexpr int SIM_CAND = AUGSCHED_SIM_CAND;      // small-candidate list capacity
+#ifndef AUGSCHED_SIM_SCAP
+#define AUGSCHED_SIM_SCAP 384
+#endif
+constexpr uint32_t SIM_SCAP = AUGSCHED_SIM_SCAP;  // queue entries whose step keys stay in shared memory
+#ifndef AUGSCHED_SIM_MINB
+#define AUGSCHED_SIM_MINB 16
+#endif
+#ifndef AUGSCHED_SIM_UNROLL
+#define AUGSCHED_SIM_UNROLL 2
+#endif
+constexpr int SIM_MINB = AUGSCHED_SIM_MINB;   // CTAs per SM the kernel is register-bounded for
+constexpr int SIM_UNROLL = AUGSCHED_SIM_UNROLL;  // queue entries in flight per thread in the key pass
 constexpr int SIM_NW = SIM_NT / 32;
 constexpr int KBITS = 50;                 // tier(2) | key(32) | id(16)
 constexpr uint64_t KMASK = (1ull << KBITS) - 1;
@@ -51,17 +72,24 @@ struct InstHdr {
   uint32_t started, pad;
 };
 
+// Mutable state of one request, packed in one 32-byte sector so the engine
+// advance of a granted entry is a single gather (two 16-byte loads).
+struct __align__(32) ReqState {
+  int32_t ctx;         // context tokens (prompt + generated + returned so far)
+  int32_t kv;          // tokens whose KV is on the GPU
+  int32_t cpu;         // tokens swapped out to host memory (Swap policy)
+  int32_t pend;        // tokens to prefill / assimilate (prompt or returned R)
+  uint32_t meta;       // seg:8 | status:4 | pol:4 | n_seg:8
+  uint32_t ft;         // first-token iteration (t+1 >= 1; 0 = none)
+  uint32_t lastc;      // last-scheduled iteration while paused (R14)
+  uint32_t left;       // tokens still to decode in the current segment
+};
+
 // Handle-owned per-instance arena (stride = max_active entries per instance).
 struct Arena {
   // cold state by request id
-  int32_t* ctx;
-  int32_t* kv;
-  int32_t* cpu;
-  int32_t* pend;
-  uint32_t* meta;      // seg:8 | status:4 | pol:4 | gen_done:16
+  ReqState* rs;
   uint64_t* ret;       // return tick of the outstanding call
-  uint32_t* ft;        // first-token iteration (t+1 >= 1; 0 = none)
-  uint32_t* lastc;     // last-scheduled iteration while paused (R14)
   // active list by position
   uint32_t* ac_id;     // id | tier << 30  (tier 0 running, 1 swapped, 2 waiting)
   double* ac_V;
@@ -95,9 +123,12 @@ struct SimParams {
 __device__ __forceinline__ uint32_t meta_seg(uint32_t m) { return m & 0xFF; }
 __device__ __forceinline__ uint32_t meta_st(uint32_t m) { return (m >> 8) & 0xF; }
 __device__ __forceinline__ uint32_t meta_pol(uint32_t m) { return (m >> 12) & 0xF; }
-__device__ __forceinline__ uint32_t meta_gen(uint32_t m) { return m >> 16; }
-__device__ __forceinline__ uint32_t make_meta(uint32_t seg, uint32_t st, uint32_t pol, uint32_t gen) {
-  return (seg & 0xFF) | (st << 8) | (pol << 12) | (gen << 16);
+__device__ __forceinline__ uint32_t meta_nseg(uint32_t m) { return (m >> 16) & 0xFF; }
+__device__ __forceinline__ uint32_t make_meta(uint32_t seg, uint32_t st, uint32_t pol, uint32_t nseg) {
+  return (seg & 0xFF) | (st << 8) | (pol << 12) | ((nseg & 0xFF) << 16);
+}
+__device__ __forceinline__ uint32_t meta_with(uint32_t m, uint32_t st, uint32_t pol) {
+  return (m & 0xFFFF00FFu) | (st << 8) | (pol << 12);
 }
 
 }  // namespace augsched

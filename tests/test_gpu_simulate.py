@@ -158,3 +158,41 @@ def test_cfg3_sampled_parity():
     keep = [i for i in range(len(oracle.FIELDS)) if i not in slo_fields]
     assert (f[:, :, keep] == f[:, :1, keep]).all()          # schedules identical across SLOs
     assert (np.diff(f[:, :, slo_fields[0]].astype(np.int64), axis=1) >= 0).all()
+
+
+def test_cfg2_parity():
+    """Config 2: one instance per request rate 1..8 req/s, 10,000 requests
+    each, full math/QA/web/chatbot tool mix (seed 2).
+    Every record byte-identical to the oracle's."""
+    tr = tracegen.gen_traces(8, 10_000, [1.0, 2.0, 3.0, 4.0, 5.0, 6.0, 7.0, 8.0], seed=2)
+    ip = tracegen.inst_params(8)
+    tid = np.arange(8, dtype=np.uint32)
+    g, _ = gpu_run(tracegen.PRESET_7B, ip, tr, tid)
+    o = oracle.simulate(tracegen.PRESET_7B, ip, tr, tid, threads=8)
+    assert_equal_records(g, o, "cfg2")
+
+
+def test_cfg5_bench_launch_sampled_parity():
+    """Config 5 at full size in the launch configuration bench.py times:
+    65,536 instances of 5,000-request traces, advanced in 1,500-iteration
+    resumable windows; a sample of instances is re-simulated by the oracle
+    for the same number of iterations and compared record by record."""
+    import bench
+    import argparse
+    args = argparse.Namespace(workload="cfg5", instances=65536)
+    tr, ip, tid, ma, _ = bench.workload(args, 0)
+    n = len(tid)
+    s = aug.Scheduler(tracegen.PRESET_7B, ip, n, ma)
+    dt = aug.DeviceTraces(tr)
+    tid_d = torch.from_numpy(tid.astype(np.int32)).cuda()
+    out = torch.empty(n * aug.RESULT_DTYPE.itemsize, dtype=torch.uint8, device="cuda")
+    W = 1500
+    for k in range(2):
+        s.simulate(dt, tid_d, (k + 1) * W, out=out, resume=k > 0)
+    g = aug.results_to_numpy(out)
+    s.sync()
+    s.close()
+    sample = np.concatenate([np.arange(16), np.arange(16, n, 4099)])
+    sub = {k: v[sample] for k, v in ip.items()}
+    o = oracle.simulate(tracegen.PRESET_7B, sub, tr, tid[sample], max_iters=2 * W, threads=16)
+    assert_equal_records(g[sample], o, "cfg5")
