@@ -21,6 +21,8 @@ struct __align__(16) SimShm {
   unsigned long long cnt[AUGSCHED_R_NFIELD];
   unsigned int holes[HOLE_CAP];
   unsigned int wtot[SIM_NW + 1];
+  Coef coef;                         // per-instance constants (§8(c).1)
+  augsched_instance_params ip;
   // instance scalars
   unsigned long long t, tT, min_ret, next_tick;
   long long A, P, A_snap, B, need, freev;
@@ -61,8 +63,8 @@ __device__ __forceinline__ uint32_t block_flag_scan(SimShm& s, bool f) {
 struct Ctx {
   const SimParams& p;
   SimShm& s;
-  Coef k;
-  augsched_instance_params ip;
+  const Coef& k;                        // in shared memory (keeps registers free)
+  const augsched_instance_params& ip;   // in shared memory
   // arena slices of this instance
   ReqState* rs;
   uint32_t *ac_id, *ac_last, *ac_dem, *pz_id;
@@ -219,9 +221,10 @@ __device__ void run_instance(const SimParams& p, SimShm& s, uint64_t* Ksm, uint3
   const int tid = threadIdx.x;
   const size_t off = (size_t)inst * p.max_active;
   const Arena& a = p.ar;
-  Ctx c{p, s, {}, p.ip[inst], a.rs + off, a.ac_id + off, a.ac_last + off, a.ac_dem + off, a.pz_id + off,
+  if (tid == 0) { s.coef = make_coef(p.cfg, p.ip[inst]); s.ip = p.ip[inst]; }
+  __syncthreads();
+  Ctx c{p, s, s.coef, s.ip, a.rs + off, a.ac_id + off, a.ac_last + off, a.ac_dem + off, a.pz_id + off,
         a.ret + off, a.ac_V + off, 0, 0, 0};
-  c.k = make_coef(p.cfg, c.ip);
   c.trace = p.inst_trace[inst];
   c.r0 = p.tr.req_off[c.trace];
   c.n = p.tr.req_off[c.trace + 1] - c.r0;

@@ -32,11 +32,11 @@ constexpr int SIM_RB = SIM_NT >= 256 ? 8 : 5;   // radix bits of the fallback se
 #endif
 constexpr int SIM_CAND = AUGSCHED_SIM_CAND;      // small-candidate list capacity
 #ifndef AUGSCHED_SIM_SCAP
-#define AUGSCHED_SIM_SCAP 384
+#define AUGSCHED_SIM_SCAP 0
 #endif
 constexpr uint32_t SIM_SCAP = AUGSCHED_SIM_SCAP;  // queue entries whose step keys stay in shared memory
 #ifndef AUGSCHED_SIM_MINB
-#define AUGSCHED_SIM_MINB 16
+#define AUGSCHED_SIM_MINB 24
 #endif
 #ifndef AUGSCHED_SIM_UNROLL
 #define AUGSCHED_SIM_UNROLL 2

@@ -9,9 +9,19 @@ namespace augsched {
 namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
-constexpr int SNT = 256;              // sort / per-instance kernels
-constexpr int SITEMS = 16;            // items per thread per sort tile
-constexpr int STILE = SNT * SITEMS;   // 4096 elements per tile
+#ifndef AUGSCHED_SORT_NT
+#define AUGSCHED_SORT_NT 256
+#endif
+#ifndef AUGSCHED_SORT_ITEMS
+#define AUGSCHED_SORT_ITEMS 16
+#endif
+#ifndef AUGSCHED_KEYS_MATCH
+#define AUGSCHED_KEYS_MATCH 0
+#endif
+constexpr int KNT = 256;                      // keys kernel threads
+constexpr int SNT = AUGSCHED_SORT_NT;         // sort-pass threads
+constexpr int SITEMS = AUGSCHED_SORT_ITEMS;   // items per thread per sort tile
+constexpr int STILE = SNT * SITEMS;           // elements per tile
 constexpr int SW = SNT / 32;
 
 __device__ __forceinline__ void flag_err(uint32_t* e, uint32_t bits) { atomicOr(e, bits); }
@@ -145,76 +155,105 @@ struct KeyArgs {
   augsched_config cfg;
   int64_t cap;
   uint64_t now;
-  uint32_t* k0;
-  uint32_t* v0;
+  unsigned long long* k0;
   uint32_t* ghist;
   uint32_t* n_active;
   long long* budget;
   int npass;
   PassDesc passes[STEP_MAX_PASS];
-  size_t N;
+  uint32_t N;
 };
 
-__device__ __forceinline__ int digit_of(uint32_t k, uint32_t v, const PassDesc& d, uint32_t MA) {
-  if (d.src == 0) return (int)((k >> d.shift) & 255u);
-  if (d.src == 1) return (int)(v >> 30);
-  return (int)((((v & 0x3FFFFFFFu) / MA) >> d.shift) & 255u);
+// Packed sort word of one slot: tier:2 | key:32 | slot:30 (tier 3 = not queued).
+constexpr int PK_KEY = 30;
+constexpr int PK_TIER = 62;
+constexpr uint32_t SLOT_MASK = (1u << 30) - 1;
+
+__device__ __forceinline__ uint32_t digit_of(unsigned long long x, const PassDesc& d, uint32_t MA) {
+  if (d.src == 0) return (uint32_t)(x >> d.shift) & ((1u << d.bits) - 1u);
+  return ((((uint32_t)x & SLOT_MASK) / MA) >> d.shift) & 255u;
 }
 
 // Score every slot (a4): key = orderable u32 of fp32(V - alpha*wait) for
-// queued slots (tier 0 running, 1 swapped, 2 waiting); empty / paused slots get
-// tier 3 and sort behind.  Payload = global slot | tier << 30.  Also the token
-// limit of each instance (a3) and the digit histograms of every sort pass.
-__global__ void __launch_bounds__(SNT) keys_kernel(KeyArgs a) {
-  __shared__ uint32_t h[STEP_MAX_PASS][256];
+// queued slots (tier 0 running, 1 swapped, 2 waiting); empty / paused slots
+// get tier 3 and sort behind their instance's queue.  Also the token limit of
+// each instance (a3), its queue size and the digit histograms of every sort
+// pass (warp-aggregated shared atomics).
+constexpr int KCNT = 1024;   // per-block instance-count table of the keys kernel
+
+__global__ void __launch_bounds__(KNT) keys_kernel(KeyArgs a) {
+  __shared__ uint32_t h[STEP_HIST_WORDS];
+  __shared__ uint32_t qcnt[KCNT];
   const int tid = threadIdx.x, lane = tid & 31;
-  for (int p = 0; p < a.npass; ++p) h[p][tid] = 0;
+  const int hw = a.passes[a.npass - 1].hoff + (1 << a.passes[a.npass - 1].bits);
+  for (int b = tid; b < hw; b += KNT) h[b] = 0;
+  for (int b = tid; b < KCNT; b += KNT) qcnt[b] = 0;
   __syncthreads();
   const uint32_t MA = a.S.MA;
-  for (size_t base = (size_t)blockIdx.x * SNT; base < a.N; base += (size_t)gridDim.x * SNT) {
-    const size_t s = base + tid;
-    bool valid = s < a.N;
-    uint32_t inst = 0, tier = 3, key = 0, v = 0;
+  // contiguous chunk per block: the instances it touches are contiguous, so
+  // their queue counts aggregate in shared memory (one global atomic per
+  // block and instance instead of one per warp)
+  const uint32_t chunk = (a.N + gridDim.x - 1) / gridDim.x;
+  const uint32_t c0 = blockIdx.x * chunk;
+  const uint32_t c1 = c0 + chunk < a.N ? c0 + chunk : a.N;
+  const uint32_t i0 = c0 / MA;
+  const bool local_cnt = c1 > c0 && (c1 - 1) / MA - i0 < (uint32_t)KCNT;
+  for (uint32_t base = c0; base < c1; base += KNT) {   // block-uniform trip count
+    const uint32_t s = base + tid;
+    const bool valid = s < c1;
+    uint32_t inst = 0, tier = 3, key = 0;
     if (valid) {
-      inst = (uint32_t)(s / MA);
+      inst = MA == a.N ? 0u : s / MA;
       const uint32_t stv = a.S.st[s] & 15;
       tier = (stv >= ST_RUN && stv <= ST_WAIT) ? stv - ST_RUN : 3u;
       if (tier < 3 && a.S.ip[inst].ranking != AUGSCHED_RANK_FCFS)
         key = sched_key(a.S.coef[inst], a.S.V[s], a.now, a.S.last[s]);
-      v = (uint32_t)s | (tier << 30);
-      a.k0[s] = key;
-      a.v0[s] = v;
-      if (s % MA == 0)
+      if (s == inst * MA)
         a.budget[inst] = token_limit(a.cfg, a.S.coef[inst], a.S.ip[inst], a.cap,
                                      ld_ll(&a.S.A[inst]), ld_ll(&a.S.P[inst]));
     }
+    const unsigned long long x = ((unsigned long long)tier << PK_TIER) |
+                                 ((unsigned long long)key << PK_KEY) | s;
+    if (valid) a.k0[s] = x;
     // queued count per instance (warp-aggregated)
     const bool q = valid && tier < 3;
-    const int gi = q ? (int)inst : -1;
-    const unsigned peers = __match_any_sync(FULL, gi);
-    if (q && lane == __ffs(peers) - 1) atomicAdd(&a.n_active[inst], (unsigned)__popc(peers));
+    const unsigned qm = __ballot_sync(FULL, q);
+    if (qm) {
+      const unsigned peers = __match_any_sync(FULL, q ? (int)inst : -1) & qm;
+      if (q && lane == __ffs(peers) - 1) {
+        if (local_cnt) atomicAdd(&qcnt[inst - i0], (unsigned)__popc(peers));
+        else atomicAdd(&a.n_active[inst], (unsigned)__popc(peers));
+      }
+    }
     for (int p = 0; p < a.npass; ++p) {
-      const int d = valid ? digit_of(key, v, a.passes[p], MA) : -1;
+      const int d = valid ? (int)digit_of(x, a.passes[p], MA) : -1;
+#if AUGSCHED_KEYS_MATCH
       const unsigned pe = __match_any_sync(FULL, d);
-      if (d >= 0 && lane == __ffs(pe) - 1) atomicAdd(&h[p][d], (unsigned)__popc(pe));
+      if (d >= 0 && lane == __ffs(pe) - 1) atomicAdd(&h[a.passes[p].hoff + d], (unsigned)__popc(pe));
+#else
+      if (d >= 0) atomicAdd(&h[a.passes[p].hoff + d], 1u);
+#endif
     }
   }
   __syncthreads();
-  for (int p = 0; p < a.npass; ++p)
-    if (h[p][tid]) atomicAdd(&a.ghist[p * 256 + tid], h[p][tid]);
+  for (int b = tid; b < hw; b += KNT)
+    if (h[b]) atomicAdd(&a.ghist[b], h[b]);
+  if (local_cnt)
+    for (uint32_t b = tid; b <= (c1 - 1) / MA - i0; b += KNT)
+      if (qcnt[b]) atomicAdd(&a.n_active[i0 + b], qcnt[b]);
 }
 
 // ------------------------------------------------------------------ sort pass
 struct SortArgs {
-  const uint32_t* kin;
-  const uint32_t* vin;
-  uint32_t* kout;
-  uint32_t* vout;
-  size_t n;
+  const unsigned long long* kin;
+  unsigned long long* kout;
+  uint32_t n;
   PassDesc d;
   uint32_t MA;
-  const uint32_t* ghist;        // this pass's 256 bins
-  unsigned long long* status;   // [tiles][256] look-back words
+  const uint32_t* ghist;        // this pass's bins
+  unsigned long long* status;   // [tiles][1 << RB] tile aggregates
+  unsigned long long* gstatus;  // [groups][1 << RB] group aggregates
+  uint32_t G;                   // tiles per group
   unsigned long long epoch;
   uint32_t* tile_ctr;
   int final_;                   // last pass: write order (local slot) and key
@@ -222,24 +261,64 @@ struct SortArgs {
   uint32_t* keyout;
 };
 
-// One stable LSD counting-sort pass over an 8-bit digit.  Tile = 4,096
-// elements; each warp ranks its contiguous 512-element segment with
+constexpr int LB_BATCH = 8;     // aggregate words loaded together by one thread
+
+// Spin until every word of a strided run carries this pass's epoch; return
+// the sum of their counts (the low 32 bits).
+__device__ __forceinline__ uint32_t sum_published(volatile unsigned long long* base, uint32_t count,
+                                                  size_t stride, unsigned long long ep) {
+  uint32_t total = 0;
+  for (uint32_t k0 = 0; k0 < count; k0 += LB_BATCH) {
+    unsigned long long w[LB_BATCH];
+    bool ok;
+    do {
+#pragma unroll
+      for (int k = 0; k < LB_BATCH; ++k)
+        w[k] = k0 + k < count ? base[(size_t)(k0 + k) * stride] : (ep << 34);
+      ok = true;
+#pragma unroll
+      for (int k = 0; k < LB_BATCH; ++k) ok &= (w[k] >> 34) == ep;
+    } while (!ok);
+#pragma unroll
+    for (int k = 0; k < LB_BATCH; ++k) total += k0 + k < count ? (uint32_t)w[k] : 0u;
+  }
+  return total;
+}
+
+// One stable LSD counting-sort pass over a digit of RB bits.  Tile = SNT x
+// SITEMS elements; each warp ranks its contiguous segment with
 // __match_any_sync and warp-private digit counters, one barrier combines
-// warps, and the tile's digit offsets come from a decoupled look-back over
-// preceding tiles (tile ids handed out in launch order by an atomic counter).
+// warps.  The tile's digit offsets come from a two-level aggregate
+// look-back with no serial chain: every tile publishes its digit counts, the
+// last tile of each group of G tiles publishes the group's counts, and tile
+// t (group g) sums the aggregates of groups < g and of the tiles before it in
+// its own group (<= 2*sqrt(tiles) independent loads per digit).  Tile ids are
+// handed out in launch order by an atomic counter, so every awaited tile has
+// started.
+template <int RB>
 __global__ void __launch_bounds__(SNT) sort_pass_kernel(SortArgs a) {
-  __shared__ uint32_t bin_off[256];
-  __shared__ uint32_t wcnt[SW][256];
-  __shared__ uint32_t tbase[256];
+  constexpr int NB = 1 << RB;
+  constexpr int DPT = NB / SNT > 0 ? NB / SNT : 1;   // digits per thread
+  __shared__ uint32_t bin_off[NB];
+  __shared__ uint32_t wcnt[SW][NB];
+  __shared__ uint32_t tbase[NB];
   __shared__ uint32_t wtot[SW];
   __shared__ uint32_t tile_s;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) tile_s = atomicAdd(a.tile_ctr, 1u);
-  for (int w = 0; w < SW; ++w) wcnt[w][tid] = 0;
-  // exclusive scan of the global digit histogram (256 bins, one per thread)
+  for (int w = 0; w < SW; ++w)
+    for (int b = tid; b < NB; b += SNT) wcnt[w][b] = 0;
+  // exclusive scan of the global digit histogram: thread tid owns bins
+  // [tid*DPT, tid*DPT + DPT)
   {
-    const uint32_t x = a.ghist[tid];
-    uint32_t inc = x;
+    uint32_t loc[DPT], sum = 0;
+#pragma unroll
+    for (int j = 0; j < DPT; ++j) {
+      const int b = tid * DPT + j;
+      loc[j] = b < NB ? a.ghist[b] : 0u;
+      sum += loc[j];
+    }
+    uint32_t inc = sum;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const uint32_t y = __shfl_up_sync(FULL, inc, o);
@@ -247,23 +326,28 @@ __global__ void __launch_bounds__(SNT) sort_pass_kernel(SortArgs a) {
     }
     if (lane == 31) wtot[warp] = inc;
     __syncthreads();
-    uint32_t wb = 0;
-    for (int w = 0; w < warp; ++w) wb += wtot[w];
-    bin_off[tid] = wb + inc - x;
+    uint32_t run = inc - sum;
+    for (int w = 0; w < warp; ++w) run += wtot[w];
+#pragma unroll
+    for (int j = 0; j < DPT; ++j) {
+      const int b = tid * DPT + j;
+      if (b < NB) bin_off[b] = run;
+      run += loc[j];
+    }
   }
-  const size_t tile = tile_s;
-  const size_t seg = tile * STILE + (size_t)warp * (32 * SITEMS);
-  uint32_t kk[SITEMS], vv[SITEMS], rk[SITEMS];
+  const uint32_t tile = tile_s;
+  const size_t seg = (size_t)tile * STILE + (size_t)warp * (32 * SITEMS);
+  unsigned long long kk[SITEMS];
+  uint32_t rk[SITEMS];
   int dg[SITEMS];
 #pragma unroll
   for (int r = 0; r < SITEMS; ++r) {
     const size_t idx = seg + (size_t)r * 32 + lane;
     if (idx < a.n) {
       kk[r] = a.kin[idx];
-      vv[r] = a.vin[idx];
-      dg[r] = digit_of(kk[r], vv[r], a.d, a.MA);
+      dg[r] = (int)digit_of(kk[r], a.d, a.MA);
     } else {
-      kk[r] = 0; vv[r] = 0; dg[r] = -1;
+      kk[r] = 0; dg[r] = -1;
     }
   }
   __syncthreads();  // wcnt cleared, bin_off ready
@@ -271,62 +355,57 @@ __global__ void __launch_bounds__(SNT) sort_pass_kernel(SortArgs a) {
 #pragma unroll
   for (int r = 0; r < SITEMS; ++r) {
     const unsigned peers = __match_any_sync(FULL, dg[r]);
-    if (dg[r] >= 0) {
-      rk[r] = wcnt[warp][dg[r]] + __popc(peers & lt);
-    }
+    if (dg[r] >= 0) rk[r] = wcnt[warp][dg[r]] + __popc(peers & lt);
     __syncwarp();
     if (dg[r] >= 0 && lane == __ffs(peers) - 1) wcnt[warp][dg[r]] += __popc(peers);
     __syncwarp();
   }
   __syncthreads();
-  // per digit (thread tid): exclusive offsets of the warps, tile count
-  uint32_t cnt = 0;
-  for (int w = 0; w < SW; ++w) {
-    const uint32_t c = wcnt[w][tid];
-    wcnt[w][tid] = cnt;
-    cnt += c;
-  }
-  // decoupled look-back: flag 1 = tile aggregate, 2 = inclusive prefix
+  // per digit: exclusive offsets of the warps, tile count, decoupled look-back
   volatile unsigned long long* st = a.status;
-  const unsigned long long ep = a.epoch << 34;
-  if (tile == 0) {
-    st[tid] = ep | (2ull << 32) | cnt;
-    tbase[tid] = 0;
-  } else {
-    st[tile * 256 + tid] = ep | (1ull << 32) | cnt;
-    uint32_t excl = 0;
-    size_t t = tile - 1;
-    for (;;) {
-      const unsigned long long w = st[t * 256 + tid];
-      if ((w >> 34) != a.epoch) continue;
-      excl += (uint32_t)w;
-      if (((w >> 32) & 3ull) == 2ull) break;
-      --t;
+  volatile unsigned long long* gst = a.gstatus;
+  const unsigned long long ep = a.epoch;
+#pragma unroll
+  for (int j = 0; j < DPT; ++j) {
+    const int d = tid * DPT + j;
+    if (d >= NB) break;
+    uint32_t cnt = 0;
+    for (int w = 0; w < SW; ++w) {
+      const uint32_t c = wcnt[w][d];
+      wcnt[w][d] = cnt;
+      cnt += c;
     }
-    tbase[tid] = excl;
-    st[tile * 256 + tid] = ep | (2ull << 32) | (excl + cnt);
+    // aggregate word: epoch << 34 | count
+    st[(size_t)tile * NB + d] = (ep << 34) | cnt;
+    const uint32_t g = tile / a.G, t0 = g * a.G;
+    if (tile == t0 + a.G - 1 || tile == gridDim.x - 1)   // last tile of its group
+      gst[(size_t)g * NB + d] = (ep << 34) | (sum_published(st + (size_t)t0 * NB + d, tile - t0, NB, ep) + cnt);
+    const uint32_t excl = sum_published(gst + d, g, NB, ep) +
+                          sum_published(st + (size_t)t0 * NB + d, tile - t0, NB, ep);
+    tbase[d] = excl;
   }
   __syncthreads();
 #pragma unroll
   for (int r = 0; r < SITEMS; ++r) {
     if (dg[r] < 0) continue;
     const uint32_t d = (uint32_t)dg[r];
-    const size_t pos = (size_t)bin_off[d] + tbase[d] + wcnt[warp][d] + rk[r];
+    const uint32_t pos = bin_off[d] + tbase[d] + wcnt[warp][d] + rk[r];
     if (a.final_) {
-      const uint32_t gsl = vv[r] & 0x3FFFFFFFu;
+      const uint32_t gsl = (uint32_t)kk[r] & SLOT_MASK;
       a.order[pos] = gsl - (gsl / a.MA) * a.MA;
-      a.keyout[pos] = kk[r];
+      a.keyout[pos] = (uint32_t)(kk[r] >> PK_KEY);
     } else {
       a.kout[pos] = kk[r];
-      a.vout[pos] = vv[r];
     }
   }
 }
 
 // ------------------------------------------------------------------ block scan helpers
+template <int NT>
 __device__ __forceinline__ unsigned long long block_incl_scan_u64(unsigned long long x,
                                                                   unsigned long long* wsum,
                                                                   unsigned long long* total) {
+  constexpr int NW = NT / 32;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   unsigned long long inc = x;
 #pragma unroll
@@ -337,9 +416,10 @@ __device__ __forceinline__ unsigned long long block_incl_scan_u64(unsigned long 
   if (lane == 31) wsum[warp] = inc;
   __syncthreads();
   unsigned long long base = 0, tot = 0;
-  for (int w = 0; w < SW; ++w) {
-    if (w < warp) base += wsum[w];
-    tot += wsum[w];
+  for (int w = 0; w < NW; ++w) {
+    const unsigned long long v = wsum[w];
+    if (w < warp) base += v;
+    tot += v;
   }
   *total = tot;
   __syncthreads();
@@ -350,128 +430,113 @@ __device__ __forceinline__ uint32_t slot_demand(const Slots& S, uint32_t g, uint
   return demand_of(S.ctx[g], S.kv[g], S.cpu[g], S.pend[g], s_in);
 }
 
-// a6: per instance, grants of the admitted prefix (P_{j-1} < B, partial last)
-__global__ void __launch_bounds__(SNT) admit_kernel(Slots S, augsched_config cfg, int64_t cap,
+constexpr int ANT = 512;    // threads of the per-instance admission kernel
+constexpr int ANW = ANT / 32;
+
+// One block per instance, after the sort:
+//   a6  grants of the admitted prefix (P_{j-1} < B, partial last, R17)
+//   a7  (rare) demote Preserve-paused KV (kv desc, slot asc), then evict from
+//       the tail of the order over entries with kv + g > 0, until the grants
+//       fit the free KV memory (R20)
+//   S9  last = now and the granted batch's token accounting (decode adds one
+//       token; the engine reports segment ends with CALL / FINISH records)
+__global__ void __launch_bounds__(ANT) admit_kernel(Slots S, augsched_config cfg, int64_t cap, uint64_t now,
                                                     const long long* budget, const uint32_t* n_active,
                                                     const uint32_t* order, uint32_t* grant,
-                                                    uint32_t* admitted, long long* need, uint32_t* flag) {
-  __shared__ unsigned long long wsum[SW];
+                                                    uint32_t* admitted) {
+  __shared__ unsigned long long wsum[ANW];
+  __shared__ SelShm sel;
+  __shared__ unsigned long long freed;
+  __shared__ uint32_t adm_s;
   const uint32_t i = blockIdx.x;
+  const int tid = threadIdx.x;
   const uint32_t MA = S.MA;
   const size_t base = (size_t)i * MA;
   const long long B = budget[i];
   const uint32_t n = n_active[i];
+  // ---- a6 admission
   unsigned long long Prun = 0, gsum = 0;
   uint32_t adm = 0;
-  for (uint32_t j0 = 0; j0 < n && (long long)Prun < B; j0 += SNT) {
-    const uint32_t j = j0 + threadIdx.x;
+  for (uint32_t j0 = 0; j0 < n && (long long)Prun < B; j0 += ANT) {
+    const uint32_t j = j0 + tid;
     unsigned long long d = 0;
     if (j < n) d = slot_demand(S, (uint32_t)(base + order[base + j]), cfg.s_in);
     unsigned long long tot;
-    const unsigned long long inc = block_incl_scan_u64(d, wsum, &tot);
+    const unsigned long long inc = block_incl_scan_u64<ANT>(d, wsum, &tot);
     const unsigned long long ex = Prun + inc - d;
-    if (j < n && (long long)ex < B) {
+    const bool in = j < n && (long long)ex < B;
+    if (in) {
       const unsigned long long g = d < (unsigned long long)B - ex ? d : (unsigned long long)B - ex;
       grant[base + j] = (uint32_t)g;
       gsum += g;
     }
-    const uint32_t c = __syncthreads_count(j < n && (long long)ex < B);
-    adm += c;
+    adm += __syncthreads_count(in);
     Prun += tot;
   }
-  // block-reduce the granted tokens
-  unsigned long long tot;
-  block_incl_scan_u64(gsum, wsum, &tot);
-  if (threadIdx.x == 0) {
-    admitted[i] = adm;
-    need[i] = (long long)tot;
-    const long long fr = cap - ld_ll(&S.A[i]) - ld_ll(&S.P[i]);
-    flag[i] = (long long)tot > fr ? 1u : 0u;
-  }
-}
-
-// a7 (rare): demote Preserve-paused KV (kv desc, slot asc), then evict from
-// the tail of the order over entries with kv + g > 0, until the grants fit.
-__global__ void __launch_bounds__(SNT) resolve_kernel(Slots S, int64_t cap, const uint32_t* n_active,
-                                                      const uint32_t* order, uint32_t* grant,
-                                                      const uint32_t* admitted, const long long* need,
-                                                      const uint32_t* flag) {
-  __shared__ SelShm sel;
-  __shared__ unsigned long long freed;
-  const uint32_t i = blockIdx.x;
-  if (!flag[i]) return;
-  const uint32_t MA = S.MA;
-  const size_t base = (size_t)i * MA;
-  const long long nd = need[i];
+  unsigned long long need;
+  block_incl_scan_u64<ANT>(gsum, wsum, &need);
   long long fr = cap - ld_ll(&S.A[i]) - ld_ll(&S.P[i]);
-  if (threadIdx.x == 0) freed = 0;
-  // (1) demotion
-  auto getp = [&](uint32_t x, uint64_t& key, uint32_t& w) {
-    const size_t g = base + x;
-    const uint32_t stv = S.st[g];
-    const int32_t kv = S.kv[g];
-    if ((stv & 15) != ST_PAUSED || ((stv >> 4) & 3) != POL_P || kv <= 0) return false;
-    key = ((uint64_t)(0xFFFFFFFFu - (uint32_t)kv) << 24) | x;
-    w = (uint32_t)kv;
-    return true;
-  };
-  wselect<SNT>(sel, MA, (uint64_t)(nd - fr), 56, getp);
-  {
-    const bool f0 = sel.r.found != 0;
-    const uint64_t k0 = sel.r.k;
-    for (uint32_t x = threadIdx.x; x < MA; x += SNT) {
-      uint64_t key;
-      uint32_t w;
-      if (getp(x, key, w) && (!f0 || key <= k0)) {
-        const size_t g = base + x;
-        atomicAdd(&freed, (unsigned long long)w);
-        S.kv[g] = 0;
-        S.st[g] = ST_PAUSED | ((uint32_t)POL_D << 4);
+  // ---- a7 resolution (rare)
+  if ((long long)need > fr) {
+    if (tid == 0) freed = 0;
+    auto getp = [&](uint32_t x, uint64_t& key, uint32_t& w) {
+      const size_t g = base + x;
+      const uint32_t stv = S.st[g];
+      const int32_t kv = S.kv[g];
+      if ((stv & 15) != ST_PAUSED || ((stv >> 4) & 3) != POL_P || kv <= 0) return false;
+      key = ((uint64_t)(0xFFFFFFFFu - (uint32_t)kv) << 24) | x;
+      w = (uint32_t)kv;
+      return true;
+    };
+    wselect<ANT>(sel, MA, (uint64_t)((long long)need - fr), 56, getp);
+    {
+      const bool f0 = sel.r.found != 0;
+      const uint64_t k0 = sel.r.k;
+      for (uint32_t x = tid; x < MA; x += ANT) {
+        uint64_t key;
+        uint32_t w;
+        if (getp(x, key, w) && (!f0 || key <= k0)) {
+          const size_t g = base + x;
+          atomicAdd(&freed, (unsigned long long)w);
+          S.kv[g] = 0;
+          S.st[g] = ST_PAUSED | ((uint32_t)POL_D << 4);
+        }
       }
     }
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) ledger_add(&S.P[i], -(long long)freed);
-  fr += (long long)freed;
-  __syncthreads();
-  if (nd <= fr) return;
-  // (2) tail eviction
-  const uint32_t n = n_active[i], adm = admitted[i];
-  auto gete = [&](uint32_t j, uint64_t& key, uint32_t& w) {
-    const size_t g = base + order[base + j];
-    w = (uint32_t)S.kv[g] + (j < adm ? grant[base + j] : 0u);
-    key = (uint64_t)(n - 1 - j);
-    return w > 0;
-  };
-  wselect<SNT>(sel, n, (uint64_t)(nd - fr), 24, gete);
-  const bool f1 = sel.r.found != 0;
-  const uint64_t k1 = sel.r.k;
-  long long dA = 0;
-  for (uint32_t j = threadIdx.x; j < n; j += SNT) {
-    uint64_t key;
-    uint32_t w;
-    if (gete(j, key, w) && (!f1 || key <= k1)) {
-      const size_t g = base + order[base + j];
-      dA -= S.kv[g];
-      S.kv[g] = 0;
-      S.cpu[g] = 0;
-      S.st[g] = ST_WAIT | (S.st[g] & 0x30u);
-      if (j < adm) grant[base + j] = 0;
+    __syncthreads();
+    if (tid == 0) ledger_add(&S.P[i], -(long long)freed);
+    fr += (long long)freed;
+    if ((long long)need > fr) {
+      auto gete = [&](uint32_t j, uint64_t& key, uint32_t& w) {
+        const size_t g = base + order[base + j];
+        w = (uint32_t)S.kv[g] + (j < adm ? grant[base + j] : 0u);
+        key = (uint64_t)(n - 1 - j);
+        return w > 0;
+      };
+      wselect<ANT>(sel, n, (uint64_t)((long long)need - fr), 24, gete);
+      const bool f1 = sel.r.found != 0;
+      const uint64_t k1 = sel.r.k;
+      __syncthreads();
+      long long dA = 0;
+      for (uint32_t j = tid; j < n; j += ANT) {
+        uint64_t key;
+        uint32_t w;
+        if (gete(j, key, w) && (!f1 || key <= k1)) {
+          const size_t g = base + order[base + j];
+          dA -= S.kv[g];
+          S.kv[g] = 0;
+          S.cpu[g] = 0;
+          S.st[g] = ST_WAIT | (S.st[g] & 0x30u);
+          if (j < adm) grant[base + j] = 0;
+        }
+      }
+      if (dA) ledger_add(&S.A[i], dA);
     }
   }
-  if (dA) ledger_add(&S.A[i], dA);
-}
-
-// S9 + token accounting of the granted batch (decode adds one token; the
-// engine reports segment ends with CALL / FINISH records).
-__global__ void __launch_bounds__(SNT) apply_kernel(Slots S, uint64_t now, const uint32_t* order,
-                                                    const uint32_t* grant, const uint32_t* admitted) {
-  __shared__ unsigned long long wsum[SW];
-  const uint32_t i = blockIdx.x;
-  const size_t base = (size_t)i * S.MA;
-  const uint32_t adm = admitted[i];
+  __syncthreads();   // grants final, ledger updates visible in the block
+  // ---- S9 + token accounting
   unsigned long long dA = 0;
-  for (uint32_t j = threadIdx.x; j < adm; j += SNT) {
+  for (uint32_t j = tid; j < adm; j += ANT) {
     const uint32_t gr = grant[base + j];
     if (gr == 0) continue;
     const size_t g = base + order[base + j];
@@ -489,8 +554,9 @@ __global__ void __launch_bounds__(SNT) apply_kernel(Slots S, uint64_t now, const
     S.st[g] = ST_RUN | (S.st[g] & 0x30u);
   }
   unsigned long long tot;
-  block_incl_scan_u64(dA, wsum, &tot);
-  if (threadIdx.x == 0) {
+  block_incl_scan_u64<ANT>(dA, wsum, &tot);
+  if (tid == 0) {
+    admitted[i] = adm;
     const long long a = ld_ll(&S.A[i]) + (long long)tot;
     S.A[i] = a;
     S.Aevt[i] = a;
@@ -572,6 +638,21 @@ int step_ensure(StepState& st, uint32_t n_inst, uint32_t max_active, cudaStream_
   st.max_active = max_active;
   st.N = N;
   st.n_tiles = (uint32_t)((N + STILE - 1) / STILE);
+  // digit passes (LSD): key bits 0-7, 8-15, 16-23, then key bits 24-31 with
+  // the tier above them (10 bits), then the instance bytes
+  st.npass = 0;
+  int hoff = 0;
+  auto add = [&](int src, int shift, int bits) {
+    st.passes[st.npass++] = PassDesc{src, shift, bits, hoff};
+    hoff += 1 << bits;
+  };
+  add(0, PK_KEY, 8);
+  add(0, PK_KEY + 8, 8);
+  add(0, PK_KEY + 16, 8);
+  add(0, PK_KEY + 24, 10);
+  for (uint32_t x = n_inst - 1, b = 0; x > 0; x >>= 8, ++b) add(2, (int)(8 * b), 8);
+  if (hoff > STEP_HIST_WORDS) return set_error(AUGSCHED_E_CAPACITY, "step: too many sort passes");
+  const size_t zwords = (size_t)n_inst + STEP_HIST_WORDS + STEP_MAX_PASS;
   int rc;
   if ((rc = salloc(st, &st.st, N)) || (rc = salloc(st, &st.V, N)) || (rc = salloc(st, &st.last, N)) ||
       (rc = salloc(st, &st.ctx, N)) || (rc = salloc(st, &st.kv, N)) || (rc = salloc(st, &st.cpu, N)) ||
@@ -579,15 +660,18 @@ int step_ensure(StepState& st, uint32_t n_inst, uint32_t max_active, cudaStream_
       (rc = salloc(st, &st.P, n_inst)) || (rc = salloc(st, &st.Aevt, n_inst)) ||
       (rc = salloc(st, &st.Asnap, n_inst)) || (rc = salloc(st, &st.need, n_inst)) ||
       (rc = salloc(st, &st.coef, n_inst)) || (rc = salloc(st, &st.budget, n_inst)) ||
-      (rc = salloc(st, &st.n_active, n_inst)) || (rc = salloc(st, &st.admitted, n_inst)) ||
+      (rc = salloc(st, &st.zbuf, zwords)) || (rc = salloc(st, &st.admitted, n_inst)) ||
       (rc = salloc(st, &st.flag, n_inst)) || (rc = salloc(st, &st.order, N)) ||
       (rc = salloc(st, &st.grant, N)) || (rc = salloc(st, &st.key, N)) ||
-      (rc = salloc(st, &st.k0, N)) || (rc = salloc(st, &st.v0, N)) || (rc = salloc(st, &st.k1, N)) ||
-      (rc = salloc(st, &st.v1, N)) ||
-      (rc = salloc(st, &st.lb_status, (size_t)st.n_tiles * 256)) ||
-      (rc = salloc(st, &st.ghist, STEP_MAX_PASS * 256)) ||
-      (rc = salloc(st, &st.tile_ctr, STEP_MAX_PASS)))
+      (rc = salloc(st, &st.k0, N)) || (rc = salloc(st, &st.k1, N)) ||
+      (rc = salloc(st, &st.lb_status, (size_t)st.n_tiles << STEP_RB_MAX)) ||
+      (rc = salloc(st, &st.lb_gstatus, (size_t)st.n_tiles << STEP_RB_MAX)))
     return rc;
+  // one memset per step clears the queue counts, histograms and tile counters
+  st.zwords = zwords;
+  st.n_active = st.zbuf;
+  st.ghist = st.zbuf + n_inst;
+  st.tile_ctr = st.ghist + STEP_HIST_WORDS;
   cudaMemsetAsync(st.st, 0, sizeof(uint32_t) * N, s);
   cudaMemsetAsync(st.ctx, 0, sizeof(int32_t) * N, s);
   cudaMemsetAsync(st.kv, 0, sizeof(int32_t) * N, s);
@@ -596,14 +680,15 @@ int step_ensure(StepState& st, uint32_t n_inst, uint32_t max_active, cudaStream_
   cudaMemsetAsync(st.A, 0, sizeof(long long) * n_inst, s);
   cudaMemsetAsync(st.P, 0, sizeof(long long) * n_inst, s);
   cudaMemsetAsync(st.Aevt, 0, sizeof(long long) * n_inst, s);
-  cudaMemsetAsync(st.lb_status, 0, sizeof(unsigned long long) * st.n_tiles * 256, s);
+  cudaMemsetAsync(st.lb_status, 0, sizeof(unsigned long long) * ((size_t)st.n_tiles << STEP_RB_MAX), s);
+  cudaMemsetAsync(st.lb_gstatus, 0, sizeof(unsigned long long) * ((size_t)st.n_tiles << STEP_RB_MAX), s);
+  st.G = 1;
+  while ((uint64_t)st.G * st.G < st.n_tiles) ++st.G;   // ~sqrt(tiles) tiles per look-back group
   coef_kernel<<<(n_inst + 255) / 256, 256, 0, s>>>(cfg, d_ip, st.coef, n_inst);
   *launches += 1;
-  // digit passes: 4 key bytes, the tier, then the instance bytes (LSD)
-  st.npass = 0;
-  for (int b = 0; b < 4; ++b) st.passes[st.npass++] = PassDesc{0, 8 * b};
-  st.passes[st.npass++] = PassDesc{1, 0};
-  for (uint32_t x = n_inst - 1, b = 0; x > 0; x >>= 8, ++b) st.passes[st.npass++] = PassDesc{2, (int)(8 * b)};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&st.sms, cudaDevAttrMultiProcessorCount, dev);
   st.epoch = 0;
   st.ready = true;
   return cuda_check(cudaGetLastError(), "step_ensure");
@@ -662,39 +747,34 @@ int step_run(StepState& st, const augsched_config& cfg, int64_t cap,
     *launches += 3;
     st.r_n = 0;
   }
-  cudaMemsetAsync(st.n_active, 0, sizeof(uint32_t) * ni, s);
-  cudaMemsetAsync(st.ghist, 0, sizeof(uint32_t) * STEP_MAX_PASS * 256, s);
-  cudaMemsetAsync(st.tile_ctr, 0, sizeof(uint32_t) * STEP_MAX_PASS, s);
+  cudaMemsetAsync(st.zbuf, 0, sizeof(uint32_t) * st.zwords, s);
   KeyArgs ka;
-  ka.S = S; ka.cfg = cfg; ka.cap = cap; ka.now = now; ka.k0 = st.k0; ka.v0 = st.v0;
+  ka.S = S; ka.cfg = cfg; ka.cap = cap; ka.now = now; ka.k0 = st.k0;
   ka.ghist = st.ghist; ka.n_active = st.n_active; ka.budget = st.budget; ka.npass = st.npass;
   for (int p = 0; p < st.npass; ++p) ka.passes[p] = st.passes[p];
-  ka.N = st.N;
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const size_t kblocks = (st.N + SNT - 1) / SNT;
-  const int kgrid = (int)(kblocks < (size_t)sms * 8 ? kblocks : (size_t)sms * 8);
-  keys_kernel<<<kgrid, SNT, 0, s>>>(ka);
+  ka.N = (uint32_t)st.N;
+  const size_t kblocks = (st.N + KNT - 1) / KNT;
+  // few fat blocks: each zeroes and flushes ~2K histogram bins once
+  const int kgrid = (int)(kblocks < (size_t)st.sms * 2 ? kblocks : (size_t)st.sms * 2);
+  keys_kernel<<<kgrid, KNT, 0, s>>>(ka);
   *launches += 1;
-  uint32_t *kin = st.k0, *vin = st.v0, *kout = st.k1, *vout = st.v1;
+  unsigned long long *kin = st.k0, *kout = st.k1;
   for (int p = 0; p < st.npass; ++p) {
     SortArgs sa;
-    sa.kin = kin; sa.vin = vin; sa.kout = kout; sa.vout = vout; sa.n = st.N; sa.d = st.passes[p];
-    sa.MA = st.max_active; sa.ghist = st.ghist + p * 256; sa.status = st.lb_status;
-    sa.epoch = ++st.epoch; sa.tile_ctr = st.tile_ctr + p; sa.final_ = p == st.npass - 1;
+    sa.kin = kin; sa.kout = kout; sa.n = (uint32_t)st.N; sa.d = st.passes[p];
+    sa.MA = st.max_active; sa.ghist = st.ghist + st.passes[p].hoff; sa.status = st.lb_status;
+    sa.gstatus = st.lb_gstatus; sa.G = st.G;
+    sa.epoch = ++st.epoch & ((1ull << 30) - 1); sa.tile_ctr = st.tile_ctr + p;
+    sa.final_ = p == st.npass - 1;
     sa.order = st.order; sa.keyout = st.key;
-    sort_pass_kernel<<<st.n_tiles, SNT, 0, s>>>(sa);
+    if (st.passes[p].bits == 10) sort_pass_kernel<10><<<st.n_tiles, SNT, 0, s>>>(sa);
+    else sort_pass_kernel<8><<<st.n_tiles, SNT, 0, s>>>(sa);
     *launches += 1;
-    uint32_t* t = kin; kin = kout; kout = t;
-    t = vin; vin = vout; vout = t;
+    unsigned long long* t = kin; kin = kout; kout = t;
   }
-  admit_kernel<<<ni, SNT, 0, s>>>(S, cfg, cap, st.budget, st.n_active, st.order, st.grant,
-                                  st.admitted, st.need, st.flag);
-  resolve_kernel<<<ni, SNT, 0, s>>>(S, cap, st.n_active, st.order, st.grant, st.admitted, st.need,
-                                    st.flag);
-  apply_kernel<<<ni, SNT, 0, s>>>(S, now, st.order, st.grant, st.admitted);
-  *launches += 3;
+  admit_kernel<<<ni, ANT, 0, s>>>(S, cfg, cap, now, st.budget, st.n_active, st.order, st.grant,
+                                  st.admitted);
+  *launches += 1;
   out->budget = reinterpret_cast<const int64_t*>(st.budget);
   out->n_active = st.n_active;
   out->admitted = st.admitted;

@@ -2,11 +2,16 @@
 // One step (Algorithm 1, for every instance at once):
 //   [records]  CALL/FINISH -> snapshot -> RETURN (Stage II) / NEW (Stage I) / IMPORT
 //   keys       Eq.26 key per slot + token limit (Eq.27-32) + digit histograms
-//   sort       stable LSD radix sort of (instance, tier, key) with slot-id
-//              payload, one kernel per 8-bit digit, decoupled look-back
-//   admit      block prefix scan of demand over each instance's order (R17)
-//   resolve    demotion + tail eviction when the grants exceed free KV (R20)
-//   apply      last = now and the granted batch's token accounting
+//              of every sort pass; writes one packed u64 per slot:
+//              tier:2 | key:32 | slot:30 (most significant first)
+//   sort       stable LSD radix sort of (instance, tier, key) with the slot
+//              id carried in the low bits: 8+8+8 key bits, then a 10-bit
+//              digit (top key byte + tier), then instance bytes; one kernel
+//              per digit with a two-level (group / tile) aggregate look-back
+//   admit      one block per instance: prefix scan of demand over the order
+//              (R17), demotion + tail eviction when the grants exceed free
+//              KV (R20), then last = now and the granted batch's token
+//              accounting
 #pragma once
 #include <cuda_runtime.h>
 #include <cstdint>
@@ -16,10 +21,14 @@
 namespace augsched {
 
 constexpr int STEP_MAX_PASS = 8;
+constexpr int STEP_RB_MAX = 10;                 // widest digit (bins = 1 << bits)
+constexpr int STEP_HIST_WORDS = 4 * 256 + 1024 + 3 * 256;  // bins over all passes (<= 8)
 
 struct PassDesc {
-  int src;    // 0: byte of the u32 key, 1: tier (payload >> 30), 2: byte of the instance index
+  int src;    // 0: `bits` bits of the packed key at `shift`; 2: byte of the instance index
   int shift;
+  int bits;
+  int hoff;   // offset of this pass's bins in the histogram array
 };
 
 struct StepState {
@@ -44,14 +53,19 @@ struct StepState {
   uint32_t *n_active = nullptr, *admitted = nullptr, *order = nullptr, *grant = nullptr,
            *key = nullptr, *flag = nullptr;
   // sort scratch
-  uint32_t *k0 = nullptr, *v0 = nullptr, *k1 = nullptr, *v1 = nullptr;
-  unsigned long long* lb_status = nullptr;
-  uint32_t* ghist = nullptr;      // [STEP_MAX_PASS][256]
+  unsigned long long *k0 = nullptr, *k1 = nullptr;   // packed tier:2 | key:32 | slot:30
+  unsigned long long* lb_status = nullptr;           // [tiles][1 << STEP_RB_MAX] tile aggregates
+  unsigned long long* lb_gstatus = nullptr;          // [groups][1 << STEP_RB_MAX] group aggregates
+  uint32_t G = 1;                                    // tiles per look-back group
+  uint32_t* ghist = nullptr;      // [STEP_HIST_WORDS]
   uint32_t* tile_ctr = nullptr;   // [STEP_MAX_PASS]
   unsigned long long epoch = 0;
   int npass = 0;
   PassDesc passes[STEP_MAX_PASS];
   uint32_t n_tiles = 0;
+  uint32_t* zbuf = nullptr;       // [n_inst | STEP_HIST_WORDS | STEP_MAX_PASS], zeroed every step
+  size_t zwords = 0;
+  int sms = 148;
   void* alloc_list[64];
   int n_alloc = 0;
 };
