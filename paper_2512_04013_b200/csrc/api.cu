@@ -128,10 +128,9 @@ int ensure_sim(augsched_t* h) {
       (rc = h->alloc(&a.ac_V, N)) || (rc = h->alloc(&a.ac_last, N)) ||
       (rc = h->alloc(&a.ac_dem, N)) || (rc = h->alloc(&a.pz_id, N)) ||
       (rc = h->alloc(&a.kscr, N)) || (rc = h->alloc(&a.wscr, N)) ||
+      (rc = h->alloc(&a.kscr2, N)) || (rc = h->alloc(&a.wscr2, N)) ||
       (rc = h->alloc(&h->d_hdr, h->n_inst)) || (rc = h->alloc(&h->d_acc, h->n_inst)))
     return rc;
-  a.kscr2 = nullptr;
-  a.wscr2 = nullptr;
   // shared-memory queue capacity and persistent grid
   h->scap = h->max_active < SIM_SCAP ? h->max_active : SIM_SCAP;
   h->sim_smem = sim_smem_bytes(h->scap);

@@ -216,6 +216,23 @@ __device__ void compact_paused(Ctx& c) {
   __syncthreads();
 }
 
+// Selections, kept out of line: one instantiation of each serves every call
+// site (the hot loop stays small in the instruction cache).
+// Weighted radix select over arrays: key K[i] (or KMASK - K[i] when rev),
+// weight W[i]; entries with weight 0 are skipped.
+__device__ __noinline__ void select_arr(SimShm& s, const uint64_t* K, const uint32_t* W, uint32_t n,
+                                        uint64_t D, int nbits, bool rev) {
+  wselect<SIM_NT, SIM_RB>(s.u.b, s.res, n, D, nbits, [&](uint32_t i, uint64_t& key, uint32_t& w) {
+    w = W[i];
+    key = rev ? KMASK - K[i] : K[i];
+    return w > 0;
+  });
+}
+
+__device__ __noinline__ void select_cand(SimShm& s, int list, int m, uint64_t D, uint64_t w0) {
+  rank_select<SIM_NT, SIM_CAND>(s.u.c, list, s.res, m, D, w0);
+}
+
 __device__ void run_instance(const SimParams& p, SimShm& s, uint64_t* Ksm, uint32_t* Wsm,
                              uint32_t inst) {
   const int tid = threadIdx.x;
@@ -411,9 +428,9 @@ __device__ void run_instance(const SimParams& p, SimShm& s, uint64_t* Ksm, uint3
         if (tid == 0) { s.res.found = 0; s.res.total = w0 + w1 + w2; }    // everything admitted
         done = true;
       } else if (w0 >= Bu) {
-        if (s.tc[0] <= SIM_CAND) { rank_select<SIM_NT, SIM_CAND>(s.u.c, 0, s.res, (int)s.tc[0], Bu, 0); done = true; }
+        if (s.tc[0] <= SIM_CAND) { select_cand(s, 0, (int)s.tc[0], Bu, 0); done = true; }
       } else if (w0 + w1 >= Bu) {
-        if (s.tc[1] <= SIM_CAND) { rank_select<SIM_NT, SIM_CAND>(s.u.c, 1, s.res, (int)s.tc[1], Bu, w0); done = true; }
+        if (s.tc[1] <= SIM_CAND) { select_cand(s, 1, (int)s.tc[1], Bu, w0); done = true; }
       } else {
         // waiting tier: pop the smallest remaining waiting keys in order, one
         // per round (one barrier each).  Every thread offers its smallest
@@ -462,10 +479,7 @@ __device__ void run_instance(const SimParams& p, SimShm& s, uint64_t* Ksm, uint3
           }
         }
       }
-      if (!done) {
-        wselect<SIM_NT, SIM_RB>(s.u.b, s.res, na, Bu, KBITS, [&](uint32_t i, uint64_t& key, uint32_t& w) {
-          key = K[i]; w = W[i]; return true; });
-      }
+      if (!done) select_arr(s, K, W, na, Bu, KBITS, false);
       __syncthreads();
     }
     const bool found = s.res.found != 0;
@@ -503,8 +517,19 @@ __device__ void run_instance(const SimParams& p, SimShm& s, uint64_t* Ksm, uint3
         }
       }
       __syncthreads();
-      if (s.tc[0] <= SIM_CAND) rank_select<SIM_NT, SIM_CAND>(s.u.c, 0, s.res, (int)s.tc[0], D0, 0);
-      else wselect<SIM_NT, SIM_RB>(s.u.b, s.res, npz, D0, 48, getp);
+      if (s.tc[0] <= SIM_CAND) select_cand(s, 0, (int)s.tc[0], D0, 0);
+      else {
+        // many Preserve-paused contexts: materialise (key, kv) and select over the arrays
+        uint64_t* K2 = a.kscr2 + off;
+        uint32_t* W2 = a.wscr2 + off;
+        for (uint32_t i = tid; i < npz; i += SIM_NT) {
+          uint64_t key = 0; uint32_t w = 0;
+          if (!getp(i, key, w)) w = 0;
+          K2[i] = key; W2[i] = w;
+        }
+        __syncthreads();
+        select_arr(s, K2, W2, npz, D0, 48, false);
+      }
       {
         const bool f0 = s.res.found != 0;
         const uint64_t k0 = s.res.k;
@@ -541,8 +566,8 @@ __device__ void run_instance(const SimParams& p, SimShm& s, uint64_t* Ksm, uint3
           key = KMASK - K[i];
           return w > 0;
         };
-        if (s.tc[1] <= SIM_CAND) rank_select<SIM_NT, SIM_CAND>(s.u.c, 1, s.res, (int)s.tc[1], D1, 0);
-        else wselect<SIM_NT, SIM_RB>(s.u.b, s.res, na, D1, KBITS, gete);
+        if (s.tc[1] <= SIM_CAND) select_cand(s, 1, (int)s.tc[1], D1, 0);
+        else select_arr(s, K, W, na, D1, KBITS, true);
         const bool f1 = s.res.found != 0;
         const uint64_t k1 = s.res.k;
         for (uint32_t i = tid; i < na; i += SIM_NT) {
@@ -693,7 +718,7 @@ __device__ void run_instance(const SimParams& p, SimShm& s, uint64_t* Ksm, uint3
   }
 }
 
-__global__ void __launch_bounds__(SIM_NT, SIM_MINB) sim_kernel(SimParams p) {
+__global__ void __launch_bounds__(SIM_NT, SIM_MINB) sim_kernel(const __grid_constant__ SimParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   SimShm& s = *reinterpret_cast<SimShm*>(smem_raw);
   uint64_t* Ksm = reinterpret_cast<uint64_t*>(smem_raw + ((sizeof(SimShm) + 15) & ~size_t(15)));
