@@ -13,7 +13,7 @@
 #include "step.cuh"
 
 namespace augsched {
-size_t sim_smem_bytes(uint32_t scap);
+size_t sim_smem_bytes();
 const void* sim_kernel_ptr();
 cudaError_t launch_sim(const SimParams& p, int grid, size_t smem, cudaStream_t st);
 }  // namespace augsched
@@ -67,7 +67,6 @@ struct augsched_handle {
   InstHdr* d_hdr = nullptr;
   augsched_result* d_acc = nullptr;
   bool sim_ready = false;
-  uint32_t scap = 0;
   int sim_grid = 0;
   size_t sim_smem = 0;
   // host-trace staging (AUGSCHED_HOST_TRACES)
@@ -124,16 +123,16 @@ int ensure_sim(augsched_t* h) {
   const size_t N = (size_t)h->n_inst * h->max_active;
   Arena& a = h->ar;
   int rc;
-  if ((rc = h->alloc(&a.rs, N)) || (rc = h->alloc(&a.ret, N)) || (rc = h->alloc(&a.ac_id, N)) ||
-      (rc = h->alloc(&a.ac_V, N)) || (rc = h->alloc(&a.ac_last, N)) ||
-      (rc = h->alloc(&a.ac_dem, N)) || (rc = h->alloc(&a.pz_id, N)) ||
+  if ((rc = h->alloc(&a.rs, N)) || (rc = h->alloc(&a.ret, N)) || (rc = h->alloc(&a.r_id, N)) ||
+      (rc = h->alloc(&a.r_V, N)) || (rc = h->alloc(&a.r_last, N)) || (rc = h->alloc(&a.r_dem, N)) ||
+      (rc = h->alloc(&a.w_id, N)) || (rc = h->alloc(&a.w_V, N)) || (rc = h->alloc(&a.w_last, N)) ||
+      (rc = h->alloc(&a.w_dem, N)) || (rc = h->alloc(&a.pz_id, N)) ||
       (rc = h->alloc(&a.kscr, N)) || (rc = h->alloc(&a.wscr, N)) ||
       (rc = h->alloc(&a.kscr2, N)) || (rc = h->alloc(&a.wscr2, N)) ||
       (rc = h->alloc(&h->d_hdr, h->n_inst)) || (rc = h->alloc(&h->d_acc, h->n_inst)))
     return rc;
   // shared-memory queue capacity and persistent grid
-  h->scap = h->max_active < SIM_SCAP ? h->max_active : SIM_SCAP;
-  h->sim_smem = sim_smem_bytes(h->scap);
+  h->sim_smem = sim_smem_bytes();
   CUDA_TRY(cudaFuncSetAttribute(sim_kernel_ptr(), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)h->sim_smem));
   int per_sm = 0, sms = 0;
@@ -299,7 +298,6 @@ int augsched_simulate(augsched_t* h, const augsched_trace* traces, const uint32_
   p.max_iters = max_iters;
   p.n_inst = h->n_inst;
   p.max_active = h->max_active;
-  p.scap = h->scap;
   p.work = h->d_work;
   p.err = h->d_err;
   const int grid = (int)(h->n_inst < (uint32_t)h->sim_grid ? h->n_inst : (uint32_t)h->sim_grid);

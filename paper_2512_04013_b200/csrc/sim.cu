@@ -1,11 +1,24 @@
 // augsched_simulate: persistent per-instance simulation kernel for sm_100a.
 // See sim.cuh for the design; the per-step sequence follows DESIGN.md §"Step
 // sequence" (S1..S12), i.e. Algorithm 1 plus the engine model.
+//
+// The queue of an instance is held as two lists: R (running u swapped, tiers
+// 0 and 1 of P:1221) and W (waiting_resume u waiting_new, tier 2, R16).  The
+// order is (tier, key, id), so every R entry precedes every W entry and a
+// step only needs the keys of the tier where the admission prefix ends:
+//   - R keys are always computed (R is small: what fits in KV memory);
+//   - W keys are computed only when the prefix reaches W, and then only the
+//     smallest few matter: each lane keeps its two smallest W keys and the
+//     block pops the global minimum round by round (one barrier per round)
+//     until the popped demand reaches the limit;
+//   - the grant / engine-advance loop touches R and the popped W entries only.
 #include <cuda_runtime.h>
 #include "sim.cuh"
 #include "select.cuh"
 
 namespace augsched {
+
+constexpr int MAXPOP = 32;   // pop rounds before falling back to a radix select over W
 
 struct __align__(16) SimShm {
   union {
@@ -13,23 +26,38 @@ struct __align__(16) SimShm {
     CandShmT<SIM_CAND> c;            // small candidate lists (fast path)
   } u;
   SelRes res;
-  unsigned long long tw[3];          // per-tier demand (clamped to B) of the step
-  unsigned int tc[3];                // per-tier queue counts of the step
-  unsigned long long rk[2][SIM_NW];  // waiting-tier pop rounds: per-warp smallest key
-  unsigned int rw[2][SIM_NW];        //   and its demand (double-buffered by round parity)
+  unsigned long long tw[3];          // per-tier demand of the step (unclamped)
+  unsigned int tc[3];                // per-tier candidate counts of the step
+  unsigned long long rk[2][SIM_NW];  // pop rounds: per-warp smallest key, its demand and
+  unsigned int rw[2][SIM_NW];        //   W position (double-buffered by round parity)
+  unsigned int rp[2][SIM_NW];
+  unsigned long long pk[MAXPOP];     // popped W entries of the step: key (| KEVICT if
+  unsigned int pw[MAXPOP];           //   its grant was cancelled), demand, W position
+  unsigned int pp[MAXPOP];
+  unsigned int npop;
+  int wmode;                         // which W entries the step grants (see WMODE_*)
+  int wkeys;                         // W keys materialised in kscr[nR ..]
   int due;                           // intake or idle handling needed this iteration
   unsigned long long cnt[AUGSCHED_R_NFIELD];
-  unsigned int holes[HOLE_CAP];
+  unsigned int holes[2][HOLE_CAP];   // hole positions of R (0) and W (1)
+  unsigned int nholes[2];
   unsigned int wtot[SIM_NW + 1];
   Coef coef;                         // per-instance constants (§8(c).1)
   augsched_instance_params ip;
   // instance scalars
   unsigned long long t, tT, min_ret, next_tick;
-  long long A, P, A_snap, B, need, freev;
+  long long A, P, A_snap, B;
   unsigned long long freed;
-  unsigned int next_arr, n_act, n_pz, n_fin, n_holes, n_pholes, wpos;
-  unsigned int inst, n_req, r0;
+  unsigned int next_arr, n_r, n_w, n_pz, n_fin, wpos;
+  unsigned int inst;
   int run, idle;
+};
+
+enum : int {
+  WMODE_NONE = 0,   // the prefix ends in R (or B <= 0): no W entry is granted
+  WMODE_POP = 1,    // the popped W entries s.pk/pw/pp are granted
+  WMODE_ALL = 2,    // everything fits: every W entry is granted in full
+  WMODE_KEY = 3,    // fallback: W keys materialised, grant by the key rule
 };
 
 namespace {
@@ -55,11 +83,17 @@ __device__ __forceinline__ uint32_t block_flag_scan(SimShm& s, bool f) {
   return s.wtot[warp] + __popc(b & ((1u << lane) - 1));
 }
 
-// Weighted MSD radix select.  Among items i < n for which get(i, key, w)
-// returns true (w >= 1, keys unique, key < 2^nbits) find the smallest key k*
-// with sum_{key <= k*} w >= D.  Results: s.sel.found (1 found / 0 not: then
-// s.sel.total holds the full weight), s.sel.k, s.sel.wbelow = sum_{key < k*} w.
-// Weights are clamped to D (exact: every item before k* has w < D).
+// One queue list (SoA by position).
+struct List {
+  uint32_t* id;     // request id | tier << 30; INVALID marks a hole
+  double* V;        // value (Stage I / II / final), fixed between events
+  uint32_t* last;   // last-scheduled iteration (R14)
+  uint32_t* dem;    // demand of the next grant (R17, R18)
+  __device__ __forceinline__ void put(uint32_t pos, uint32_t e, double v, uint32_t l, uint32_t d) const {
+    id[pos] = e; V[pos] = v; last[pos] = l; dem[pos] = d;
+  }
+};
+
 struct Ctx {
   const SimParams& p;
   SimShm& s;
@@ -67,9 +101,13 @@ struct Ctx {
   const augsched_instance_params& ip;   // in shared memory
   // arena slices of this instance
   ReqState* rs;
-  uint32_t *ac_id, *ac_last, *ac_dem, *pz_id;
+  List R, W;
+  uint32_t* pz_id;
   uint64_t* ret;
-  double* ac_V;
+  uint64_t* K;      // step keys: R at [0, nR), W (when materialised) at [nR, nR + nW)
+  uint32_t* Ws;     // step weights, same layout
+  uint64_t* K2;     // secondary selections
+  uint32_t* W2;
   uint32_t r0, n, trace;
 };
 
@@ -78,6 +116,11 @@ __device__ __forceinline__ uint32_t gen_total(const DevTrace& tr, uint32_t rid) 
   uint32_t g = 0;
   for (uint32_t q = 0; q < ns; ++q) g += tr.gen_true[s0 + q];
   return g;
+}
+
+// Composite order key (tier, score key, id): unique, < 2^KBITS.
+__device__ __forceinline__ uint64_t order_key(uint32_t e, uint32_t key) {
+  return ((uint64_t)(e >> 30) << 48) | ((uint64_t)key << 16) | (e & 0xFFFF);
 }
 
 // S2: one returned call (Algorithm 1 lines 10-24).
@@ -110,15 +153,13 @@ __device__ void do_return(Ctx& c, uint32_t id) {
   r.left = tr.gen_true[s0 + kk + 1];
   c.rs[id] = r;
   atomicAdd(&s.cnt[AUGSCHED_R_RETURNS], 1ull);
-  const uint32_t pos = atomicAdd(&s.n_act, 1u);
-  c.ac_id[pos] = id | (tier << 30);
-  c.ac_V[pos] = V;
-  c.ac_last[pos] = r.lastc;  // not reset on return (R14)
-  c.ac_dem[pos] = demand_of(ctx, kv, cpu, (int32_t)R, c.p.cfg.s_in);
+  const uint32_t dem = demand_of(ctx, kv, cpu, (int32_t)R, c.p.cfg.s_in);
+  // last is not reset on return (R14)
+  if (tier < 2) c.R.put(atomicAdd(&s.n_r, 1u), id | (tier << 30), V, r.lastc, dem);
+  else c.W.put(atomicAdd(&s.n_w, 1u), id | (2u << 30), V, r.lastc, dem);
 }
 
-
-// S3: arrival of request `id` at active position `pos` (Algorithm 1 lines 2-9).
+// S3: arrival of request `id` at W position `pos` (Algorithm 1 lines 2-9).
 __device__ void do_arrival(Ctx& c, uint32_t id, uint32_t pos, uint64_t t) {
   const DevTrace& tr = c.p.tr;
   const uint32_t rid = c.r0 + id;
@@ -136,63 +177,62 @@ __device__ void do_arrival(Ctx& c, uint32_t id, uint32_t pos, uint64_t t) {
   r.ft = 0; r.lastc = 0;
   r.left = tr.gen_true[s0];
   c.rs[id] = r;
-  c.ac_id[pos] = id | (2u << 30);
-  c.ac_V[pos] = V;
-  c.ac_last[pos] = (uint32_t)t;           // R14, R31
-  c.ac_dem[pos] = (uint32_t)L;
+  c.W.put(pos, id | (2u << 30), V, (uint32_t)t, (uint32_t)L);   // R14, R31
 }
 
-// Remove the active entries whose ac_id was set to INVALID.
-__device__ void compact_active(Ctx& c) {
-  SimShm& s = c.s;
+// Remove the entries of list `L` (0 = R, 1 = W) whose id is INVALID.
+__device__ void compact_list(SimShm& s, const List& l, int L, unsigned int& n_ref) {
   const int tid = threadIdx.x;
   __syncthreads();
-  if (s.n_holes == 0) return;
-  if (s.n_holes <= HOLE_CAP) {
+  const uint32_t nh = s.nholes[L];
+  if (nh == 0) return;
+  if (nh <= HOLE_CAP) {
     if (tid == 0) {
-      const uint32_t L = s.n_holes, n = s.n_act, n_new = n - L;
-      uint32_t* h = s.holes;
-      for (uint32_t a = 1; a < L; ++a) {  // insertion sort (L small)
+      const uint32_t n = n_ref, n_new = n - nh;
+      uint32_t* h = s.holes[L];
+      for (uint32_t a = 1; a < nh; ++a) {  // insertion sort (few holes)
         uint32_t x = h[a];
         int b = (int)a - 1;
         while (b >= 0 && h[b] > x) { h[b + 1] = h[b]; --b; }
         h[b + 1] = x;
       }
-      int j = (int)L - 1;
+      int j = (int)nh - 1;
       int src = (int)n - 1;
-      for (uint32_t a = 0; a < L; ++a) {
+      for (uint32_t a = 0; a < nh; ++a) {
         const uint32_t hp = h[a];
         if (hp >= n_new) break;
         while (j >= 0 && (int)h[j] == src) { --j; --src; }
-        c.ac_id[hp] = c.ac_id[src];
-        c.ac_V[hp] = c.ac_V[src];
-        c.ac_last[hp] = c.ac_last[src];
-        c.ac_dem[hp] = c.ac_dem[src];
+        l.put(hp, l.id[src], l.V[src], l.last[src], l.dem[src]);
         --src;
       }
-      s.n_act = n_new;
+      n_ref = n_new;
+      s.nholes[L] = 0;
     }
     __syncthreads();
     return;
   }
   // many removals: in-place tiled stream compaction
   if (tid == 0) s.wpos = 0;
-  const uint32_t n = s.n_act;
+  const uint32_t n = n_ref;
   for (uint32_t base = 0; base < n; base += SIM_NT) {
     const uint32_t i = base + tid;
     uint32_t id = INVALID, last = 0, dem = 0;
     double V = 0;
-    if (i < n) { id = c.ac_id[i]; if (id != INVALID) { V = c.ac_V[i]; last = c.ac_last[i]; dem = c.ac_dem[i]; } }
+    if (i < n) { id = l.id[i]; if (id != INVALID) { V = l.V[i]; last = l.last[i]; dem = l.dem[i]; } }
     const bool keep = id != INVALID;
     const uint32_t pre = block_flag_scan(s, keep);  // syncs: all reads of the tile are done
-    const uint32_t w = s.wpos + pre;
-    if (keep) { c.ac_id[w] = id; c.ac_V[w] = V; c.ac_last[w] = last; c.ac_dem[w] = dem; }
+    if (keep) l.put(s.wpos + pre, id, V, last, dem);
     __syncthreads();
     if (tid == 0) s.wpos += s.wtot[SIM_NW];
     __syncthreads();
   }
-  if (tid == 0) s.n_act = s.wpos;
+  if (tid == 0) { n_ref = s.wpos; s.nholes[L] = 0; }
   __syncthreads();
+}
+
+__device__ __forceinline__ void mark_hole(SimShm& s, int L, uint32_t pos) {
+  const uint32_t h = atomicAdd(&s.nholes[L], 1u);
+  if (h < HOLE_CAP) s.holes[L][h] = pos;
 }
 
 // Remove paused entries marked INVALID (small list; tiled compaction).
@@ -233,15 +273,32 @@ __device__ __noinline__ void select_cand(SimShm& s, int list, int m, uint64_t D,
   rank_select<SIM_NT, SIM_CAND>(s.u.c, list, s.res, m, D, w0);
 }
 
-__device__ void run_instance(const SimParams& p, SimShm& s, uint64_t* Ksm, uint32_t* Wsm,
-                             uint32_t inst) {
+// Grant rule of the step (R17): full demand before k*, the remainder at k*,
+// nothing after it or for an entry whose grant was cancelled (KEVICT).
+struct GrantRule {
+  long long B;
+  uint64_t kstar, wb;
+  bool found;
+  __device__ __forceinline__ uint32_t operator()(uint64_t Ki, uint32_t dem) const {
+    if (Ki & KEVICT) return 0u;
+    if (B <= 0) return 0u;
+    if (!found || Ki < kstar) return dem;
+    if (Ki == kstar) return (uint32_t)((uint64_t)B - wb);
+    return 0u;
+  }
+};
+
+__device__ void run_instance(const SimParams& p, SimShm& s, uint32_t inst) {
   const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
   const size_t off = (size_t)inst * p.max_active;
   const Arena& a = p.ar;
   if (tid == 0) { s.coef = make_coef(p.cfg, p.ip[inst]); s.ip = p.ip[inst]; }
   __syncthreads();
-  Ctx c{p, s, s.coef, s.ip, a.rs + off, a.ac_id + off, a.ac_last + off, a.ac_dem + off, a.pz_id + off,
-        a.ret + off, a.ac_V + off, 0, 0, 0};
+  Ctx c{p, s, s.coef, s.ip, a.rs + off,
+        List{a.r_id + off, a.r_V + off, a.r_last + off, a.r_dem + off},
+        List{a.w_id + off, a.w_V + off, a.w_last + off, a.w_dem + off},
+        a.pz_id + off, a.ret + off, a.kscr + off, a.wscr + off, a.kscr2 + off, a.wscr2 + off, 0, 0, 0};
   c.trace = p.inst_trace[inst];
   c.r0 = p.tr.req_off[c.trace];
   c.n = p.tr.req_off[c.trace + 1] - c.r0;
@@ -258,17 +315,22 @@ __device__ void run_instance(const SimParams& p, SimShm& s, uint64_t* Ksm, uint3
   // ---- load (or initialise) the resumable state -------------------------
   if (tid == 0) {
     if (!H.started) {
-      H.t = 0; H.A = 0; H.P = 0; H.min_ret = ~0ull; H.next_arr = 0; H.n_act = 0; H.n_pz = 0;
+      H.t = 0; H.A = 0; H.P = 0; H.min_ret = ~0ull; H.next_arr = 0; H.n_r = 0; H.n_w = 0; H.n_pz = 0;
       H.n_fin = 0; H.started = 1;
     }
     s.t = H.t; s.A = H.A; s.P = H.P; s.min_ret = H.min_ret; s.next_arr = H.next_arr;
-    s.n_act = H.n_act; s.n_pz = H.n_pz; s.n_fin = H.n_fin;
+    s.n_r = H.n_r; s.n_w = H.n_w; s.n_pz = H.n_pz; s.n_fin = H.n_fin;
+    s.nholes[0] = s.nholes[1] = 0;
     s.next_tick = s.next_arr < n ? p.tr.arr_tick[c.r0 + s.next_arr] : ~0ull;
   }
   for (int f = tid; f < AUGSCHED_R_NFIELD; f += SIM_NT) s.cnt[f] = acc.f[f];
   __syncthreads();
   if (tid == 0) s.cnt[AUGSCHED_R_NREQ] = n;
   const int64_t cap = p.cap;
+  const bool fcfs = c.ip.ranking == AUGSCHED_RANK_FCFS;
+  auto key_of = [&](double V, uint64_t t, uint32_t last) -> uint32_t {
+    return fcfs ? 0u : sched_key(c.k, V, t, last);
+  };
 
   // thread 0 prepares iteration s.t: stop rule, S1 snapshot, whether intake
   // or the idle jump must run, and (when no intake is due) the token limit.
@@ -276,11 +338,11 @@ __device__ void run_instance(const SimParams& p, SimShm& s, uint64_t* Ksm, uint3
     s.run = (s.n_fin < n) && (s.t < p.max_iters);
     s.tT = s.t * T;
     s.A_snap = s.A;
-    s.n_holes = 0;
-    s.due = s.n_act == 0 || s.tT >= s.min_ret || s.tT >= s.next_tick;
+    s.due = s.n_r + s.n_w == 0 || s.tT >= s.min_ret || s.tT >= s.next_tick;
     if (!s.due) s.B = token_limit(p.cfg, c.k, c.ip, cap, s.A, s.P);
     s.tw[0] = s.tw[1] = s.tw[2] = 0;
     s.tc[0] = s.tc[1] = s.tc[2] = 0;
+    s.wkeys = 0;
   };
   if (tid == 0) prep();
   __syncthreads();
@@ -307,10 +369,10 @@ __device__ void run_instance(const SimParams& p, SimShm& s, uint64_t* Ksm, uint3
         const uint32_t j = s.next_arr + tid;
         const bool arrive = j < n && p.tr.arr_tick[c.r0 + j] <= tT;
         const int cnt = __syncthreads_count(arrive);
-        if (arrive) do_arrival(c, j, s.n_act + tid, t);
+        if (arrive) do_arrival(c, j, s.n_w + tid, t);
         __syncthreads();
         if (tid == 0) {
-          s.n_act += cnt; s.next_arr += cnt; s.cnt[AUGSCHED_R_ARRIVED] += cnt;
+          s.n_w += cnt; s.next_arr += cnt; s.cnt[AUGSCHED_R_ARRIVED] += cnt;
           if (cnt < SIM_NT) s.next_tick = s.next_arr < n ? p.tr.arr_tick[c.r0 + s.next_arr] : ~0ull;
         }
         __syncthreads();
@@ -319,7 +381,7 @@ __device__ void run_instance(const SimParams& p, SimShm& s, uint64_t* Ksm, uint3
       // ---- idle jump (not counted) or S4 token limit ---------------------------
       if (tid == 0) {
         s.idle = 0;
-        if (s.n_act == 0) {
+        if (s.n_r + s.n_w == 0) {
           uint64_t te = ~0ull;
           if (s.next_arr < n) te = (p.tr.arr_tick[c.r0 + s.next_arr] + T - 1) / T;
           if (s.n_pz > 0) { const uint64_t tr_ = (s.min_ret + T - 1) / T; te = tr_ < te ? tr_ : te; }
@@ -332,65 +394,36 @@ __device__ void run_instance(const SimParams& p, SimShm& s, uint64_t* Ksm, uint3
       __syncthreads();
       if (s.idle) continue;
     }
-    // ---- S5 keys, per-tier demand, running/swapped candidate lists -----------
-    const uint32_t na = s.n_act;
+    const uint32_t nR = s.n_r, nW = s.n_w, na = nR + nW;
     const long long B = s.B;
-    const uint32_t Bc = B > 0 ? (uint32_t)B : 0u;
-    const bool in_smem = na <= p.scap;
-    uint64_t* K = in_smem ? Ksm : a.kscr + off;
-    uint32_t* W = in_smem ? Wsm : a.wscr + off;
-    const bool fcfs = c.ip.ranking == AUGSCHED_RANK_FCFS;
-    // This thread's two smallest waiting-tier keys (and demands): the first
-    // candidates of the pop rounds below.
-    uint64_t c1 = ~0ull, c2 = ~0ull;
-    uint32_t cw1 = 0, cw2 = 0;
+    const unsigned long long Bu = B > 0 ? (unsigned long long)B : 0ull;
+    const unsigned lt = (1u << lane) - 1;
+    // ---- S5 keys of R, per-tier demand, running / swapped candidate lists ----
     {
-      unsigned long long tw0 = 0, tw1 = 0, tw2 = 0;
-      constexpr int U = SIM_UNROLL;  // entries in flight per thread (independent L2 loads)
-      const int lane = tid & 31;
-      const unsigned lt = (1u << lane) - 1;
-      // warp-uniform trip count (the candidate lists use warp ballots)
-      for (uint32_t b0 = 0; b0 < na; b0 += SIM_NT * U) {
-        uint32_t e[U], l[U], d[U];
-        double V[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const uint32_t i = b0 + u * SIM_NT + tid;
-          if (i < na) { e[u] = c.ac_id[i]; V[u] = c.ac_V[i]; l[u] = c.ac_last[i]; d[u] = c.ac_dem[i]; }
+      unsigned long long tw0 = 0, tw1 = 0;
+      for (uint32_t b0 = 0; b0 < nR; b0 += SIM_NT) {   // warp-uniform trip count
+        const uint32_t i = b0 + tid;
+        uint32_t tier = 3, d = 0;
+        uint64_t Ki = 0;
+        if (i < nR) {
+          const uint32_t e = c.R.id[i];
+          d = c.R.dem[i];
+          tier = e >> 30;
+          Ki = order_key(e, key_of(c.R.V[i], t, c.R.last[i]));
+          c.K[i] = Ki;
+          c.Ws[i] = d;
+          if (tier == 0) tw0 += d; else tw1 += d;
         }
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const uint32_t i = b0 + u * SIM_NT + tid;
-          uint32_t tier = 3;
-          uint64_t Ki = 0;
-          if (i < na) {
-            tier = e[u] >> 30;
-            const uint32_t key = fcfs ? 0u : sched_key(c.k, V[u], t, l[u]);
-            Ki = ((uint64_t)tier << 48) | ((uint64_t)key << 16) | (e[u] & 0xFFFF);
-            K[i] = Ki;
-            W[i] = d[u];
-            const uint32_t dc = d[u] < Bc ? d[u] : Bc;
-            if (tier == 2) {
-              tw2 += dc;
-              if (Ki < c2) {
-                if (Ki < c1) { c2 = c1; cw2 = cw1; c1 = Ki; cw1 = d[u]; }
-                else { c2 = Ki; cw2 = d[u]; }
-              }
-            } else if (tier == 0) tw0 += dc;
-            else tw1 += dc;
-          }
-          // running / swapped candidate lists, one shared atomic per warp and tier
-#pragma unroll
-          for (uint32_t tt = 0; tt < 2; ++tt) {
-            const unsigned m = __ballot_sync(FULL, tier == tt);
-            if (m) {
-              const int leader = __ffs(m) - 1;
-              uint32_t q0 = 0;
-              if (lane == leader) q0 = atomicAdd(&s.tc[tt], (unsigned)__popc(m));
-              q0 = __shfl_sync(FULL, q0, leader);
-              const uint32_t q = q0 + __popc(m & lt);
-              if (tier == tt && q < SIM_CAND) { s.u.c.ck[tt][q] = Ki; s.u.c.cw[tt][q] = d[u]; }
-            }
+        for (uint32_t tt = 0; tt < 2; ++tt) {
+          const unsigned m = __ballot_sync(FULL, tier == tt);
+          if (m) {
+            const int leader = __ffs(m) - 1;
+            uint32_t q0 = 0;
+            if (lane == leader) q0 = atomicAdd(&s.tc[tt], (unsigned)__popc(m));
+            q0 = __shfl_sync(FULL, q0, leader);
+            const uint32_t q = q0 + __popc(m & lt);
+            if (tier == tt && q < SIM_CAND) { s.u.c.ck[tt][q] = Ki; s.u.c.cw[tt][q] = d; }
           }
         }
       }
@@ -398,12 +431,10 @@ __device__ void run_instance(const SimParams& p, SimShm& s, uint64_t* Ksm, uint3
       for (int o = 16; o > 0; o >>= 1) {
         tw0 += __shfl_xor_sync(FULL, tw0, o);
         tw1 += __shfl_xor_sync(FULL, tw1, o);
-        tw2 += __shfl_xor_sync(FULL, tw2, o);
       }
-      if ((tid & 31) == 0) {
+      if (lane == 0) {
         if (tw0) atomicAdd(&s.tw[0], tw0);
         if (tw1) atomicAdd(&s.tw[1], tw1);
-        if (tw2) atomicAdd(&s.tw[2], tw2);
       }
       if (tid == 0) {
         s.cnt[AUGSCHED_R_BUSY_STEPS] += 1;
@@ -412,88 +443,131 @@ __device__ void run_instance(const SimParams& p, SimShm& s, uint64_t* Ksm, uint3
       }
     }
     __syncthreads();
-    // ---- S6/S7 order + admission: find the last admitted entry k* --------------
-    // Tiers are ordered running < swapped < waiting, so the crossing tier follows
-    // from the per-tier totals; within it the crossing comes from a rank select
-    // over the (small) candidate list, or from argmin rounds over the waiting
-    // tier; the radix select over the whole queue is the fallback.
+    // ---- S6/S7 order + admission: the last admitted entry k* ------------------
+    // Tiers are ordered running < swapped < waiting, so the tier where the
+    // prefix ends follows from the per-tier totals.
     {
-      const unsigned long long w0 = s.tw[0], w1 = s.tw[1], w2 = s.tw[2];
-      const unsigned long long Bu = (unsigned long long)Bc;
-      bool done = false;
+      const unsigned long long w0 = s.tw[0], w1 = s.tw[1];
+      int wmode = WMODE_NONE;
       if (B <= 0) {
         if (tid == 0) { s.res.found = 1; s.res.k = 0; s.res.wbelow = 0; }  // nothing admitted
-        done = true;
-      } else if (w0 + w1 + w2 < Bu) {
-        if (tid == 0) { s.res.found = 0; s.res.total = w0 + w1 + w2; }    // everything admitted
-        done = true;
       } else if (w0 >= Bu) {
-        if (s.tc[0] <= SIM_CAND) { select_cand(s, 0, (int)s.tc[0], Bu, 0); done = true; }
+        if (s.tc[0] <= SIM_CAND) select_cand(s, 0, (int)s.tc[0], Bu, 0);
+        else select_arr(s, c.K, c.Ws, nR, Bu, KBITS, false);
       } else if (w0 + w1 >= Bu) {
-        if (s.tc[1] <= SIM_CAND) { select_cand(s, 1, (int)s.tc[1], Bu, w0); done = true; }
+        if (s.tc[1] <= SIM_CAND) select_cand(s, 1, (int)s.tc[1], Bu, w0);
+        else select_arr(s, c.K, c.Ws, nR, Bu, KBITS, false);
       } else {
-        // waiting tier: pop the smallest remaining waiting keys in order, one
-        // per round (one barrier each).  Every thread offers its smallest
-        // unconsumed waiting key (c1, then c2, then a rescan of its own
-        // entries); the block minimum is the next entry of the order.
-        const int lane = tid & 31, warp = tid >> 5;
-        unsigned long long wb = w0 + w1;
-        uint64_t myk = c1;
-        uint32_t myw = cw1;
-        int cons = 0;
-        for (int r = 0; r < 32; ++r) {
-          uint64_t mk = myk;
+        // the prefix reaches W: this lane's two smallest W keys and their
+        // demands / positions, and the W demand total
+        uint64_t c1 = ~0ull, c2 = ~0ull;
+        uint32_t cw1 = 0, cw2 = 0, cp1 = 0, cp2 = 0;
+        unsigned long long tw2 = 0;
+        constexpr int U = SIM_UNROLL;  // entries in flight per thread (independent L2 loads)
+        for (uint32_t b0 = 0; b0 < nW; b0 += SIM_NT * U) {
+          uint32_t e[U], l[U], d[U];
+          double V[U];
 #pragma unroll
-          for (int o = 16; o > 0; o >>= 1) {
-            const uint64_t y = __shfl_xor_sync(FULL, mk, o);
-            mk = y < mk ? y : mk;
+          for (int u = 0; u < U; ++u) {
+            const uint32_t i = b0 + u * SIM_NT + tid;
+            if (i < nW) { e[u] = c.W.id[i]; V[u] = c.W.V[i]; l[u] = c.W.last[i]; d[u] = c.W.dem[i]; }
           }
-          const unsigned own = __ballot_sync(FULL, myk == mk);
-          if (lane == __ffs(own) - 1) { s.rk[r & 1][warp] = mk; s.rw[r & 1][warp] = myw; }
-          __syncthreads();
-          uint64_t bk = s.rk[r & 1][0];
-          uint32_t bw = s.rw[r & 1][0];
 #pragma unroll
-          for (int w = 1; w < SIM_NW; ++w) {
-            const uint64_t x = s.rk[r & 1][w];
-            if (x < bk) { bk = x; bw = s.rw[r & 1][w]; }
-          }
-          if (bk == ~0ull) break;  // not reachable: w0 + w1 + w2 >= B
-          if (wb + bw >= Bu) {
-            if (tid == 0) { s.res.found = 1; s.res.k = bk; s.res.wbelow = wb; }
-            done = true;
-            break;
-          }
-          wb += bw;
-          if (myk == bk) {
-            if (++cons == 1) { myk = c2; myw = cw2; }
-            else {
-              uint64_t nk = ~0ull;
-              uint32_t nw = 0;
-              for (uint32_t i = tid; i < na; i += SIM_NT) {
-                const uint64_t Ki = K[i];
-                if ((Ki >> 48) == 2 && Ki > bk && Ki < nk) { nk = Ki; nw = W[i]; }
+          for (int u = 0; u < U; ++u) {
+            const uint32_t i = b0 + u * SIM_NT + tid;
+            if (i < nW) {
+              const uint64_t Ki = order_key(e[u], key_of(V[u], t, l[u]));
+              tw2 += d[u];
+              if (Ki < c2) {
+                if (Ki < c1) { c2 = c1; cw2 = cw1; cp2 = cp1; c1 = Ki; cw1 = d[u]; cp1 = i; }
+                else { c2 = Ki; cw2 = d[u]; cp2 = i; }
               }
-              myk = nk; myw = nw;
             }
           }
         }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) tw2 += __shfl_xor_sync(FULL, tw2, o);
+        if (lane == 0 && tw2) atomicAdd(&s.tw[2], tw2);
+        __syncthreads();
+        const unsigned long long wall = w0 + w1 + s.tw[2];
+        if (wall < Bu) {
+          if (tid == 0) { s.res.found = 0; s.res.total = wall; }   // everything admitted
+          wmode = WMODE_ALL;
+        } else {
+          // pop the smallest remaining W keys in order, one per round (one
+          // barrier each); a lane offers c1, then c2, then rescans its own
+          // positions for the next key above the last one popped
+          unsigned long long wb = w0 + w1;
+          uint64_t myk = c1;
+          uint32_t myw = cw1, myp = cp1;
+          int cons = 0;
+          for (int r = 0; r < MAXPOP; ++r) {
+            uint64_t mk = myk;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+              const uint64_t y = __shfl_xor_sync(FULL, mk, o);
+              mk = y < mk ? y : mk;
+            }
+            const unsigned own = __ballot_sync(FULL, myk == mk);
+            if (lane == __ffs(own) - 1) { s.rk[r & 1][warp] = mk; s.rw[r & 1][warp] = myw; s.rp[r & 1][warp] = myp; }
+            __syncthreads();
+            uint64_t bk = s.rk[r & 1][0];
+            uint32_t bw = s.rw[r & 1][0], bp = s.rp[r & 1][0];
+#pragma unroll
+            for (int w = 1; w < SIM_NW; ++w) {
+              const uint64_t x = s.rk[r & 1][w];
+              if (x < bk) { bk = x; bw = s.rw[r & 1][w]; bp = s.rp[r & 1][w]; }
+            }
+            if (bk == ~0ull) break;  // not reachable: the W total reaches B
+            if (tid == 0) { s.pk[r] = bk; s.pw[r] = bw; s.pp[r] = bp; }
+            if (wb + bw >= Bu) {
+              if (tid == 0) { s.res.found = 1; s.res.k = bk; s.res.wbelow = wb; s.npop = r + 1; }
+              wmode = WMODE_POP;
+              break;
+            }
+            wb += bw;
+            if (myk == bk) {
+              if (++cons == 1) { myk = c2; myw = cw2; myp = cp2; }
+              else {
+                uint64_t nk = ~0ull;
+                uint32_t nw = 0, np = 0;
+                for (uint32_t i = tid; i < nW; i += SIM_NT) {
+                  const uint64_t Ki = order_key(c.W.id[i], key_of(c.W.V[i], t, c.W.last[i]));
+                  if (Ki > bk && Ki < nk) { nk = Ki; nw = c.W.dem[i]; np = i; }
+                }
+                myk = nk; myw = nw; myp = np;
+              }
+            }
+          }
+          if (wmode != WMODE_POP) {
+            // many small W demands: materialise every key and radix-select
+            for (uint32_t i = tid; i < nW; i += SIM_NT) {
+              c.K[nR + i] = order_key(c.W.id[i], key_of(c.W.V[i], t, c.W.last[i]));
+              c.Ws[nR + i] = c.W.dem[i];
+            }
+            if (tid == 0) s.wkeys = 1;
+            select_arr(s, c.K, c.Ws, na, Bu, KBITS, false);
+            wmode = WMODE_KEY;
+          }
+        }
       }
-      if (!done) select_arr(s, K, W, na, Bu, KBITS, false);
+      if (tid == 0) s.wmode = wmode;
       __syncthreads();
     }
+    const int wmode = s.wmode;
     const bool found = s.res.found != 0;
-    const uint64_t kstar = B > 0 ? s.res.k : 0;
-    const uint64_t wb = s.res.wbelow;
-    auto grant = [&](uint64_t Ki, uint32_t dem) -> uint32_t {
-      if (Ki & KEVICT) return 0u;
-      if (B <= 0) return 0u;
-      if (!found || Ki < kstar) return dem;
-      if (Ki == kstar) return (uint32_t)((uint64_t)B - wb);
-      return 0u;
-    };
+    const GrantRule grant{B, B > 0 ? s.res.k : 0ull, s.res.wbelow, found};
     const long long need = B <= 0 ? 0 : (found ? B : (long long)s.res.total);
     long long freev = cap - s.A - s.P;
+    // Granted entries are addressed by a virtual index v: v < nR is R entry v,
+    // v >= nR is the (v - nR)-th W candidate: popped entry (WMODE_POP) or W
+    // position (WMODE_ALL / WMODE_KEY).
+    const uint32_t nGW = wmode == WMODE_POP ? s.npop : (wmode == WMODE_NONE ? 0u : nW);
+    auto w_pos = [&](uint32_t j) -> uint32_t { return wmode == WMODE_POP ? s.pp[j] : j; };
+    auto w_key = [&](uint32_t j) -> uint64_t {
+      if (wmode == WMODE_POP) return s.pk[j];
+      return s.wkeys ? c.K[nR + j] : 0ull;   // WMODE_ALL without resolution: every key passes
+    };
     // ---- S8 memory resolution (R20) -------------------------------------------
     if (need > freev) {
       // (1) demote Preserve-paused contexts, kv desc, id asc
@@ -520,15 +594,13 @@ __device__ void run_instance(const SimParams& p, SimShm& s, uint64_t* Ksm, uint3
       if (s.tc[0] <= SIM_CAND) select_cand(s, 0, (int)s.tc[0], D0, 0);
       else {
         // many Preserve-paused contexts: materialise (key, kv) and select over the arrays
-        uint64_t* K2 = a.kscr2 + off;
-        uint32_t* W2 = a.wscr2 + off;
         for (uint32_t i = tid; i < npz; i += SIM_NT) {
           uint64_t key = 0; uint32_t w = 0;
           if (!getp(i, key, w)) w = 0;
-          K2[i] = key; W2[i] = w;
+          c.K2[i] = key; c.W2[i] = w;
         }
         __syncthreads();
-        select_arr(s, K2, W2, npz, D0, 48, false);
+        select_arr(s, c.K2, c.W2, npz, D0, 48, false);
       }
       {
         const bool f0 = s.res.found != 0;
@@ -547,44 +619,65 @@ __device__ void run_instance(const SimParams& p, SimShm& s, uint64_t* Ksm, uint3
       __syncthreads();
       freev += (long long)s.freed;
       if (tid == 0) { s.P -= (long long)s.freed; s.tc[1] = 0; }
+      if (need > freev && (wmode == WMODE_ALL) && !s.wkeys) {
+        // the eviction order needs the W keys of this step
+        __syncthreads();
+        for (uint32_t i = tid; i < nW; i += SIM_NT)
+          c.K[nR + i] = order_key(c.W.id[i], key_of(c.W.V[i], t, c.W.last[i]));
+        if (tid == 0) s.wkeys = 1;
+      }
       __syncthreads();
       // (2) evict from the tail of the order over entries with kv + g > 0
       if (need > freev) {
         const uint64_t D1 = (uint64_t)(need - freev);
-        for (uint32_t i = tid; i < na; i += SIM_NT) {
-          const uint32_t id = c.ac_id[i] & 0xFFFF;
-          const uint32_t w = (uint32_t)c.rs[id].kv + grant(K[i], c.ac_dem[i]);
-          W[i] = w;
+        const uint32_t nv = nR + nGW;
+        for (uint32_t v = tid; v < nv; v += SIM_NT) {
+          uint64_t Ki;
+          uint32_t w;
+          if (v < nR) {
+            Ki = c.K[v];
+            w = (uint32_t)c.rs[c.R.id[v] & 0xFFFF].kv + grant(Ki, c.R.dem[v]);
+          } else {
+            const uint32_t j = v - nR;
+            Ki = w_key(j);
+            w = grant(Ki, wmode == WMODE_POP ? s.pw[j] : c.W.dem[j]);   // W entries hold no KV
+          }
+          c.K2[v] = Ki;
+          c.W2[v] = w;
           if (w > 0) {
             const uint32_t q = atomicAdd(&s.tc[1], 1u);
-            if (q < SIM_CAND) { s.u.c.ck[1][q] = KMASK - K[i]; s.u.c.cw[1][q] = w; }
+            if (q < SIM_CAND) { s.u.c.ck[1][q] = KMASK - Ki; s.u.c.cw[1][q] = w; }
           }
         }
         __syncthreads();
-        auto gete = [&](uint32_t i, uint64_t& key, uint32_t& w) {
-          w = W[i];
-          key = KMASK - K[i];
-          return w > 0;
-        };
         if (s.tc[1] <= SIM_CAND) select_cand(s, 1, (int)s.tc[1], D1, 0);
-        else select_arr(s, K, W, na, D1, KBITS, true);
+        else select_arr(s, c.K2, c.W2, nv, D1, KBITS, true);
         const bool f1 = s.res.found != 0;
         const uint64_t k1 = s.res.k;
-        for (uint32_t i = tid; i < na; i += SIM_NT) {
-          uint64_t key; uint32_t w;
-          if (gete(i, key, w) && (!f1 || key <= k1)) {
-            const uint32_t e = c.ac_id[i];
-            const uint32_t id = e & 0xFFFF;
+        for (uint32_t v = tid; v < nv; v += SIM_NT) {
+          const uint32_t w = c.W2[v];
+          const uint64_t Ki = c.K2[v];
+          if (w == 0 || (f1 && KMASK - Ki > k1)) continue;
+          atomicAdd(&s.cnt[AUGSCHED_R_EVICTIONS], 1ull);
+          if (v < nR) {
+            // running / swapped entry: drop its KV and requeue it in W
+            const uint32_t id = c.R.id[v] & 0xFFFF;
             ReqState r = c.rs[id];
             atomicAdd((unsigned long long*)&s.A, (unsigned long long)(-(long long)r.kv));
             r.kv = 0;
             r.cpu = 0;
             r.meta = meta_with(r.meta, ST_WAIT, meta_pol(r.meta));
             c.rs[id] = r;
-            c.ac_id[i] = id | (2u << 30);
-            c.ac_dem[i] = demand_of(r.ctx, 0, 0, r.pend, p.cfg.s_in);
-            K[i] |= KEVICT;
-            atomicAdd(&s.cnt[AUGSCHED_R_EVICTIONS], 1ull);
+            c.W.put(atomicAdd(&s.n_w, 1u), id | (2u << 30), c.R.V[v], c.R.last[v],
+                    demand_of(r.ctx, 0, 0, r.pend, p.cfg.s_in));
+            c.R.id[v] = INVALID;
+            c.K[v] |= KEVICT;
+            mark_hole(s, 0, v);
+          } else {
+            // granted W entry: its grant is cancelled (it holds no KV)
+            const uint32_t j = v - nR;
+            if (wmode == WMODE_POP) s.pk[j] |= KEVICT;
+            else c.K[nR + j] |= KEVICT;
           }
         }
         __syncthreads();
@@ -594,9 +687,24 @@ __device__ void run_instance(const SimParams& p, SimShm& s, uint64_t* Ksm, uint3
     {
       uint32_t my_tok = 0, my_adm = 0;
       long long accA = 0, accP = 0;
-      for (uint32_t i = tid; i < na; i += SIM_NT) {
-        const uint64_t Ki = K[i];
-        const uint32_t dem = c.ac_dem[i], e = c.ac_id[i];  // independent loads, issued together
+      const uint32_t nv = nR + nGW;
+      for (uint32_t v = tid; v < nv; v += SIM_NT) {
+        const bool inR = v < nR;
+        uint32_t pos, e, dem;
+        uint64_t Ki;
+        if (inR) {
+          pos = v;
+          e = c.R.id[v];
+          if (e == INVALID) continue;        // evicted to W this step
+          Ki = c.K[v];
+          dem = c.R.dem[v];
+        } else {
+          const uint32_t j = v - nR;
+          pos = w_pos(j);
+          e = c.W.id[pos];
+          Ki = w_key(j);
+          dem = wmode == WMODE_POP ? s.pw[j] : c.W.dem[pos];
+        }
         const uint32_t g = grant(Ki, dem);
         if (g == 0) continue;
         my_tok += g; my_adm += 1;
@@ -669,14 +777,19 @@ __device__ void run_instance(const SimParams& p, SimShm& s, uint64_t* Ksm, uint3
         c.rs[id] = r;
         accA += dA;
         accP += dP;
-        if (leave) {
-          c.ac_id[i] = INVALID;
-          const uint32_t hslot = atomicAdd(&s.n_holes, 1u);
-          if (hslot < HOLE_CAP) s.holes[hslot] = i;
+        const uint32_t nd = demand_of(ctx, kv, cpu, pend, p.cfg.s_in);
+        if (inR) {
+          if (leave) { c.R.id[pos] = INVALID; mark_hole(s, 0, pos); }
+          else {                                         // tier 0: running (R16, R14)
+            c.R.id[pos] = id;
+            c.R.last[pos] = (uint32_t)t;
+            c.R.dem[pos] = nd;
+          }
         } else {
-          c.ac_id[i] = id;                               // tier 0: running (R16)
-          c.ac_last[i] = (uint32_t)t;                    // R14
-          c.ac_dem[i] = demand_of(ctx, kv, cpu, pend, p.cfg.s_in);
+          // a granted waiting entry ends the step running: move it to R
+          if (!leave) c.R.put(atomicAdd(&s.n_r, 1u), id, c.W.V[pos], (uint32_t)t, nd);
+          c.W.id[pos] = INVALID;
+          mark_hole(s, 1, pos);
         }
       }
       // one shared atomic per warp (64-bit shared atomicAdd is a CAS loop)
@@ -687,14 +800,15 @@ __device__ void run_instance(const SimParams& p, SimShm& s, uint64_t* Ksm, uint3
         accA += __shfl_xor_sync(FULL, accA, o);
         accP += __shfl_xor_sync(FULL, accP, o);
       }
-      if ((tid & 31) == 0) {
+      if (lane == 0) {
         if (my_tok) atomicAdd(&s.cnt[AUGSCHED_R_TOKENS], (unsigned long long)my_tok);
         if (my_adm) atomicAdd(&s.cnt[AUGSCHED_R_ADMITTED], (unsigned long long)my_adm);
         if (accA) atomicAdd((unsigned long long*)&s.A, (unsigned long long)accA);
         if (accP) atomicAdd((unsigned long long*)&s.P, (unsigned long long)accP);
       }
     }
-    compact_active(c);  // syncs
+    compact_list(s, c.R, 0, s.n_r);  // syncs
+    compact_list(s, c.W, 1, s.n_w);
     if (tid == 0) {
       if (s.A < 0 || s.P < 0 || s.A + s.P > cap) s.cnt[AUGSCHED_R_ERR] |= 1;
       s.t = t + 1;                                       // S12
@@ -706,7 +820,7 @@ __device__ void run_instance(const SimParams& p, SimShm& s, uint64_t* Ksm, uint3
   __syncthreads();
   if (tid == 0) {
     H.t = s.t; H.A = s.A; H.P = s.P; H.min_ret = s.min_ret; H.next_arr = s.next_arr;
-    H.n_act = s.n_act; H.n_pz = s.n_pz; H.n_fin = s.n_fin;
+    H.n_r = s.n_r; H.n_w = s.n_w; H.n_pz = s.n_pz; H.n_fin = s.n_fin;
     s.cnt[AUGSCHED_R_FINAL_T] = s.t;
   }
   __syncthreads();
@@ -721,23 +835,19 @@ __device__ void run_instance(const SimParams& p, SimShm& s, uint64_t* Ksm, uint3
 __global__ void __launch_bounds__(SIM_NT, SIM_MINB) sim_kernel(const __grid_constant__ SimParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   SimShm& s = *reinterpret_cast<SimShm*>(smem_raw);
-  uint64_t* Ksm = reinterpret_cast<uint64_t*>(smem_raw + ((sizeof(SimShm) + 15) & ~size_t(15)));
-  uint32_t* Wsm = reinterpret_cast<uint32_t*>(Ksm + p.scap);
   for (;;) {
     if (threadIdx.x == 0) s.inst = atomicAdd(p.work, 1u);
     __syncthreads();
     const uint32_t inst = s.inst;
     if (inst >= p.n_inst) return;
-    run_instance(p, s, Ksm, Wsm, inst);
+    run_instance(p, s, inst);
     __syncthreads();
   }
 }
 
 }  // namespace
 
-size_t sim_smem_bytes(uint32_t scap) {
-  return ((sizeof(SimShm) + 15) & ~size_t(15)) + (size_t)scap * (sizeof(uint64_t) + sizeof(uint32_t));
-}
+size_t sim_smem_bytes() { return (sizeof(SimShm) + 15) & ~size_t(15); }
 
 const void* sim_kernel_ptr() { return reinterpret_cast<const void*>(&sim_kernel); }
 

@@ -31,10 +31,6 @@ constexpr int SIM_RB = SIM_NT >= 256 ? 8 : 5;   // radix bits of the fallback se
 #define AUGSCHED_SIM_CAND 64
 #endif
 constexpr int SIM_CAND = AUGSCHED_SIM_CAND;      // small-candidate list capacity
-#ifndef AUGSCHED_SIM_SCAP
-#define AUGSCHED_SIM_SCAP 0
-#endif
-constexpr uint32_t SIM_SCAP = AUGSCHED_SIM_SCAP;  // queue entries whose step keys stay in shared memory
 #ifndef AUGSCHED_SIM_MINB
 #define AUGSCHED_SIM_MINB 24
 #endif
@@ -68,8 +64,8 @@ struct InstHdr {
   uint64_t t;
   int64_t A, P;           // KV ledger in tokens: active, Preserve-paused
   uint64_t min_ret;       // min return tick over the paused list
-  uint32_t next_arr, n_act, n_pz, n_fin;
-  uint32_t started, pad;
+  uint32_t next_arr, n_r, n_w, n_pz, n_fin;
+  uint32_t started;
 };
 
 // Mutable state of one request, packed in one 32-byte sector so the engine
@@ -90,17 +86,23 @@ struct Arena {
   // cold state by request id
   ReqState* rs;
   uint64_t* ret;       // return tick of the outstanding call
-  // active list by position
-  uint32_t* ac_id;     // id | tier << 30  (tier 0 running, 1 swapped, 2 waiting)
-  double* ac_V;
-  uint32_t* ac_last;
-  uint32_t* ac_dem;
+  // queue lists by position (tier-split): R = running u swapped (tier 0/1),
+  // W = waiting (tier 2); entry = id | tier << 30, V, last, demand
+  uint32_t* r_id;
+  double* r_V;
+  uint32_t* r_last;
+  uint32_t* r_dem;
+  uint32_t* w_id;
+  double* w_V;
+  uint32_t* w_last;
+  uint32_t* w_dem;
   // paused list by position
   uint32_t* pz_id;
-  // scratch for steps whose queue exceeds the shared-memory capacity
+  // per-step scratch: keys / weights of the R list (and of W when a step
+  // needs them materialised); secondary selections (demotion, eviction)
   uint64_t* kscr;
   uint32_t* wscr;
-  uint64_t* kscr2;     // secondary selections (demotion)
+  uint64_t* kscr2;
   uint32_t* wscr2;
 };
 
@@ -115,7 +117,7 @@ struct SimParams {
   augsched_result* acc;                      // [n_inst] handle-owned accumulators
   augsched_result* out;                      // [n_inst] caller's results (device)
   uint64_t max_iters;
-  uint32_t n_inst, max_active, scap;
+  uint32_t n_inst, max_active;
   uint32_t* work;                            // work-stealing counter
   uint32_t* err;                             // device error word
 };

@@ -447,7 +447,6 @@ __global__ void __launch_bounds__(ANT) admit_kernel(Slots S, augsched_config cfg
   __shared__ unsigned long long wsum[ANW];
   __shared__ SelShm sel;
   __shared__ unsigned long long freed;
-  __shared__ uint32_t adm_s;
   const uint32_t i = blockIdx.x;
   const int tid = threadIdx.x;
   const uint32_t MA = S.MA;
