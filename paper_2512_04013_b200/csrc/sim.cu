@@ -39,6 +39,8 @@ struct __align__(16) SimShm {
   int wkeys;                         // W keys materialised in kscr[nR ..]
   int due;                           // intake or idle handling needed this iteration
   unsigned long long cnt[AUGSCHED_R_NFIELD];
+  unsigned int c32[AUGSCHED_R_NFIELD];  // this call's counts (native 32-bit shared atomics),
+                                        // folded into cnt when the instance's window ends
   unsigned int holes[2][HOLE_CAP];   // hole positions of R (0) and W (1)
   unsigned int nholes[2];
   unsigned int wtot[SIM_NW + 1];
@@ -81,6 +83,16 @@ __device__ __forceinline__ uint32_t block_flag_scan(SimShm& s, bool f) {
   }
   __syncthreads();
   return s.wtot[warp] + __popc(b & ((1u << lane) - 1));
+}
+
+// Count into this call's 32-bit counters.
+__device__ __forceinline__ void cinc(SimShm& s, int f, uint32_t v = 1u) { atomicAdd(&s.c32[f], v); }
+
+// Shared 64-bit accumulation by one warp: a plain update when the CTA is a
+// single warp (no other writer), else an atomic.
+__device__ __forceinline__ void warp_add64(unsigned long long* x, unsigned long long v) {
+  if (SIM_NW == 1) *x += v;
+  else atomicAdd(x, v);
 }
 
 // One queue list (SoA by position).
@@ -152,7 +164,7 @@ __device__ void do_return(Ctx& c, uint32_t id) {
   r.meta = make_meta(kk + 1, st, (uint32_t)pol, ns);
   r.left = tr.gen_true[s0 + kk + 1];
   c.rs[id] = r;
-  atomicAdd(&s.cnt[AUGSCHED_R_RETURNS], 1ull);
+  cinc(s, AUGSCHED_R_RETURNS);
   const uint32_t dem = demand_of(ctx, kv, cpu, (int32_t)R, c.p.cfg.s_in);
   // last is not reset on return (R14)
   if (tier < 2) c.R.put(atomicAdd(&s.n_r, 1u), id | (tier << 30), V, r.lastc, dem);
@@ -273,6 +285,27 @@ __device__ __noinline__ void select_cand(SimShm& s, int list, int m, uint64_t D,
   rank_select<SIM_NT, SIM_CAND>(s.u.c, list, s.res, m, D, w0);
 }
 
+// Thread 0 prepares iteration s.t: stop rule, S1 snapshot, whether intake
+// or the idle jump must run, and (when no intake is due) the token limit.
+__device__ __noinline__ void prep_step(const SimParams& p, SimShm& s, uint32_t n) {
+  s.run = (s.n_fin < n) && (s.t < p.max_iters);
+  s.tT = s.t * p.cfg.t_fwd_ticks;
+  s.A_snap = s.A;
+  s.due = s.n_r + s.n_w == 0 || s.tT >= s.min_ret || s.tT >= s.next_tick;
+  if (!s.due) s.B = token_limit(p.cfg, s.coef, s.ip, p.cap, s.A, s.P);
+  s.tw[0] = s.tw[1] = s.tw[2] = 0;
+  s.tc[0] = s.tc[1] = s.tc[2] = 0;
+  s.wkeys = 0;
+}
+
+// Order key of W entry i at iteration t (out of line: the rare rescans and
+// materialisations share one copy).
+__device__ __noinline__ uint64_t w_order_key(const SimShm& s, const uint32_t* id, const double* V,
+                                             const uint32_t* last, uint32_t i, uint64_t t) {
+  const uint32_t key = s.ip.ranking == AUGSCHED_RANK_FCFS ? 0u : sched_key(s.coef, V[i], t, last[i]);
+  return order_key(id[i], key);
+}
+
 // Grant rule of the step (R17): full demand before k*, the remainder at k*,
 // nothing after it or for an entry whose grant was cancelled (KEVICT).
 struct GrantRule {
@@ -323,7 +356,7 @@ __device__ void run_instance(const SimParams& p, SimShm& s, uint32_t inst) {
     s.nholes[0] = s.nholes[1] = 0;
     s.next_tick = s.next_arr < n ? p.tr.arr_tick[c.r0 + s.next_arr] : ~0ull;
   }
-  for (int f = tid; f < AUGSCHED_R_NFIELD; f += SIM_NT) s.cnt[f] = acc.f[f];
+  for (int f = tid; f < AUGSCHED_R_NFIELD; f += SIM_NT) { s.cnt[f] = acc.f[f]; s.c32[f] = 0; }
   __syncthreads();
   if (tid == 0) s.cnt[AUGSCHED_R_NREQ] = n;
   const int64_t cap = p.cap;
@@ -332,19 +365,7 @@ __device__ void run_instance(const SimParams& p, SimShm& s, uint32_t inst) {
     return fcfs ? 0u : sched_key(c.k, V, t, last);
   };
 
-  // thread 0 prepares iteration s.t: stop rule, S1 snapshot, whether intake
-  // or the idle jump must run, and (when no intake is due) the token limit.
-  auto prep = [&]() {
-    s.run = (s.n_fin < n) && (s.t < p.max_iters);
-    s.tT = s.t * T;
-    s.A_snap = s.A;
-    s.due = s.n_r + s.n_w == 0 || s.tT >= s.min_ret || s.tT >= s.next_tick;
-    if (!s.due) s.B = token_limit(p.cfg, c.k, c.ip, cap, s.A, s.P);
-    s.tw[0] = s.tw[1] = s.tw[2] = 0;
-    s.tc[0] = s.tc[1] = s.tc[2] = 0;
-    s.wkeys = 0;
-  };
-  if (tid == 0) prep();
+  if (tid == 0) prep_step(p, s, n);
   __syncthreads();
 
   for (;;) {
@@ -386,7 +407,7 @@ __device__ void run_instance(const SimParams& p, SimShm& s, uint32_t inst) {
           if (s.next_arr < n) te = (p.tr.arr_tick[c.r0 + s.next_arr] + T - 1) / T;
           if (s.n_pz > 0) { const uint64_t tr_ = (s.min_ret + T - 1) / T; te = tr_ < te ? tr_ : te; }
           if (te == ~0ull) { s.idle = 2; s.run = 0; }
-          else { s.t = te; s.idle = 1; prep(); }
+          else { s.t = te; s.idle = 1; prep_step(p, s, n); }
         } else {
           s.B = token_limit(p.cfg, c.k, c.ip, cap, s.A, s.P);
         }
@@ -433,8 +454,8 @@ __device__ void run_instance(const SimParams& p, SimShm& s, uint32_t inst) {
         tw1 += __shfl_xor_sync(FULL, tw1, o);
       }
       if (lane == 0) {
-        if (tw0) atomicAdd(&s.tw[0], tw0);
-        if (tw1) atomicAdd(&s.tw[1], tw1);
+        if (tw0) warp_add64(&s.tw[0], tw0);
+        if (tw1) warp_add64(&s.tw[1], tw1);
       }
       if (tid == 0) {
         s.cnt[AUGSCHED_R_BUSY_STEPS] += 1;
@@ -487,7 +508,7 @@ __device__ void run_instance(const SimParams& p, SimShm& s, uint32_t inst) {
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) tw2 += __shfl_xor_sync(FULL, tw2, o);
-        if (lane == 0 && tw2) atomicAdd(&s.tw[2], tw2);
+        if (lane == 0 && tw2) warp_add64(&s.tw[2], tw2);
         __syncthreads();
         const unsigned long long wall = w0 + w1 + s.tw[2];
         if (wall < Bu) {
@@ -532,7 +553,7 @@ __device__ void run_instance(const SimParams& p, SimShm& s, uint32_t inst) {
                 uint64_t nk = ~0ull;
                 uint32_t nw = 0, np = 0;
                 for (uint32_t i = tid; i < nW; i += SIM_NT) {
-                  const uint64_t Ki = order_key(c.W.id[i], key_of(c.W.V[i], t, c.W.last[i]));
+                  const uint64_t Ki = w_order_key(s, c.W.id, c.W.V, c.W.last, i, t);
                   if (Ki > bk && Ki < nk) { nk = Ki; nw = c.W.dem[i]; np = i; }
                 }
                 myk = nk; myw = nw; myp = np;
@@ -542,7 +563,7 @@ __device__ void run_instance(const SimParams& p, SimShm& s, uint32_t inst) {
           if (wmode != WMODE_POP) {
             // many small W demands: materialise every key and radix-select
             for (uint32_t i = tid; i < nW; i += SIM_NT) {
-              c.K[nR + i] = order_key(c.W.id[i], key_of(c.W.V[i], t, c.W.last[i]));
+              c.K[nR + i] = w_order_key(s, c.W.id, c.W.V, c.W.last, i, t);
               c.Ws[nR + i] = c.W.dem[i];
             }
             if (tid == 0) s.wkeys = 1;
@@ -612,7 +633,7 @@ __device__ void run_instance(const SimParams& p, SimShm& s, uint32_t inst) {
             atomicAdd(&s.freed, (unsigned long long)w);
             c.rs[id].kv = 0;
             c.rs[id].meta = meta_with(c.rs[id].meta, meta_st(c.rs[id].meta), POL_D);
-            atomicAdd(&s.cnt[AUGSCHED_R_DEMOTIONS], 1ull);
+            cinc(s, AUGSCHED_R_DEMOTIONS);
           }
         }
       }
@@ -622,8 +643,7 @@ __device__ void run_instance(const SimParams& p, SimShm& s, uint32_t inst) {
       if (need > freev && (wmode == WMODE_ALL) && !s.wkeys) {
         // the eviction order needs the W keys of this step
         __syncthreads();
-        for (uint32_t i = tid; i < nW; i += SIM_NT)
-          c.K[nR + i] = order_key(c.W.id[i], key_of(c.W.V[i], t, c.W.last[i]));
+        for (uint32_t i = tid; i < nW; i += SIM_NT) c.K[nR + i] = w_order_key(s, c.W.id, c.W.V, c.W.last, i, t);
         if (tid == 0) s.wkeys = 1;
       }
       __syncthreads();
@@ -658,7 +678,7 @@ __device__ void run_instance(const SimParams& p, SimShm& s, uint32_t inst) {
           const uint32_t w = c.W2[v];
           const uint64_t Ki = c.K2[v];
           if (w == 0 || (f1 && KMASK - Ki > k1)) continue;
-          atomicAdd(&s.cnt[AUGSCHED_R_EVICTIONS], 1ull);
+          cinc(s, AUGSCHED_R_EVICTIONS);
           if (v < nR) {
             // running / swapped entry: drop its KV and requeue it in W
             const uint32_t id = c.R.id[v] & 0xFFFF;
@@ -743,10 +763,10 @@ __device__ void run_instance(const SimParams& p, SimShm& s, uint32_t inst) {
               const bool ok5 = ttft < 5 * c.ip.slo_ttft_ticks &&
                                e2e * c.ip.slo_norm_den < 5 * (uint64_t)c.ip.slo_norm_num * T * gt;
               atomicAdd(&s.n_fin, 1u);
-              atomicAdd(&s.cnt[AUGSCHED_R_COMPLETED], 1ull);
-              if (ok) atomicAdd(&s.cnt[AUGSCHED_R_SLO_OK], 1ull);
-              if (ok5) atomicAdd(&s.cnt[AUGSCHED_R_SLO_OK_5X], 1ull);
-              atomicMax(&s.cnt[AUGSCHED_R_MAKESPAN], (unsigned long long)fin);
+              cinc(s, AUGSCHED_R_COMPLETED);
+              if (ok) cinc(s, AUGSCHED_R_SLO_OK);
+              if (ok5) cinc(s, AUGSCHED_R_SLO_OK_5X);
+              atomicMax(&s.c32[AUGSCHED_R_MAKESPAN], (uint32_t)fin);
               atomicAdd(&s.cnt[AUGSCHED_R_SUM_TTFT], (unsigned long long)ttft);
               atomicAdd(&s.cnt[AUGSCHED_R_SUM_E2E], (unsigned long long)e2e);
               atomicAdd(&s.cnt[AUGSCHED_R_SUM_GEN], (unsigned long long)gt);
@@ -762,9 +782,9 @@ __device__ void run_instance(const SimParams& p, SimShm& s, uint32_t inst) {
               c.ret[id] = rt;
               r.lastc = (uint32_t)t;
               dA -= kv;
-              if (np == POL_P) { dP += kv; atomicAdd(&s.cnt[AUGSCHED_R_CALLS_PRESERVE], 1ull); }
-              else if (np == POL_S) { cpu = ctx; kv = 0; atomicAdd(&s.cnt[AUGSCHED_R_CALLS_SWAP], 1ull); }
-              else { kv = 0; atomicAdd(&s.cnt[AUGSCHED_R_CALLS_DISCARD], 1ull); }
+              if (np == POL_P) { dP += kv; cinc(s, AUGSCHED_R_CALLS_PRESERVE); }
+              else if (np == POL_S) { cpu = ctx; kv = 0; cinc(s, AUGSCHED_R_CALLS_SWAP); }
+              else { kv = 0; cinc(s, AUGSCHED_R_CALLS_DISCARD); }
               m = meta_with(m, ST_PAUSED, (uint32_t)np);
               const uint32_t q = atomicAdd(&s.n_pz, 1u);
               c.pz_id[q] = id;
@@ -801,10 +821,10 @@ __device__ void run_instance(const SimParams& p, SimShm& s, uint32_t inst) {
         accP += __shfl_xor_sync(FULL, accP, o);
       }
       if (lane == 0) {
-        if (my_tok) atomicAdd(&s.cnt[AUGSCHED_R_TOKENS], (unsigned long long)my_tok);
-        if (my_adm) atomicAdd(&s.cnt[AUGSCHED_R_ADMITTED], (unsigned long long)my_adm);
-        if (accA) atomicAdd((unsigned long long*)&s.A, (unsigned long long)accA);
-        if (accP) atomicAdd((unsigned long long*)&s.P, (unsigned long long)accP);
+        if (my_tok) cinc(s, AUGSCHED_R_TOKENS, my_tok);
+        if (my_adm) cinc(s, AUGSCHED_R_ADMITTED, my_adm);
+        if (accA) warp_add64((unsigned long long*)&s.A, (unsigned long long)accA);
+        if (accP) warp_add64((unsigned long long*)&s.P, (unsigned long long)accP);
       }
     }
     compact_list(s, c.R, 0, s.n_r);  // syncs
@@ -812,11 +832,16 @@ __device__ void run_instance(const SimParams& p, SimShm& s, uint32_t inst) {
     if (tid == 0) {
       if (s.A < 0 || s.P < 0 || s.A + s.P > cap) s.cnt[AUGSCHED_R_ERR] |= 1;
       s.t = t + 1;                                       // S12
-      prep();
+      prep_step(p, s, n);
     }
     __syncthreads();
   }
   // ---- save state and results ------------------------------------------------
+  __syncthreads();
+  for (int f = tid; f < AUGSCHED_R_NFIELD; f += SIM_NT) {
+    if (f == AUGSCHED_R_MAKESPAN) { if (s.c32[f] > s.cnt[f]) s.cnt[f] = s.c32[f]; }
+    else s.cnt[f] += s.c32[f];
+  }
   __syncthreads();
   if (tid == 0) {
     H.t = s.t; H.A = s.A; H.P = s.P; H.min_ret = s.min_ret; H.next_arr = s.next_arr;

@@ -32,10 +32,10 @@ constexpr int SIM_RB = SIM_NT >= 256 ? 8 : 5;   // radix bits of the fallback se
 #endif
 constexpr int SIM_CAND = AUGSCHED_SIM_CAND;      // small-candidate list capacity
 #ifndef AUGSCHED_SIM_MINB
-#define AUGSCHED_SIM_MINB 24
+#define AUGSCHED_SIM_MINB 32
 #endif
 #ifndef AUGSCHED_SIM_UNROLL
-#define AUGSCHED_SIM_UNROLL 2
+#define AUGSCHED_SIM_UNROLL 1
 #endif
 constexpr int SIM_MINB = AUGSCHED_SIM_MINB;   // CTAs per SM the kernel is register-bounded for
 constexpr int SIM_UNROLL = AUGSCHED_SIM_UNROLL;  // queue entries in flight per thread in the key pass
