@@ -56,6 +56,14 @@ def parse():
 
 
 # ----------------------------------------------------------------------------- workload
+def workload_name(args):
+    if args.workload == "cfg5":
+        n_inst = args.instances
+        return (f"cfg5: {n_inst} instances/GPU = {max(1, n_inst // 16)} W2 traces x 5000 requests (2-5 req/s, "
+                f"math/QA/web/chatbot tool mix) x 16 params (target_max 250-1000 x alpha 0-1000M), 7B preset")
+    return "cfg3: 4096 instances (64 target_max x 64 TTFT SLO) x 2000 requests @4 req/s, 7B preset"
+
+
 def workload(args, rank):
     """Synthetic traces + per-instance parameters of this rank's shard."""
     if args.workload == "cfg5":
@@ -69,13 +77,11 @@ def workload(args, rank):
         tr = tracegen._finish(req_off, *cat)
         ip = tracegen.cfg5_params(n_inst)
         tid = (np.arange(n_inst) // 16).astype(np.uint32)
-        name = (f"cfg5: {n_inst} instances/GPU = {n_tr} W2 traces x 5000 requests (2-5 req/s, "
-                f"math/QA/web/chatbot tool mix) x 16 params (target_max 250-1000 x alpha 0-1000M), 7B preset")
-        return tr, ip, tid, 5000, name
+        return tr, ip, tid, 5000, workload_name(args)
     tr = tracegen.gen_traces(1, 2000, [4.0], seed=3)
     ip = tracegen.cfg3_params()
     tid = np.zeros(4096, np.uint32)
-    return tr, ip, tid, 2000, "cfg3: 4096 instances (64 target_max x 64 TTFT SLO) x 2000 requests @4 req/s, 7B preset"
+    return tr, ip, tid, 2000, workload_name(args)
 
 
 # ----------------------------------------------------------------------------- clocks
@@ -298,11 +304,15 @@ def run_gpu(args):
             "frac": round(achieved / peak, 4), "traffic": None,
             "kernel": "sim_kernel (persistent, one CTA per instance)", "peak_source": peak_src,
             "algorithmic_bytes_per_decision": 32}
+    # DRAM bytes per launch of the same kernel on the same workload, from one
+    # ncu capture of bench.py's timed launches (tools/traffic.py)
     prof = os.path.join(ROOT, "profiles", "sim_kernel_traffic.json")
     if os.path.exists(prof):
         try:
             pj = _j.load(open(prof))
-            roof["traffic"] = pj.get("dram_bytes_per_decision", None) and pj["dram_bytes_per_decision"] * dec / args.steps
+            if pj.get("workload") == name and pj.get("window_iters", W) == W:
+                roof["traffic"] = pj["dram_bytes_per_launch_mean"]
+                roof["traffic_source"] = "profiles/sim_kernel_traffic.json (ncu, same workload)"
         except Exception:
             pass
 
@@ -311,7 +321,7 @@ def run_gpu(args):
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": name, "window_iters": W, "instances_per_gpu": n_inst,
                        "l2": "inputs larger than L2 (per-GPU state %.1f GB)" % (
-                           n_inst * ma * 60 / 1e9)},
+                           n_inst * ma * 100 / 1e9)},
             "instance_steps_per_s": isteps_all / (total_ms / 1e3),
             "gpu_launches": launches, "roofline": roof, "allgather_ms": gather_ms}
     line["clocks"] = clk.summary()

@@ -15,6 +15,9 @@ constexpr unsigned FULL = 0xffffffffu;
 #ifndef AUGSCHED_SORT_ITEMS
 #define AUGSCHED_SORT_ITEMS 16
 #endif
+#ifndef AUGSCHED_SORT_BALLOT
+#define AUGSCHED_SORT_BALLOT 1
+#endif
 #ifndef AUGSCHED_KEYS_MATCH
 #define AUGSCHED_KEYS_MATCH 0
 #endif
@@ -261,6 +264,25 @@ struct SortArgs {
   uint32_t* keyout;
 };
 
+// Lanes of the warp holding the same RB-bit digit as this lane (d < 0: the
+// lane holds no item and is in no other lane's set).  RB + 1 ballots; the
+// __match_any_sync variant is kept for comparison (AUGSCHED_SORT_BALLOT=0).
+template <int RB>
+__device__ __forceinline__ unsigned digit_peers(int d) {
+#if AUGSCHED_SORT_BALLOT
+  unsigned m = __ballot_sync(FULL, d >= 0);
+#pragma unroll
+  for (int b = 0; b < RB; ++b) {
+    const bool bit = (d >> b) & 1;
+    const unsigned v = __ballot_sync(FULL, bit);
+    m &= bit ? v : ~v;
+  }
+  return m;
+#else
+  return __match_any_sync(FULL, d);
+#endif
+}
+
 constexpr int LB_BATCH = 8;     // aggregate words loaded together by one thread
 
 // Spin until every word of a strided run carries this pass's epoch; return
@@ -354,7 +376,7 @@ __global__ void __launch_bounds__(SNT) sort_pass_kernel(SortArgs a) {
   const unsigned lt = (1u << lane) - 1;
 #pragma unroll
   for (int r = 0; r < SITEMS; ++r) {
-    const unsigned peers = __match_any_sync(FULL, dg[r]);
+    const unsigned peers = digit_peers<RB>(dg[r]);
     if (dg[r] >= 0) rk[r] = wcnt[warp][dg[r]] + __popc(peers & lt);
     __syncwarp();
     if (dg[r] >= 0 && lane == __ffs(peers) - 1) wcnt[warp][dg[r]] += __popc(peers);
