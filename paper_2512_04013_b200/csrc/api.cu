@@ -123,10 +123,9 @@ int ensure_sim(augsched_t* h) {
   const size_t N = (size_t)h->n_inst * h->max_active;
   Arena& a = h->ar;
   int rc;
-  if ((rc = h->alloc(&a.rs, N)) || (rc = h->alloc(&a.ret, N)) || (rc = h->alloc(&a.r_id, N)) ||
-      (rc = h->alloc(&a.r_V, N)) || (rc = h->alloc(&a.r_last, N)) || (rc = h->alloc(&a.r_dem, N)) ||
-      (rc = h->alloc(&a.w_id, N)) || (rc = h->alloc(&a.w_V, N)) || (rc = h->alloc(&a.w_last, N)) ||
-      (rc = h->alloc(&a.w_dem, N)) || (rc = h->alloc(&a.pz_id, N)) ||
+  if ((rc = h->alloc(&a.rs, N)) || (rc = h->alloc(&a.ret, N)) || (rc = h->alloc(&a.r_q, N)) ||
+      (rc = h->alloc(&a.r_dem, N)) || (rc = h->alloc(&a.w_q, N)) || (rc = h->alloc(&a.w_dem, N)) ||
+      (rc = h->alloc(&a.pz_id, N)) ||
       (rc = h->alloc(&a.kscr, N)) || (rc = h->alloc(&a.wscr, N)) ||
       (rc = h->alloc(&a.kscr2, N)) || (rc = h->alloc(&a.wscr2, N)) ||
       (rc = h->alloc(&h->d_hdr, h->n_inst)) || (rc = h->alloc(&h->d_acc, h->n_inst)))

@@ -27,6 +27,7 @@ struct __align__(16) SimShm {
   } u;
   SelRes res;
   unsigned long long tw[3];          // per-tier demand of the step (unclamped)
+  unsigned long long w2;             // demand total of the W list (maintained incrementally)
   unsigned int tc[3];                // per-tier candidate counts of the step
   unsigned long long rk[2][SIM_NW];  // pop rounds: per-warp smallest key, its demand and
   unsigned int rw[2][SIM_NW];        //   W position (double-buffered by round parity)
@@ -95,14 +96,17 @@ __device__ __forceinline__ void warp_add64(unsigned long long* x, unsigned long 
   else atomicAdd(x, v);
 }
 
-// One queue list (SoA by position).
+// One queue list by position: the scoring record (V, last, id | tier << 30)
+// as one 16-byte entry (a single vector load per entry and step) and the
+// demand beside it (read only for the entries a step grants or offers).
 struct List {
-  uint32_t* id;     // request id | tier << 30; INVALID marks a hole
-  double* V;        // value (Stage I / II / final), fixed between events
-  uint32_t* last;   // last-scheduled iteration (R14)
+  QEnt* q;          // e == INVALID marks a hole
   uint32_t* dem;    // demand of the next grant (R17, R18)
   __device__ __forceinline__ void put(uint32_t pos, uint32_t e, double v, uint32_t l, uint32_t d) const {
-    id[pos] = e; V[pos] = v; last[pos] = l; dem[pos] = d;
+    QEnt x;
+    x.V = v; x.last = l; x.e = e;
+    q[pos] = x;
+    dem[pos] = d;
   }
 };
 
@@ -168,7 +172,10 @@ __device__ void do_return(Ctx& c, uint32_t id) {
   const uint32_t dem = demand_of(ctx, kv, cpu, (int32_t)R, c.p.cfg.s_in);
   // last is not reset on return (R14)
   if (tier < 2) c.R.put(atomicAdd(&s.n_r, 1u), id | (tier << 30), V, r.lastc, dem);
-  else c.W.put(atomicAdd(&s.n_w, 1u), id | (2u << 30), V, r.lastc, dem);
+  else {
+    c.W.put(atomicAdd(&s.n_w, 1u), id | (2u << 30), V, r.lastc, dem);
+    atomicAdd(&s.w2, (unsigned long long)dem);
+  }
 }
 
 // S3: arrival of request `id` at W position `pos` (Algorithm 1 lines 2-9).
@@ -190,6 +197,7 @@ __device__ void do_arrival(Ctx& c, uint32_t id, uint32_t pos, uint64_t t) {
   r.left = tr.gen_true[s0];
   c.rs[id] = r;
   c.W.put(pos, id | (2u << 30), V, (uint32_t)t, (uint32_t)L);   // R14, R31
+  atomicAdd(&c.s.w2, (unsigned long long)L);
 }
 
 // Remove the entries of list `L` (0 = R, 1 = W) whose id is INVALID.
@@ -214,7 +222,8 @@ __device__ void compact_list(SimShm& s, const List& l, int L, unsigned int& n_re
         const uint32_t hp = h[a];
         if (hp >= n_new) break;
         while (j >= 0 && (int)h[j] == src) { --j; --src; }
-        l.put(hp, l.id[src], l.V[src], l.last[src], l.dem[src]);
+        l.q[hp] = l.q[src];
+        l.dem[hp] = l.dem[src];
         --src;
       }
       n_ref = n_new;
@@ -228,12 +237,13 @@ __device__ void compact_list(SimShm& s, const List& l, int L, unsigned int& n_re
   const uint32_t n = n_ref;
   for (uint32_t base = 0; base < n; base += SIM_NT) {
     const uint32_t i = base + tid;
-    uint32_t id = INVALID, last = 0, dem = 0;
-    double V = 0;
-    if (i < n) { id = l.id[i]; if (id != INVALID) { V = l.V[i]; last = l.last[i]; dem = l.dem[i]; } }
-    const bool keep = id != INVALID;
+    QEnt x;
+    x.e = INVALID;
+    uint32_t dem = 0;
+    if (i < n) { x = l.q[i]; if (x.e != INVALID) dem = l.dem[i]; }
+    const bool keep = x.e != INVALID;
     const uint32_t pre = block_flag_scan(s, keep);  // syncs: all reads of the tile are done
-    if (keep) l.put(s.wpos + pre, id, V, last, dem);
+    if (keep) { l.q[s.wpos + pre] = x; l.dem[s.wpos + pre] = dem; }
     __syncthreads();
     if (tid == 0) s.wpos += s.wtot[SIM_NW];
     __syncthreads();
@@ -300,10 +310,10 @@ __device__ __noinline__ void prep_step(const SimParams& p, SimShm& s, uint32_t n
 
 // Order key of W entry i at iteration t (out of line: the rare rescans and
 // materialisations share one copy).
-__device__ __noinline__ uint64_t w_order_key(const SimShm& s, const uint32_t* id, const double* V,
-                                             const uint32_t* last, uint32_t i, uint64_t t) {
-  const uint32_t key = s.ip.ranking == AUGSCHED_RANK_FCFS ? 0u : sched_key(s.coef, V[i], t, last[i]);
-  return order_key(id[i], key);
+__device__ __noinline__ uint64_t w_order_key(const SimShm& s, const QEnt* q, uint32_t i, uint64_t t) {
+  const QEnt x = q[i];
+  const uint32_t key = s.ip.ranking == AUGSCHED_RANK_FCFS ? 0u : sched_key(s.coef, x.V, t, x.last);
+  return order_key(x.e, key);
 }
 
 // Grant rule of the step (R17): full demand before k*, the remainder at k*,
@@ -329,8 +339,8 @@ __device__ void run_instance(const SimParams& p, SimShm& s, uint32_t inst) {
   if (tid == 0) { s.coef = make_coef(p.cfg, p.ip[inst]); s.ip = p.ip[inst]; }
   __syncthreads();
   Ctx c{p, s, s.coef, s.ip, a.rs + off,
-        List{a.r_id + off, a.r_V + off, a.r_last + off, a.r_dem + off},
-        List{a.w_id + off, a.w_V + off, a.w_last + off, a.w_dem + off},
+        List{a.r_q + off, a.r_dem + off},
+        List{a.w_q + off, a.w_dem + off},
         a.pz_id + off, a.ret + off, a.kscr + off, a.wscr + off, a.kscr2 + off, a.wscr2 + off, 0, 0, 0};
   c.trace = p.inst_trace[inst];
   c.r0 = p.tr.req_off[c.trace];
@@ -349,10 +359,11 @@ __device__ void run_instance(const SimParams& p, SimShm& s, uint32_t inst) {
   if (tid == 0) {
     if (!H.started) {
       H.t = 0; H.A = 0; H.P = 0; H.min_ret = ~0ull; H.next_arr = 0; H.n_r = 0; H.n_w = 0; H.n_pz = 0;
+      H.w2 = 0;
       H.n_fin = 0; H.started = 1;
     }
     s.t = H.t; s.A = H.A; s.P = H.P; s.min_ret = H.min_ret; s.next_arr = H.next_arr;
-    s.n_r = H.n_r; s.n_w = H.n_w; s.n_pz = H.n_pz; s.n_fin = H.n_fin;
+    s.n_r = H.n_r; s.n_w = H.n_w; s.n_pz = H.n_pz; s.n_fin = H.n_fin; s.w2 = H.w2;
     s.nholes[0] = s.nholes[1] = 0;
     s.next_tick = s.next_arr < n ? p.tr.arr_tick[c.r0 + s.next_arr] : ~0ull;
   }
@@ -427,10 +438,10 @@ __device__ void run_instance(const SimParams& p, SimShm& s, uint32_t inst) {
         uint32_t tier = 3, d = 0;
         uint64_t Ki = 0;
         if (i < nR) {
-          const uint32_t e = c.R.id[i];
+          const QEnt x = c.R.q[i];
           d = c.R.dem[i];
-          tier = e >> 30;
-          Ki = order_key(e, key_of(c.R.V[i], t, c.R.last[i]));
+          tier = x.e >> 30;
+          Ki = order_key(x.e, key_of(x.V, t, x.last));
           c.K[i] = Ki;
           c.Ws[i] = d;
           if (tier == 0) tw0 += d; else tw1 += d;
@@ -479,42 +490,39 @@ __device__ void run_instance(const SimParams& p, SimShm& s, uint32_t inst) {
         if (s.tc[1] <= SIM_CAND) select_cand(s, 1, (int)s.tc[1], Bu, w0);
         else select_arr(s, c.K, c.Ws, nR, Bu, KBITS, false);
       } else {
-        // the prefix reaches W: this lane's two smallest W keys and their
-        // demands / positions, and the W demand total
-        uint64_t c1 = ~0ull, c2 = ~0ull;
-        uint32_t cw1 = 0, cw2 = 0, cp1 = 0, cp2 = 0;
-        unsigned long long tw2 = 0;
-        constexpr int U = SIM_UNROLL;  // entries in flight per thread (independent L2 loads)
-        for (uint32_t b0 = 0; b0 < nW; b0 += SIM_NT * U) {
-          uint32_t e[U], l[U], d[U];
-          double V[U];
-#pragma unroll
-          for (int u = 0; u < U; ++u) {
-            const uint32_t i = b0 + u * SIM_NT + tid;
-            if (i < nW) { e[u] = c.W.id[i]; V[u] = c.W.V[i]; l[u] = c.W.last[i]; d[u] = c.W.dem[i]; }
-          }
-#pragma unroll
-          for (int u = 0; u < U; ++u) {
-            const uint32_t i = b0 + u * SIM_NT + tid;
-            if (i < nW) {
-              const uint64_t Ki = order_key(e[u], key_of(V[u], t, l[u]));
-              tw2 += d[u];
-              if (Ki < c2) {
-                if (Ki < c1) { c2 = c1; cw2 = cw1; cp2 = cp1; c1 = Ki; cw1 = d[u]; cp1 = i; }
-                else { c2 = Ki; cw2 = d[u]; cp2 = i; }
-              }
-            }
-          }
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) tw2 += __shfl_xor_sync(FULL, tw2, o);
-        if (lane == 0 && tw2) warp_add64(&s.tw[2], tw2);
-        __syncthreads();
-        const unsigned long long wall = w0 + w1 + s.tw[2];
+        // the prefix reaches W.  The W demand total is maintained
+        // incrementally; when everything fits no W key is needed.
+        const unsigned long long wall = w0 + w1 + s.w2;
         if (wall < Bu) {
           if (tid == 0) { s.res.found = 0; s.res.total = wall; }   // everything admitted
           wmode = WMODE_ALL;
         } else {
+          // one pass over W: this lane's two smallest keys and their positions
+          // (one 16-byte load per entry), then their demands
+          uint64_t c1 = ~0ull, c2 = ~0ull;
+          uint32_t cp1 = 0, cp2 = 0;
+          constexpr int U = SIM_UNROLL;  // entries in flight per thread (independent L2 loads)
+          for (uint32_t b0 = 0; b0 < nW; b0 += SIM_NT * U) {
+            QEnt x[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              const uint32_t i = b0 + u * SIM_NT + tid;
+              if (i < nW) x[u] = c.W.q[i];
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              const uint32_t i = b0 + u * SIM_NT + tid;
+              if (i < nW) {
+                const uint64_t Ki = order_key(x[u].e, key_of(x[u].V, t, x[u].last));
+                if (Ki < c2) {
+                  if (Ki < c1) { c2 = c1; cp2 = cp1; c1 = Ki; cp1 = i; }
+                  else { c2 = Ki; cp2 = i; }
+                }
+              }
+            }
+          }
+          const uint32_t cw1 = c1 != ~0ull ? c.W.dem[cp1] : 0u;
+          const uint32_t cw2 = c2 != ~0ull ? c.W.dem[cp2] : 0u;
           // pop the smallest remaining W keys in order, one per round (one
           // barrier each); a lane offers c1, then c2, then rescans its own
           // positions for the next key above the last one popped
@@ -553,7 +561,7 @@ __device__ void run_instance(const SimParams& p, SimShm& s, uint32_t inst) {
                 uint64_t nk = ~0ull;
                 uint32_t nw = 0, np = 0;
                 for (uint32_t i = tid; i < nW; i += SIM_NT) {
-                  const uint64_t Ki = w_order_key(s, c.W.id, c.W.V, c.W.last, i, t);
+                  const uint64_t Ki = w_order_key(s, c.W.q, i, t);
                   if (Ki > bk && Ki < nk) { nk = Ki; nw = c.W.dem[i]; np = i; }
                 }
                 myk = nk; myw = nw; myp = np;
@@ -563,7 +571,7 @@ __device__ void run_instance(const SimParams& p, SimShm& s, uint32_t inst) {
           if (wmode != WMODE_POP) {
             // many small W demands: materialise every key and radix-select
             for (uint32_t i = tid; i < nW; i += SIM_NT) {
-              c.K[nR + i] = w_order_key(s, c.W.id, c.W.V, c.W.last, i, t);
+              c.K[nR + i] = w_order_key(s, c.W.q, i, t);
               c.Ws[nR + i] = c.W.dem[i];
             }
             if (tid == 0) s.wkeys = 1;
@@ -643,7 +651,7 @@ __device__ void run_instance(const SimParams& p, SimShm& s, uint32_t inst) {
       if (need > freev && (wmode == WMODE_ALL) && !s.wkeys) {
         // the eviction order needs the W keys of this step
         __syncthreads();
-        for (uint32_t i = tid; i < nW; i += SIM_NT) c.K[nR + i] = w_order_key(s, c.W.id, c.W.V, c.W.last, i, t);
+        for (uint32_t i = tid; i < nW; i += SIM_NT) c.K[nR + i] = w_order_key(s, c.W.q, i, t);
         if (tid == 0) s.wkeys = 1;
       }
       __syncthreads();
@@ -656,7 +664,7 @@ __device__ void run_instance(const SimParams& p, SimShm& s, uint32_t inst) {
           uint32_t w;
           if (v < nR) {
             Ki = c.K[v];
-            w = (uint32_t)c.rs[c.R.id[v] & 0xFFFF].kv + grant(Ki, c.R.dem[v]);
+            w = (uint32_t)c.rs[c.R.q[v].e & 0xFFFF].kv + grant(Ki, c.R.dem[v]);
           } else {
             const uint32_t j = v - nR;
             Ki = w_key(j);
@@ -681,16 +689,18 @@ __device__ void run_instance(const SimParams& p, SimShm& s, uint32_t inst) {
           cinc(s, AUGSCHED_R_EVICTIONS);
           if (v < nR) {
             // running / swapped entry: drop its KV and requeue it in W
-            const uint32_t id = c.R.id[v] & 0xFFFF;
+            const QEnt x = c.R.q[v];
+            const uint32_t id = x.e & 0xFFFF;
             ReqState r = c.rs[id];
             atomicAdd((unsigned long long*)&s.A, (unsigned long long)(-(long long)r.kv));
             r.kv = 0;
             r.cpu = 0;
             r.meta = meta_with(r.meta, ST_WAIT, meta_pol(r.meta));
             c.rs[id] = r;
-            c.W.put(atomicAdd(&s.n_w, 1u), id | (2u << 30), c.R.V[v], c.R.last[v],
-                    demand_of(r.ctx, 0, 0, r.pend, p.cfg.s_in));
-            c.R.id[v] = INVALID;
+            const uint32_t nd = demand_of(r.ctx, 0, 0, r.pend, p.cfg.s_in);
+            c.W.put(atomicAdd(&s.n_w, 1u), id | (2u << 30), x.V, x.last, nd);
+            atomicAdd(&s.w2, (unsigned long long)nd);
+            c.R.q[v].e = INVALID;
             c.K[v] |= KEVICT;
             mark_hole(s, 0, v);
           } else {
@@ -707,6 +717,7 @@ __device__ void run_instance(const SimParams& p, SimShm& s, uint32_t inst) {
     {
       uint32_t my_tok = 0, my_adm = 0;
       long long accA = 0, accP = 0;
+      unsigned long long accW2 = 0;   // demand leaving W
       const uint32_t nv = nR + nGW;
       for (uint32_t v = tid; v < nv; v += SIM_NT) {
         const bool inR = v < nR;
@@ -714,14 +725,14 @@ __device__ void run_instance(const SimParams& p, SimShm& s, uint32_t inst) {
         uint64_t Ki;
         if (inR) {
           pos = v;
-          e = c.R.id[v];
+          e = c.R.q[v].e;
           if (e == INVALID) continue;        // evicted to W this step
           Ki = c.K[v];
           dem = c.R.dem[v];
         } else {
           const uint32_t j = v - nR;
           pos = w_pos(j);
-          e = c.W.id[pos];
+          e = c.W.q[pos].e;
           Ki = w_key(j);
           dem = wmode == WMODE_POP ? s.pw[j] : c.W.dem[pos];
         }
@@ -799,16 +810,17 @@ __device__ void run_instance(const SimParams& p, SimShm& s, uint32_t inst) {
         accP += dP;
         const uint32_t nd = demand_of(ctx, kv, cpu, pend, p.cfg.s_in);
         if (inR) {
-          if (leave) { c.R.id[pos] = INVALID; mark_hole(s, 0, pos); }
+          if (leave) { c.R.q[pos].e = INVALID; mark_hole(s, 0, pos); }
           else {                                         // tier 0: running (R16, R14)
-            c.R.id[pos] = id;
-            c.R.last[pos] = (uint32_t)t;
+            c.R.q[pos].e = id;
+            c.R.q[pos].last = (uint32_t)t;
             c.R.dem[pos] = nd;
           }
         } else {
           // a granted waiting entry ends the step running: move it to R
-          if (!leave) c.R.put(atomicAdd(&s.n_r, 1u), id, c.W.V[pos], (uint32_t)t, nd);
-          c.W.id[pos] = INVALID;
+          if (!leave) c.R.put(atomicAdd(&s.n_r, 1u), id, c.W.q[pos].V, (uint32_t)t, nd);
+          c.W.q[pos].e = INVALID;
+          accW2 += dem;
           mark_hole(s, 1, pos);
         }
       }
@@ -819,12 +831,14 @@ __device__ void run_instance(const SimParams& p, SimShm& s, uint32_t inst) {
         my_adm += __shfl_xor_sync(FULL, my_adm, o);
         accA += __shfl_xor_sync(FULL, accA, o);
         accP += __shfl_xor_sync(FULL, accP, o);
+        accW2 += __shfl_xor_sync(FULL, accW2, o);
       }
       if (lane == 0) {
         if (my_tok) cinc(s, AUGSCHED_R_TOKENS, my_tok);
         if (my_adm) cinc(s, AUGSCHED_R_ADMITTED, my_adm);
         if (accA) warp_add64((unsigned long long*)&s.A, (unsigned long long)accA);
         if (accP) warp_add64((unsigned long long*)&s.P, (unsigned long long)accP);
+        if (accW2) warp_add64(&s.w2, 0ull - accW2);
       }
     }
     compact_list(s, c.R, 0, s.n_r);  // syncs
@@ -845,7 +859,7 @@ __device__ void run_instance(const SimParams& p, SimShm& s, uint32_t inst) {
   __syncthreads();
   if (tid == 0) {
     H.t = s.t; H.A = s.A; H.P = s.P; H.min_ret = s.min_ret; H.next_arr = s.next_arr;
-    H.n_r = s.n_r; H.n_w = s.n_w; H.n_pz = s.n_pz; H.n_fin = s.n_fin;
+    H.n_r = s.n_r; H.n_w = s.n_w; H.n_pz = s.n_pz; H.n_fin = s.n_fin; H.w2 = s.w2;
     s.cnt[AUGSCHED_R_FINAL_T] = s.t;
   }
   __syncthreads();

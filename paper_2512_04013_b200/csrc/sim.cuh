@@ -32,10 +32,10 @@ constexpr int SIM_RB = SIM_NT >= 256 ? 8 : 5;   // radix bits of the fallback se
 #endif
 constexpr int SIM_CAND = AUGSCHED_SIM_CAND;      // small-candidate list capacity
 #ifndef AUGSCHED_SIM_MINB
-#define AUGSCHED_SIM_MINB 32
+#define AUGSCHED_SIM_MINB 24
 #endif
 #ifndef AUGSCHED_SIM_UNROLL
-#define AUGSCHED_SIM_UNROLL 1
+#define AUGSCHED_SIM_UNROLL 2
 #endif
 constexpr int SIM_MINB = AUGSCHED_SIM_MINB;   // CTAs per SM the kernel is register-bounded for
 constexpr int SIM_UNROLL = AUGSCHED_SIM_UNROLL;  // queue entries in flight per thread in the key pass
@@ -64,6 +64,7 @@ struct InstHdr {
   uint64_t t;
   int64_t A, P;           // KV ledger in tokens: active, Preserve-paused
   uint64_t min_ret;       // min return tick over the paused list
+  uint64_t w2;            // demand total of the W list
   uint32_t next_arr, n_r, n_w, n_pz, n_fin;
   uint32_t started;
 };
@@ -81,20 +82,23 @@ struct __align__(32) ReqState {
   uint32_t left;       // tokens still to decode in the current segment
 };
 
+// Scoring record of one queued request (one 16-byte vector load).
+struct __align__(16) QEnt {
+  double V;            // value (Stage I / II / final), fixed between events
+  uint32_t last;       // last-scheduled iteration (R14)
+  uint32_t e;          // request id | tier << 30
+};
+
 // Handle-owned per-instance arena (stride = max_active entries per instance).
 struct Arena {
   // cold state by request id
   ReqState* rs;
   uint64_t* ret;       // return tick of the outstanding call
   // queue lists by position (tier-split): R = running u swapped (tier 0/1),
-  // W = waiting (tier 2); entry = id | tier << 30, V, last, demand
-  uint32_t* r_id;
-  double* r_V;
-  uint32_t* r_last;
+  // W = waiting (tier 2); scoring record + demand
+  QEnt* r_q;
   uint32_t* r_dem;
-  uint32_t* w_id;
-  double* w_V;
-  uint32_t* w_last;
+  QEnt* w_q;
   uint32_t* w_dem;
   // paused list by position
   uint32_t* pz_id;
