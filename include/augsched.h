@@ -70,6 +70,9 @@ extern "C" {
 
 #define AUGSCHED_RANK_AUGSERVE 0      /* value order of Eq.26 */
 #define AUGSCHED_RANK_FCFS 1          /* key = 0: order (tier, id) (R33) */
+#define AUGSCHED_RANK_RANDOM 2        /* random scheduling of P:266-273: a fresh shuffle every
+                                         iteration, key = hi32(mix(mix(rank_seed<<32 | id) ^ t))
+                                         with mix = the SplitMix64 output function (reading B8) */
 #define AUGSCHED_BUDGET_DYNAMIC 0     /* Eq.27-32 + clamp */
 #define AUGSCHED_BUDGET_STATIC 1      /* fixed l_static tokens */
 #define AUGSCHED_POLICY_ARGMIN 0      /* Eq.7-8 */
@@ -88,7 +91,7 @@ typedef struct augsched_instance_params {
   uint32_t ranking;          /* AUGSCHED_RANK_* */
   uint32_t budget_mode;      /* AUGSCHED_BUDGET_* */
   uint32_t policy_mode;      /* AUGSCHED_POLICY_* */
-  uint32_t reserved;         /* must be 0 */
+  uint32_t rank_seed;        /* seed of AUGSCHED_RANK_RANDOM (ignored otherwise) */
 } augsched_instance_params;
 
 /* System constants (SPEC SimConfig). */

@@ -45,7 +45,7 @@ class OInst(C.Structure):
     _fields_ = [("target_max", C.c_uint32), ("l_static", C.c_uint32), ("alpha", C.c_double),
                 ("slo_ttft_ticks", C.c_uint64), ("slo_norm_num", C.c_uint32),
                 ("slo_norm_den", C.c_uint32), ("ranking", C.c_uint32),
-                ("budget_mode", C.c_uint32), ("policy_mode", C.c_uint32), ("pad_", C.c_uint32)]
+                ("budget_mode", C.c_uint32), ("policy_mode", C.c_uint32), ("rank_seed", C.c_uint32)]
 
 
 class OTrace(C.Structure):
@@ -89,6 +89,10 @@ def lib():
         L.oracle_hist_bin.argtypes = [C.c_uint64]
         L.oracle_hist_bin.restype = C.c_uint32
         L.oracle_result_size.restype = C.c_uint32
+        L.oracle_splitmix64_mix.argtypes = [C.c_uint64]
+        L.oracle_splitmix64_mix.restype = C.c_uint64
+        L.oracle_random_key.argtypes = [C.c_uint32, C.c_uint32, C.c_uint64]
+        L.oracle_random_key.restype = C.c_uint32
         assert L.oracle_result_size() == RESULT_DTYPE.itemsize
     return _lib
 
@@ -105,7 +109,8 @@ def make_inst(p: dict) -> np.ndarray:
         arr[i] = OInst(int(p["target_max"][i]), int(p["l_static"][i]), float(p["alpha"][i]),
                        int(p["slo_ttft_ticks"][i]), int(p["slo_norm_num"][i]),
                        int(p["slo_norm_den"][i]), int(p["ranking"][i]),
-                       int(p["budget_mode"][i]), int(p["policy_mode"][i]), 0)
+                       int(p["budget_mode"][i]), int(p["policy_mode"][i]),
+                       int(p["rank_seed"][i]) if "rank_seed" in p else 0)
     return arr
 
 
@@ -185,6 +190,14 @@ def final(cfg, target_max, V2, X, next_pol, An):
 
 def key(V, alpha, Ts, now, last):
     return lib().oracle_key(V, alpha, Ts, now, last)
+
+
+def splitmix64_mix(z):
+    return lib().oracle_splitmix64_mix(z)
+
+
+def random_key(seed, id_, t):
+    return lib().oracle_random_key(seed, id_, t)
 
 
 def budget(cfg, target_max, A, P):

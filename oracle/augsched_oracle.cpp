@@ -44,10 +44,10 @@ struct OInst {                // per-instance sweep parameters
   double alpha;               // anti-starvation coefficient (Eq.26)
   uint64_t slo_ttft_ticks;    // TTFT SLO
   uint32_t slo_norm_num, slo_norm_den;  // normalized latency < num/den * T
-  uint32_t ranking;           // 0 AugServe value order, 1 FCFS
+  uint32_t ranking;           // 0 AugServe value order, 1 FCFS, 2 random
   uint32_t budget_mode;       // 0 dynamic (Eq.27-32), 1 static
   uint32_t policy_mode;       // 0 argmin (Eq.7-8), 1 Preserve, 2 Swap, 3 Discard
-  uint32_t pad_;
+  uint32_t rank_seed;         // seed of random scheduling (ranking 2)
 };
 
 struct OTrace {               // CSR trace set produced by tracegen/
@@ -165,6 +165,29 @@ uint32_t sched_key(double V, double alpha, double Ts, uint64_t now, uint64_t las
   uint32_t u;
   std::memcpy(&u, &f, 4);
   return (u & 0x80000000u) ? ~u : (u | 0x80000000u);  // order-preserving u32
+}
+
+// ---- random scheduling ("shuffle the request order") ----------
+// Reading B8: a fresh shuffle every iteration, drawn from a
+// counter-based generator so both implementations draw the same numbers:
+// the SplitMix64 output function applied twice, to (seed << 32 | id) and then
+// xor-ed with the iteration; the key is the high 32 bits.
+uint64_t splitmix64_mix(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+uint32_t random_key(uint32_t seed, uint32_t id, uint64_t t) {
+  const uint64_t a = splitmix64_mix(((uint64_t)seed << 32) | id);
+  return (uint32_t)(splitmix64_mix(a ^ t) >> 32);
+}
+
+// The order key of a queued request: Eq.26 value order, FCFS or random.
+uint32_t order_key(const OInst& ip, double V, double Ts, uint64_t now, uint64_t last, uint32_t id) {
+  if (ip.ranking == 1) return 0u;                        // FCFS (R33)
+  if (ip.ranking == 2) return random_key(ip.rank_seed, id, now);
+  return sched_key(V, ip.alpha, Ts, now, last);
 }
 
 // ---- Eq.27-32 + clamp (Algorithm 1 lines 25-27) ---------------
@@ -317,7 +340,7 @@ void simulate_one(const OCfg& cfg, const OInst& ip, const OTrace& tr, uint32_t t
     for (uint32_t id : active) {
       const Req& r = R[id];
       int tier = r.status == RUNNING ? 0 : r.status == SWAPPED ? 1 : 2;  // R16
-      uint32_t key = ip.ranking == 1 ? 0u : sched_key(r.V, ip.alpha, k.Ts, t, r.last);
+      uint32_t key = order_key(ip, r.V, k.Ts, t, r.last, id);
       ord.push_back({tier, key, id});
     }
     // S6 order: running => swapped => waiting, each by value, ties by id (R2)
@@ -559,7 +582,7 @@ int step_one(OStep& S, uint32_t i, uint64_t now, int64_t* B_out, uint32_t* n_out
   for (uint32_t id = 0; id < S.max_active; ++id) {
     const SSlot& s = I.s[id];
     if (s.status < RUNNING || s.status > WAITING) continue;
-    uint32_t key = ip.ranking == 1 ? 0u : sched_key(s.V, ip.alpha, k.Ts, now, s.last);
+    uint32_t key = order_key(ip, s.V, k.Ts, now, s.last, id);
     ord.push_back({s.status - RUNNING, key, id});
   }
   std::sort(ord.begin(), ord.end(), [](const Ent& a, const Ent& b) {
@@ -694,6 +717,8 @@ int64_t oracle_budget(const OCfg* c, uint32_t target_max, int64_t A, int64_t P) 
   return token_budget(*c, cap_tokens(*c), A, P, clamp_bounds(*c, target_max));
 }
 int64_t oracle_cap(const OCfg* c) { return cap_tokens(*c); }
+uint64_t oracle_splitmix64_mix(uint64_t z) { return splitmix64_mix(z); }
+uint32_t oracle_random_key(uint32_t seed, uint32_t id, uint64_t t) { return random_key(seed, id, t); }
 uint32_t oracle_hist_bin(uint64_t v) { return hist_bin(v); }
 uint32_t oracle_result_size(void) { return (uint32_t)sizeof(OResult); }
 

@@ -37,7 +37,7 @@ class InstanceParams(C.Structure):
     _fields_ = [("target_max", C.c_uint32), ("l_static", C.c_uint32), ("alpha", C.c_double),
                 ("slo_ttft_ticks", C.c_uint64), ("slo_norm_num", C.c_uint32),
                 ("slo_norm_den", C.c_uint32), ("ranking", C.c_uint32), ("budget_mode", C.c_uint32),
-                ("policy_mode", C.c_uint32), ("reserved", C.c_uint32)]
+                ("policy_mode", C.c_uint32), ("rank_seed", C.c_uint32)]
 
 
 class Config(C.Structure):
@@ -117,7 +117,8 @@ def make_config(cfg: dict, defaults: dict | None = None) -> Config:
 def _params_struct(d: dict) -> InstanceParams:
     return InstanceParams(int(d["target_max"]), int(d["l_static"]), float(d["alpha"]),
                           int(d["slo_ttft_ticks"]), int(d["slo_norm_num"]), int(d["slo_norm_den"]),
-                          int(d["ranking"]), int(d["budget_mode"]), int(d["policy_mode"]), 0)
+                          int(d["ranking"]), int(d["budget_mode"]), int(d["policy_mode"]),
+                          int(d.get("rank_seed", 0)))
 
 
 def params_array(p: dict):

@@ -97,7 +97,7 @@ int validate_params(const augsched_instance_params& p, uint32_t i) {
   if (!(p.alpha >= 0.0) || !std::isfinite(p.alpha))
     return fail(AUGSCHED_E_INVALID, "instance %u: alpha must be finite and >= 0", i);
   if (p.slo_norm_den < 1) return fail(AUGSCHED_E_INVALID, "instance %u: slo_norm_den must be >= 1", i);
-  if (p.ranking > 1 || p.budget_mode > 1 || p.policy_mode > 3 || p.reserved != 0)
+  if (p.ranking > 2 || p.budget_mode > 1 || p.policy_mode > 3)
     return fail(AUGSCHED_E_INVALID, "instance %u: bad ranking/budget_mode/policy_mode", i);
   if (p.l_static > (1u << 26)) return fail(AUGSCHED_E_INVALID, "instance %u: l_static too large", i);
   return AUGSCHED_OK;

@@ -122,6 +122,26 @@ __device__ __forceinline__ uint32_t sched_key(const Coef& k, double V, uint64_t 
   return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
 }
 
+// Random scheduling (reading B8): SplitMix64 output function and the
+// per-iteration key of request `id`.
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+__device__ __forceinline__ uint32_t random_key(uint32_t seed, uint32_t id, uint64_t t) {
+  return (uint32_t)(mix64(mix64(((uint64_t)seed << 32) | id) ^ t) >> 32);
+}
+
+// Score key of a queued request under the instance's ranking mode.
+__device__ __forceinline__ uint32_t rank_key(const Coef& k, const augsched_instance_params& ip, double V,
+                                             uint64_t now, uint64_t last, uint32_t id) {
+  if (ip.ranking == AUGSCHED_RANK_FCFS) return 0u;
+  if (ip.ranking == AUGSCHED_RANK_RANDOM) return random_key(ip.rank_seed, id, now);
+  return sched_key(k, V, now, last);
+}
+
 // Eq.27-32 + clamp in whole tokens (R19); static mode returns l_static.
 __device__ __forceinline__ int64_t token_limit(const augsched_config& c, const Coef& k,
                                                const augsched_instance_params& p, int64_t cap,

@@ -312,8 +312,7 @@ __device__ __noinline__ void prep_step(const SimParams& p, SimShm& s, uint32_t n
 // materialisations share one copy).
 __device__ __noinline__ uint64_t w_order_key(const SimShm& s, const QEnt* q, uint32_t i, uint64_t t) {
   const QEnt x = q[i];
-  const uint32_t key = s.ip.ranking == AUGSCHED_RANK_FCFS ? 0u : sched_key(s.coef, x.V, t, x.last);
-  return order_key(x.e, key);
+  return order_key(x.e, rank_key(s.coef, s.ip, x.V, t, x.last, x.e & 0xFFFF));
 }
 
 // Grant rule of the step (R17): full demand before k*, the remainder at k*,
@@ -371,9 +370,8 @@ __device__ void run_instance(const SimParams& p, SimShm& s, uint32_t inst) {
   __syncthreads();
   if (tid == 0) s.cnt[AUGSCHED_R_NREQ] = n;
   const int64_t cap = p.cap;
-  const bool fcfs = c.ip.ranking == AUGSCHED_RANK_FCFS;
-  auto key_of = [&](double V, uint64_t t, uint32_t last) -> uint32_t {
-    return fcfs ? 0u : sched_key(c.k, V, t, last);
+  auto key_of = [&](double V, uint64_t t, uint32_t last, uint32_t e) -> uint32_t {
+    return rank_key(c.k, c.ip, V, t, last, e & 0xFFFF);
   };
 
   if (tid == 0) prep_step(p, s, n);
@@ -441,7 +439,7 @@ __device__ void run_instance(const SimParams& p, SimShm& s, uint32_t inst) {
           const QEnt x = c.R.q[i];
           d = c.R.dem[i];
           tier = x.e >> 30;
-          Ki = order_key(x.e, key_of(x.V, t, x.last));
+          Ki = order_key(x.e, key_of(x.V, t, x.last, x.e));
           c.K[i] = Ki;
           c.Ws[i] = d;
           if (tier == 0) tw0 += d; else tw1 += d;
@@ -513,7 +511,7 @@ __device__ void run_instance(const SimParams& p, SimShm& s, uint32_t inst) {
             for (int u = 0; u < U; ++u) {
               const uint32_t i = b0 + u * SIM_NT + tid;
               if (i < nW) {
-                const uint64_t Ki = order_key(x[u].e, key_of(x[u].V, t, x[u].last));
+                const uint64_t Ki = order_key(x[u].e, key_of(x[u].V, t, x[u].last, x[u].e));
                 if (Ki < c2) {
                   if (Ki < c1) { c2 = c1; cp2 = cp1; c1 = Ki; cp1 = i; }
                   else { c2 = Ki; cp2 = i; }

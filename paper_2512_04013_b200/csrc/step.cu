@@ -209,8 +209,8 @@ __global__ void __launch_bounds__(KNT) keys_kernel(KeyArgs a) {
       inst = MA == a.N ? 0u : s / MA;
       const uint32_t stv = a.S.st[s] & 15;
       tier = (stv >= ST_RUN && stv <= ST_WAIT) ? stv - ST_RUN : 3u;
-      if (tier < 3 && a.S.ip[inst].ranking != AUGSCHED_RANK_FCFS)
-        key = sched_key(a.S.coef[inst], a.S.V[s], a.now, a.S.last[s]);
+      if (tier < 3)
+        key = rank_key(a.S.coef[inst], a.S.ip[inst], a.S.V[s], a.now, a.S.last[s], s - inst * MA);
       if (s == inst * MA)
         a.budget[inst] = token_limit(a.cfg, a.S.coef[inst], a.S.ip[inst], a.cap,
                                      ld_ll(&a.S.A[inst]), ld_ll(&a.S.P[inst]));

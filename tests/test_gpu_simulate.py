@@ -95,7 +95,7 @@ def test_random_mixed_parity(seed):
     tr = tracegen.gen_traces(6, 300, [1.0, 3.0, 6.0, 10.0, 20.0, 40.0], seed=seed, p_nocall=0.25)
     n = 48
     ip = tracegen.inst_params(
-        n, ranking=rng.integers(0, 2, n), budget_mode=rng.integers(0, 2, n),
+        n, ranking=rng.integers(0, 3, n), rank_seed=rng.integers(0, 2**32, n), budget_mode=rng.integers(0, 2, n),
         policy_mode=rng.integers(0, 4, n), target_max=rng.integers(1, 3000, n),
         l_static=rng.integers(0, 3000, n), alpha=rng.choice([0.0, 1e3, 4.6e7, 1e12], n),
         slo_ttft_ticks=rng.integers(10**5, 10**7, n))

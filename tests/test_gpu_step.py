@@ -74,14 +74,14 @@ def random_events(rng, slots, now, p_new=0.3):
 
 @pytest.mark.parametrize("seed,cap", [(1, 10**6), (2, 900), (3, 400)])
 def test_random_event_stream(seed, cap):
-    """3 instances x 64 slots, 40 steps of random NEW/CALL/RETURN/FINISH
+    """4 instances x 64 slots (value, FCFS and random ranking), 40 steps of random NEW/CALL/RETURN/FINISH
     events; small caps force demotion and tail eviction every few steps."""
     rng = np.random.default_rng(seed)
-    n_inst, MA = 3, 64
+    n_inst, MA = 4, 64
     cfg = dict(tracegen.PRESET_G0, g_total=1000 + cap, g_model=1000)
-    ip = tracegen.inst_params(n_inst, base=tracegen.INST_G0, ranking=[0, 1, 0], budget_mode=[1, 0, 0],
-                              l_static=150, target_max=[50, 200, 120], alpha=[0.0, 0.0, 3.0],
-                              policy_mode=[0, 0, 0])
+    ip = tracegen.inst_params(n_inst, base=tracegen.INST_G0, ranking=[0, 1, 0, 2], budget_mode=[1, 0, 0, 0],
+                              l_static=150, target_max=[50, 200, 120, 90], alpha=[0.0, 0.0, 3.0, 0.0],
+                              policy_mode=[0, 0, 0, 0], rank_seed=[0, 0, 0, 12345 + seed])
     st = oracle.Step(cfg, ip, MA)
     s = aug.Scheduler(cfg, ip, n_inst, MA)
     for t in range(40):

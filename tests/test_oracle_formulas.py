@@ -224,3 +224,26 @@ def test_hist_bins():
     b = [oracle.hist_bin(v) for v in range(0, 5000)]
     assert all(x <= y for x, y in zip(b, b[1:]))
     assert oracle.hist_bin(2**62) == 159
+
+
+# ---- random scheduling (reading B8) ------------------------------
+def test_splitmix64_known_answers():
+    """The counter-based generator is SplitMix64's output function: its first
+    outputs from state 0 and 1 are the published reference values."""
+    assert oracle.splitmix64_mix(0) == 0xE220A8397B1DCDAF
+    assert oracle.splitmix64_mix(1) == 0x910A2DEC89025CC1
+
+
+def test_random_ranking_reshuffles_every_iteration():
+    """Random scheduling 'shuffles the request order': for a fixed
+    pair of requests the relative order flips about half of the iterations,
+    keys are spread uniformly, and different seeds give different orders."""
+    import numpy as np
+    flips = sum(oracle.random_key(7, 3, t) < oracle.random_key(7, 11, t) for t in range(4000))
+    assert 1800 < flips < 2200
+    keys = np.array([oracle.random_key(1, i, 99) for i in range(20000)], np.uint64)
+    hist = np.bincount((keys >> np.uint64(28)).astype(np.int64), minlength=16)
+    assert hist.min() > 20000 / 16 * 0.85 and hist.max() < 20000 / 16 * 1.15
+    a = [oracle.random_key(1, i, 5) for i in range(64)]
+    b = [oracle.random_key(2, i, 5) for i in range(64)]
+    assert np.argsort(a).tolist() != np.argsort(b).tolist()

@@ -244,11 +244,11 @@ def small_traces():
 
 def test_invariants_random_runs(small_traces):
     cfg = tracegen.PRESET_7B
-    n_inst = 4 * 6
-    tid = np.repeat(np.arange(4), 6).astype(np.uint32)
-    ip = tracegen.inst_params(n_inst, ranking=[0, 1, 0, 0, 0, 0] * 4,
-                              budget_mode=[0, 0, 1, 0, 0, 0] * 4,
-                              policy_mode=[0, 0, 0, 1, 2, 3] * 4)
+    n_inst = 4 * 7
+    tid = np.repeat(np.arange(4), 7).astype(np.uint32)
+    ip = tracegen.inst_params(n_inst, ranking=[0, 1, 0, 0, 0, 0, 2] * 4,
+                              budget_mode=[0, 0, 1, 0, 0, 0, 0] * 4,
+                              policy_mode=[0, 0, 0, 1, 2, 3, 0] * 4, rank_seed=([0] * 6 + [99]) * 4)
     res = oracle.simulate(cfg, ip, small_traces, tid)
     for i in range(n_inst):
         d = oracle.as_dict(res[i])

@@ -276,9 +276,10 @@ INST_7B = dict(
     slo_ttft_ticks=1_000_000,
     slo_norm_num=10,
     slo_norm_den=1,
-    ranking=0,       # 0 = AugServe two-stage values, 1 = FCFS
+    ranking=0,       # 0 = AugServe two-stage values, 1 = FCFS, 2 = random
     budget_mode=0,   # 0 = dynamic (Eq.27-32 + clamp), 1 = static l_static
     policy_mode=0,   # 0 = adaptive argmin, 1/2/3 = forced Preserve/Swap/Discard
+    rank_seed=0,     # seed of random scheduling
 )
 
 # Hand-worked goldens' system: M = 1, T = 0.1 s, N = 50, S_in = S_out = 200
@@ -299,7 +300,7 @@ PRESET_G0 = dict(
 )
 INST_G0 = dict(
     target_max=50, l_static=100, alpha=0.0, slo_ttft_ticks=1_000_000,
-    slo_norm_num=10, slo_norm_den=1, ranking=0, budget_mode=1, policy_mode=0,
+    slo_norm_num=10, slo_norm_den=1, ranking=0, budget_mode=1, policy_mode=0, rank_seed=0,
 )
 
 
@@ -310,9 +311,9 @@ def inst_params(n: int, base: dict | None = None, **overrides) -> dict:
     out = {}
     dt = dict(target_max=np.uint32, l_static=np.uint32, alpha=np.float64,
               slo_ttft_ticks=np.uint64, slo_norm_num=np.uint32, slo_norm_den=np.uint32,
-              ranking=np.uint32, budget_mode=np.uint32, policy_mode=np.uint32)
+              ranking=np.uint32, budget_mode=np.uint32, policy_mode=np.uint32, rank_seed=np.uint32)
     for k, t in dt.items():
-        v = overrides.get(k, base[k])
+        v = overrides.get(k, base.get(k, 0))
         a = np.asarray(v, dtype=t)
         out[k] = np.ascontiguousarray(np.broadcast_to(a, (n,)).astype(t))
     return out
