@@ -312,3 +312,30 @@ def test_max_iters_prefix(small_traces):
     assert cut["final_t"] >= full["final_t"] // 2
     assert cut["completed"] <= full["completed"]
     assert cut["busy_steps"] < full["busy_steps"]
+
+
+def test_ablation_directions():
+    """Directional reproduction of the paper's comparative findings inside the
+    simulator (SPEC acceptance 4 and 8): on an
+    overloaded 7B-preset workload (4 traces x 500 requests at 4 req/s)
+      - random scheduling beats FCFS,
+      - AugServe's goodput is >= 1.5x FCFS and its mean TTFT <= 0.5x FCFS,
+      - the dynamic token limit helps FCFS and AugServe (ablation),
+      - the two-stage ordering adds on top of dynamic batching."""
+    tr = tracegen.gen_traces(4, 500, [4.0] * 4, seed=21)
+    tid = np.arange(4, dtype=np.uint32)
+    modes = {"augserve": dict(ranking=0, budget_mode=0), "aug_static": dict(ranking=0, budget_mode=1),
+             "fcfs_static": dict(ranking=1, budget_mode=1), "fcfs_dyn": dict(ranking=1, budget_mode=0),
+             "random_static": dict(ranking=2, budget_mode=1, rank_seed=5)}
+    good, ttft = {}, {}
+    for name, m in modes.items():
+        ip = tracegen.inst_params(4, l_static=500, **m)
+        d = [oracle.as_dict(x) for x in oracle.simulate(tracegen.PRESET_7B, ip, tr, tid, threads=4)]
+        good[name] = sum(x["slo_ok"] for x in d)
+        ttft[name] = sum(x["sum_ttft_ticks"] for x in d) / sum(x["completed"] for x in d)
+    assert good["random_static"] > good["fcfs_static"]
+    assert good["augserve"] >= 1.5 * good["fcfs_static"]
+    assert ttft["augserve"] <= 0.5 * ttft["fcfs_static"]
+    assert good["fcfs_dyn"] > good["fcfs_static"]
+    assert good["augserve"] > good["aug_static"]
+    assert good["augserve"] > good["fcfs_dyn"]
