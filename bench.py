@@ -170,45 +170,51 @@ def run_reference(args):
 
 
 # ----------------------------------------------------------------------------- cfg4 step
-def step_bench(args, dev, stream, peak):
-    """Config 4: augsched_step over one 1,000,000-request queue (scores, full
-    stable order, admission, grant accounting), K consecutive steps, each
-    timed with CUDA events after an L2 flush (working set ~60 MB < L2)."""
+def step_bench(args, dev, stream, peak, prefix=False, n_override=None):
+    """Config 4: one scheduling step over one 1,000,000-request queue, K
+    consecutive steps, each timed with CUDA events after an L2 flush (the
+    working set, ~60 MB, fits in L2).  prefix=False: augsched_step (scores,
+    full stable order, admission, grant accounting); prefix=True:
+    augsched_step_prefix (the same decisions, order produced for the
+    admitted prefix only)."""
     import torch
     import paper_2512_04013_b200 as aug
-    n = args.step_n
+    n = n_override or args.step_n
     rec = tracegen.cfg4_records(n)
     s = aug.Scheduler(tracegen.PRESET_CFG4, tracegen.inst_params(1), 1, n, device=dev, stream=stream)
     s.enqueue(0, rec)
     flush = torch.empty(512 * 2**20, dtype=torch.uint8, device=f"cuda:{dev}")
     t = 65536
     for _ in range(args.warmup):
-        s.step(t); t += 1
+        s.step(t, prefix=prefix); t += 1
     torch.cuda.synchronize()
     l0 = s.launches
     cold, warm = [], []
     for _ in range(args.steps):
         flush.zero_()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream); s.step(t); b.record(stream); t += 1
+        a.record(stream); s.step(t, prefix=prefix); b.record(stream); t += 1
         torch.cuda.synchronize()
         cold.append(a.elapsed_time(b))
     for _ in range(args.steps):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream); s.step(t); b.record(stream); t += 1
+        a.record(stream); s.step(t, prefix=prefix); b.record(stream); t += 1
         torch.cuda.synchronize()
         warm.append(a.elapsed_time(b))
     launches = (s.launches - l0) // (2 * args.steps)
     s.close()
     ms = float(np.median(cold))
     ach = 32.0 * n / (ms / 1e3) / 1e9
+    what = ("augsched_step_prefix: keys + top-digit histogram, collect, one-block select/sort/admit/apply"
+            if prefix else "augsched_step: keys + 4 LSD sort passes + admit/resolve/apply")
     return {"workload": f"cfg4: one queue of {n} requests (512 running, 512 swapped, rest waiting "
-                        "80% Stage I / 20% Stage II), full stable order + admission per step",
+                        "80% Stage I / 20% Stage II), " + ("admitted prefix" if prefix else "full stable order") +
+                        " + admission per step",
             "value": n / (ms / 1e3), "unit": UNIT, "ms_per_step_cold_l2": ms,
             "ms_per_step_warm_l2": float(np.median(warm)), "launches_per_step": launches,
             "roofline": {"bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(ach / peak, 4), "traffic": None,
-                         "note": "whole step (keys + 5 sort passes + admit/resolve/apply), 32 B/decision"}}
+                         "note": what + "; 32 B/decision, whole step, L2 flushed before each step"}}
 
 
 # ----------------------------------------------------------------------------- GPU arm
@@ -357,6 +363,15 @@ def run_gpu(args):
         s2.close()
     if rank == 0 and not args.no_step:
         line["step_1m"] = step_bench(args, dev, stream, peak)
+        line["step_1m_prefix"] = step_bench(args, dev, stream, peak, prefix=True)
+        # size sweep of the prefix step: queues beyond L2 show the HBM-bound regime
+        sweep = {}
+        for n_sw in (4_194_304, 16_777_216):
+            r_sw = step_bench(args, dev, stream, peak, prefix=True, n_override=n_sw)
+            sweep[str(n_sw)] = {"value": r_sw["value"], "ms_per_step_cold_l2": r_sw["ms_per_step_cold_l2"],
+                                "roofline_frac": r_sw["roofline"]["frac"],
+                                "achieved_gbs": r_sw["roofline"]["achieved"]}
+        line["step_1m_prefix"]["size_sweep"] = sweep
     if rank == 0 and world == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline(args, tr, ip, tid, W * (args.warmup + args.steps),
                                             sample=args.cpu_sample or None)

@@ -218,6 +218,17 @@ AUGSCHED_API int augsched_enqueue(augsched_t* h, uint32_t instance, const augsch
  * with device pointers.  Asynchronous. */
 AUGSCHED_API int augsched_step(augsched_t* h, uint64_t now_iter, augsched_step_out* out);
 
+/* The same decision round as augsched_step (identical grants, limits, queue
+ * sizes and state updates), producing the order only for the admitted
+ * prefix: order/key/grant are valid for positions [0, admitted) of each
+ * instance; later positions are not written.  Every queued request has
+ * demand >= 1, so the admitted prefix lies within the first min(B, n)
+ * entries of the order; a single-instance handle whose largest token limit
+ * is <= 8192 finds them by a count-based selection (keys + one histogram
+ * pass, a collect pass, one block that sorts and admits them) instead of a
+ * full sort; any other handle runs augsched_step.  Asynchronous. */
+AUGSCHED_API int augsched_step_prefix(augsched_t* h, uint64_t now_iter, augsched_step_out* out);
+
 /* Run every instance's simulation (Algorithm 1 + engine model + metrics) until
  * all its requests finished or its iteration counter reaches max_iters.
  * inst_trace_id[i] selects instance i's trace.  results: n_instances records.

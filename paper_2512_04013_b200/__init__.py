@@ -29,7 +29,7 @@ RESULT_FIELDS = [
 NBIN = 160
 RESULT_DTYPE = np.dtype([("f", np.uint64, (len(RESULT_FIELDS),)), ("hist_ttft", np.uint32, (NBIN,)),
                          ("hist_norm", np.uint32, (NBIN,))])
-EXPORTS = ["augsched_create", "augsched_enqueue", "augsched_step", "augsched_simulate",
+EXPORTS = ["augsched_create", "augsched_enqueue", "augsched_step", "augsched_step_prefix", "augsched_simulate",
            "augsched_sync", "augsched_launch_count", "augsched_destroy", "augsched_last_error"]
 
 
@@ -78,6 +78,7 @@ def lib():
         L.augsched_create.argtypes = [C.POINTER(Config), vp, u32, u32, C.c_int, vp, C.POINTER(vp)]
         L.augsched_enqueue.argtypes = [vp, u32, C.POINTER(RecordSoA), u32, C.c_int]
         L.augsched_step.argtypes = [vp, u64, C.POINTER(StepOut)]
+        L.augsched_step_prefix.argtypes = [vp, u64, C.POINTER(StepOut)]
         L.augsched_simulate.argtypes = [vp, C.POINTER(Trace), vp, u64, vp, u32]
         L.augsched_sync.argtypes = [vp]
         L.augsched_launch_count.argtypes = [vp]
@@ -85,7 +86,8 @@ def lib():
         L.augsched_destroy.argtypes = [vp]
         L.augsched_destroy.restype = None
         L.augsched_last_error.restype = C.c_char_p
-        for f in (L.augsched_create, L.augsched_enqueue, L.augsched_step, L.augsched_simulate,
+        for f in (L.augsched_create, L.augsched_enqueue, L.augsched_step, L.augsched_step_prefix,
+                  L.augsched_simulate,
                   L.augsched_sync):
             f.restype = C.c_int
         _lib = L
@@ -273,9 +275,12 @@ class Scheduler:
         s = RecordSoA(**{k: v.ctypes.data for k, v in keep.items()})
         _check(self.L.augsched_enqueue(self.h, instance, C.byref(s), n, 0))
 
-    def step(self, now: int) -> StepOut:
+    def step(self, now: int, prefix: bool = False) -> StepOut:
+        """One decision round (augsched_step); prefix=True calls
+        augsched_step_prefix (order/key/grant only for the admitted prefix)."""
         out = StepOut()
-        _check(self.L.augsched_step(self.h, int(now), C.byref(out)))
+        f = self.L.augsched_step_prefix if prefix else self.L.augsched_step
+        _check(f(self.h, int(now), C.byref(out)))
         return out
 
     def step_result(self, out: StepOut) -> dict:

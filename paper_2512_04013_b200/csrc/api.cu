@@ -163,11 +163,14 @@ int augsched_create(const augsched_config* cfg, const augsched_instance_params* 
   int rc = validate_cfg(*cfg);
   if (rc) return rc;
   std::vector<augsched_instance_params> ip(n_instances);
+  uint32_t max_limit = 0;
   for (uint32_t i = 0; i < n_instances; ++i) {
     ip[i] = per_inst ? per_inst[i] : cfg->defaults;
     if ((rc = validate_params(ip[i], i))) return rc;
     const double hi = std::floor(cfg->beta_high * (double)ip[i].target_max);
     if (hi > (double)(1u << 26)) return fail(AUGSCHED_E_INVALID, "instance %u: token limit too large", i);
+    const uint32_t lim = ip[i].budget_mode == AUGSCHED_BUDGET_STATIC ? ip[i].l_static : (uint32_t)hi;
+    max_limit = lim > max_limit ? lim : max_limit;
   }
   int ndev = 0;
   CUDA_TRY(cudaGetDeviceCount(&ndev));
@@ -178,6 +181,7 @@ int augsched_create(const augsched_config* cfg, const augsched_instance_params* 
   h->cfg = *cfg;
   h->n_inst = n_instances;
   h->max_active = max_active_per_instance;
+  h->st.max_limit = max_limit;
   h->device = device;
   h->stream = reinterpret_cast<cudaStream_t>(cuda_stream);
   h->cap = (int64_t)((cfg->g_total - (cfg->g_model + cfg->g_runtime + cfg->g_safety)) /
@@ -318,6 +322,14 @@ int augsched_enqueue(augsched_t* h, uint32_t instance, const augsched_record_soa
   int rc = step_ensure(h->st, h->n_inst, h->max_active, h->stream, h->cfg, h->d_ip, &h->launches);
   if (rc) return rc;
   return step_enqueue(h->st, instance, recs, n, recs_on_device, h->stream, h->d_err, &h->launches);
+}
+
+int augsched_step_prefix(augsched_t* h, uint64_t now_iter, augsched_step_out* out) {
+  if (!h || !out) return fail(AUGSCHED_E_INVALID, "step_prefix: NULL argument");
+  CUDA_TRY(cudaSetDevice(h->device));
+  int rc = step_ensure(h->st, h->n_inst, h->max_active, h->stream, h->cfg, h->d_ip, &h->launches);
+  if (rc) return rc;
+  return step_run_prefix(h->st, h->cfg, h->cap, h->d_ip, h->d_err, now_iter, out, h->stream, &h->launches);
 }
 
 int augsched_step(augsched_t* h, uint64_t now_iter, augsched_step_out* out) {

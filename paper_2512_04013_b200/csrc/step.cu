@@ -18,9 +18,6 @@ constexpr unsigned FULL = 0xffffffffu;
 #ifndef AUGSCHED_SORT_BALLOT
 #define AUGSCHED_SORT_BALLOT 1
 #endif
-#ifndef AUGSCHED_KEYS_MATCH
-#define AUGSCHED_KEYS_MATCH 0
-#endif
 constexpr int KNT = 256;                      // keys kernel threads
 constexpr int SNT = AUGSCHED_SORT_NT;         // sort-pass threads
 constexpr int SITEMS = AUGSCHED_SORT_ITEMS;   // items per thread per sort tile
@@ -165,6 +162,7 @@ struct KeyArgs {
   int npass;
   PassDesc passes[STEP_MAX_PASS];
   uint32_t N;
+  uint32_t* pf_cnt;   // prefix step: [|A|, |C|, b*, below, blocks done]; nullptr otherwise
 };
 
 // Packed sort word of one slot: tier:2 | key:32 | slot:30 (tier 3 = not queued).
@@ -184,15 +182,32 @@ __device__ __forceinline__ uint32_t digit_of(unsigned long long x, const PassDes
 // pass (warp-aggregated shared atomics).
 constexpr int KCNT = 1024;   // per-block instance-count table of the keys kernel
 
+constexpr int KU = 4;   // slots in flight per thread in the keys kernel
+
+// Shared histogram increment for bins that are heavily shared within a warp
+// (the top digits of similar scores): the lanes holding lane 0's bin add with
+// one atomic, the others individually.  All 32 lanes must call it; d < 0
+// means no item.
+__device__ __forceinline__ void hist_add(uint32_t* h, int d) {
+  const int lane = threadIdx.x & 31;
+  const int d0 = __shfl_sync(FULL, d, 0);
+  const unsigned same = __ballot_sync(FULL, d == d0 && d >= 0);
+  if (lane == 0 && same) atomicAdd(&h[d0], (unsigned)__popc(same));
+  if (d >= 0 && !((same >> lane) & 1u)) atomicAdd(&h[d], 1u);
+}
+
 __global__ void __launch_bounds__(KNT) keys_kernel(KeyArgs a) {
   __shared__ uint32_t h[STEP_HIST_WORDS];
   __shared__ uint32_t qcnt[KCNT];
-  const int tid = threadIdx.x, lane = tid & 31;
+  __shared__ uint32_t wsum[KNT / 32];
+  __shared__ uint32_t ticket;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int hw = a.passes[a.npass - 1].hoff + (1 << a.passes[a.npass - 1].bits);
   for (int b = tid; b < hw; b += KNT) h[b] = 0;
   for (int b = tid; b < KCNT; b += KNT) qcnt[b] = 0;
   __syncthreads();
   const uint32_t MA = a.S.MA;
+  const bool single = MA == a.N;
   // contiguous chunk per block: the instances it touches are contiguous, so
   // their queue counts aggregate in shared memory (one global atomic per
   // block and instance instead of one per warp)
@@ -201,42 +216,85 @@ __global__ void __launch_bounds__(KNT) keys_kernel(KeyArgs a) {
   const uint32_t c1 = c0 + chunk < a.N ? c0 + chunk : a.N;
   const uint32_t i0 = c0 / MA;
   const bool local_cnt = c1 > c0 && (c1 - 1) / MA - i0 < (uint32_t)KCNT;
-  for (uint32_t base = c0; base < c1; base += KNT) {   // block-uniform trip count
-    const uint32_t s = base + tid;
-    const bool valid = s < c1;
-    uint32_t inst = 0, tier = 3, key = 0;
-    if (valid) {
-      inst = MA == a.N ? 0u : s / MA;
-      const uint32_t stv = a.S.st[s] & 15;
-      tier = (stv >= ST_RUN && stv <= ST_WAIT) ? stv - ST_RUN : 3u;
-      if (tier < 3)
-        key = rank_key(a.S.coef[inst], a.S.ip[inst], a.S.V[s], a.now, a.S.last[s], s - inst * MA);
-      if (s == inst * MA)
-        a.budget[inst] = token_limit(a.cfg, a.S.coef[inst], a.S.ip[inst], a.cap,
-                                     ld_ll(&a.S.A[inst]), ld_ll(&a.S.P[inst]));
-    }
-    const unsigned long long x = ((unsigned long long)tier << PK_TIER) |
-                                 ((unsigned long long)key << PK_KEY) | s;
-    if (valid) a.k0[s] = x;
-    // queued count per instance (warp-aggregated)
-    const bool q = valid && tier < 3;
-    const unsigned qm = __ballot_sync(FULL, q);
-    if (qm) {
-      const unsigned peers = __match_any_sync(FULL, q ? (int)inst : -1) & qm;
-      if (q && lane == __ffs(peers) - 1) {
-        if (local_cnt) atomicAdd(&qcnt[inst - i0], (unsigned)__popc(peers));
-        else atomicAdd(&a.n_active[inst], (unsigned)__popc(peers));
+  uint32_t myq = 0;   // queued slots seen by this thread (single-instance handles)
+  if (single) {
+    // one instance: its constants in registers, the three scoring words of
+    // KU slots loaded together
+    const Coef k = a.S.coef[0];
+    const augsched_instance_params ip = a.S.ip[0];
+    if (c0 == 0 && c1 > 0)
+      a.budget[0] = token_limit(a.cfg, k, ip, a.cap, ld_ll(&a.S.A[0]), ld_ll(&a.S.P[0]));
+    for (uint32_t base = c0; base < c1; base += KNT * KU) {
+      uint32_t stv[KU], lst[KU];
+      double V[KU];
+#pragma unroll
+      for (int u = 0; u < KU; ++u) {
+        const uint32_t s = base + u * KNT + tid;
+        stv[u] = 0u; lst[u] = 0u; V[u] = 0.0;
+        if (s < c1) { stv[u] = a.S.st[s] & 15; V[u] = a.S.V[s]; lst[u] = a.S.last[s]; }
+      }
+#pragma unroll
+      for (int u = 0; u < KU; ++u) {
+        const uint32_t s = base + u * KNT + tid;
+        const uint32_t tier = (stv[u] >= ST_RUN && stv[u] <= ST_WAIT) ? stv[u] - ST_RUN : 3u;
+        const uint32_t key = tier < 3 ? rank_key(k, ip, V[u], a.now, lst[u], s) : 0u;
+        const unsigned long long x = ((unsigned long long)tier << PK_TIER) |
+                                     ((unsigned long long)key << PK_KEY) | s;
+        if (s < c1) {
+          a.k0[s] = x;
+          myq += tier < 3;
+        }
+        for (int p = 0; p < a.npass; ++p)
+          hist_add(h + a.passes[p].hoff, s < c1 ? (int)digit_of(x, a.passes[p], MA) : -1);
       }
     }
-    for (int p = 0; p < a.npass; ++p) {
-      const int d = valid ? (int)digit_of(x, a.passes[p], MA) : -1;
-#if AUGSCHED_KEYS_MATCH
-      const unsigned pe = __match_any_sync(FULL, d);
-      if (d >= 0 && lane == __ffs(pe) - 1) atomicAdd(&h[a.passes[p].hoff + d], (unsigned)__popc(pe));
-#else
-      if (d >= 0) atomicAdd(&h[a.passes[p].hoff + d], 1u);
-#endif
+  } else
+  for (uint32_t base = c0; base < c1; base += KNT * KU) {   // block-uniform trip count
+    uint32_t stv[KU];
+#pragma unroll
+    for (int u = 0; u < KU; ++u) {
+      const uint32_t s = base + u * KNT + tid;
+      stv[u] = s < c1 ? a.S.st[s] & 15 : 0u;
     }
+#pragma unroll
+    for (int u = 0; u < KU; ++u) {
+      const uint32_t s = base + u * KNT + tid;
+      const bool valid = s < c1;
+      uint32_t inst = 0, key = 0;
+      const uint32_t tier = (stv[u] >= ST_RUN && stv[u] <= ST_WAIT) ? stv[u] - ST_RUN : 3u;
+      if (valid) {
+        inst = s / MA;
+        if (tier < 3)
+          key = rank_key(a.S.coef[inst], a.S.ip[inst], a.S.V[s], a.now, a.S.last[s], s - inst * MA);
+        if (s == inst * MA)
+          a.budget[inst] = token_limit(a.cfg, a.S.coef[inst], a.S.ip[inst], a.cap,
+                                       ld_ll(&a.S.A[inst]), ld_ll(&a.S.P[inst]));
+      }
+      const unsigned long long x = ((unsigned long long)tier << PK_TIER) |
+                                   ((unsigned long long)key << PK_KEY) | s;
+      if (valid) a.k0[s] = x;
+      // queued count per instance
+      const bool q = valid && tier < 3;
+      {
+        const unsigned qm = __ballot_sync(FULL, q);
+        if (qm) {
+          const unsigned peers = __match_any_sync(FULL, q ? (int)inst : -1) & qm;
+          if (q && lane == __ffs(peers) - 1) {
+            if (local_cnt) atomicAdd(&qcnt[inst - i0], (unsigned)__popc(peers));
+            else atomicAdd(&a.n_active[inst], (unsigned)__popc(peers));
+          }
+        }
+      }
+      for (int p = 0; p < a.npass; ++p) {
+        const int d = valid ? (int)digit_of(x, a.passes[p], MA) : -1;
+        hist_add(h + a.passes[p].hoff, d);
+      }
+    }
+  }
+  if (single) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) myq += __shfl_xor_sync(FULL, myq, o);
+    if (lane == 0) atomicAdd(&qcnt[0], myq);
   }
   __syncthreads();
   for (int b = tid; b < hw; b += KNT)
@@ -244,6 +302,38 @@ __global__ void __launch_bounds__(KNT) keys_kernel(KeyArgs a) {
   if (local_cnt)
     for (uint32_t b = tid; b <= (c1 - 1) / MA - i0; b += KNT)
       if (qcnt[b]) atomicAdd(&a.n_active[i0 + b], qcnt[b]);
+  if (!a.pf_cnt) return;
+  // prefix step: the last block locates the bucket b* of the top digit that
+  // holds the target-th smallest entry (target = min(B, queued))
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) ticket = atomicAdd(&a.pf_cnt[4], 1u);
+  __syncthreads();
+  if (ticket != gridDim.x - 1) return;
+  __threadfence();
+  constexpr int NB = 1 << PF_BITS, PER = NB / KNT;
+  const long long B = ld_ll(a.budget);
+  const uint32_t nq = __ldcg(&a.n_active[0]);
+  const uint32_t target = B <= 0 ? 0u : ((unsigned long long)B < nq ? (uint32_t)B : nq);
+  uint32_t loc[PER], sum = 0;
+#pragma unroll
+  for (int j = 0; j < PER; ++j) { loc[j] = __ldcg(&a.ghist[tid * PER + j]); sum += loc[j]; }
+  uint32_t inc = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(FULL, inc, o);
+    if (lane >= o) inc += y;
+  }
+  if (lane == 31) wsum[warp] = inc;
+  if (tid == 0) { a.pf_cnt[2] = NB; a.pf_cnt[3] = 0; }
+  __syncthreads();
+  uint32_t run = inc - sum;
+  for (int w = 0; w < warp; ++w) run += wsum[w];
+#pragma unroll
+  for (int j = 0; j < PER; ++j) {
+    if (target > 0 && run < target && run + loc[j] >= target) { a.pf_cnt[2] = tid * PER + j; a.pf_cnt[3] = run; }
+    run += loc[j];
+  }
 }
 
 // ------------------------------------------------------------------ sort pass
@@ -584,6 +674,293 @@ __global__ void __launch_bounds__(ANT) admit_kernel(Slots S, augsched_config cfg
   }
 }
 
+
+// ====================================================================== prefix step
+// augsched_step_prefix: the same decision round, producing the order only
+// for the admitted prefix.  Every queued request has demand >= 1, so the
+// admitted prefix lies within the first min(B, n) entries of the order; it
+// is found by a count-based selection instead of a full sort:
+//   keys_kernel   packed words + histogram of the top 12-bit digit
+//   pf_collect    every block locates the bucket b* holding the target-th
+//                 entry; words below b* -> A (< target of them), in b* -> C
+//   pf_admit      one block: the (target - |A|) smallest of C by a weighted
+//                 radix select (weights 1), bitonic sort of the prefix in
+//                 shared memory, admission (R17), resolution (R20, exact:
+//                 selections over all slots), grant accounting.
+
+__device__ __forceinline__ uint32_t pf_target(long long B, uint32_t n) {
+  if (B <= 0) return 0u;
+  return (unsigned long long)B < n ? (uint32_t)B : n;
+}
+
+__global__ void __launch_bounds__(KNT) pf_collect_kernel(const unsigned long long* k0, uint32_t N,
+                                                         uint32_t* cnt, unsigned long long* A,
+                                                         unsigned long long* C) {
+  const int tid = threadIdx.x, lane = tid & 31;
+  constexpr int NB = 1 << PF_BITS;
+  const uint32_t bstar = cnt[2];   // written by the last keys_kernel block
+  if (bstar >= NB) return;         // nothing to admit
+  const unsigned lt = (1u << lane) - 1;
+  for (uint32_t base = blockIdx.x * KNT * KU; base < N; base += gridDim.x * KNT * KU) {
+    unsigned long long x[KU];
+#pragma unroll
+    for (int u = 0; u < KU; ++u) {
+      const uint32_t s = base + u * KNT + tid;
+      x[u] = s < N ? k0[s] : ~0ull;
+    }
+#pragma unroll
+    for (int u = 0; u < KU; ++u) {
+      const uint32_t d = (uint32_t)(x[u] >> (64 - PF_BITS));
+      const bool queued = (x[u] >> PK_TIER) < 3;
+      const bool inA = queued && d < bstar, inC = queued && d == bstar;
+      const unsigned ma = __ballot_sync(FULL, inA), mc = __ballot_sync(FULL, inC);
+      if (!(ma | mc)) continue;
+      uint32_t ba = 0, bc = 0;
+      if (lane == 0) {
+        if (ma) ba = atomicAdd(&cnt[0], (unsigned)__popc(ma));
+        if (mc) bc = atomicAdd(&cnt[1], (unsigned)__popc(mc));
+      }
+      ba = __shfl_sync(FULL, ba, 0);
+      bc = __shfl_sync(FULL, bc, 0);
+      if (inA) A[ba + __popc(ma & lt)] = x[u];
+      if (inC) C[bc + __popc(mc & lt)] = x[u];
+    }
+  }
+}
+
+constexpr int PNT = 1024;
+
+__global__ void __launch_bounds__(PNT) pf_admit_kernel(Slots S, augsched_config cfg, int64_t cap, uint64_t now,
+                                                       const long long* budget, const uint32_t* n_active,
+                                                       const unsigned long long* k0,
+                                                       const unsigned long long* A,
+                                                       const unsigned long long* C, const uint32_t* cnt,
+                                                       uint32_t* order, uint32_t* keyout, uint32_t* grant,
+                                                       uint32_t* admitted, uint32_t* gslot) {
+  extern __shared__ __align__(16) unsigned long long pf_sm[];
+  unsigned long long* sbuf = pf_sm;              // [2 * PF_SCAP] the prefix + exchange buffer
+  __shared__ SelShm sel;
+  __shared__ unsigned long long wsum[PNT / 32];
+  __shared__ unsigned long long freed;
+  __shared__ uint32_t m_s;
+  const int tid = threadIdx.x;
+  const uint32_t MA = S.MA;
+  const long long B = budget[0];
+  const uint32_t target = pf_target(B, n_active[0]);
+  const uint32_t nA = cnt[0], nC = cnt[1];
+  // ---- the first `target` entries of the order: A, plus the smallest of C
+  for (uint32_t i = tid; i < nA; i += PNT) sbuf[i] = A[i];
+  if (tid == 0) m_s = nA;
+  const uint32_t needC = target > nA ? target - nA : 0u;
+  if (needC > 0 && nA + nC <= PF_SCAP) {
+    // the whole crossing bucket fits beside A: sort them all, keep `target`
+    for (uint32_t i = tid; i < nC; i += PNT) sbuf[nA + i] = C[i];
+    if (tid == 0) m_s = nA + nC;
+  } else if (needC > 0) {
+    // large crossing bucket: select its (target - |A|) smallest in place
+    const unsigned long long* cb = C;
+    __syncthreads();
+    wselect<PNT>(sel, nC, needC, 64, [&](uint32_t i, uint64_t& key, uint32_t& w) {
+      key = cb[i]; w = 1u; return true; });
+    const unsigned long long tau = sel.r.found ? sel.r.k : ~0ull;
+    for (uint32_t i = tid; i < nC; i += PNT) {
+      const unsigned long long x = cb[i];
+      if (x <= tau) sbuf[atomicAdd(&m_s, 1u)] = x;
+    }
+  }
+  __syncthreads();
+  const uint32_t mt = m_s;  // >= target entries, the first `target` of the order among them
+  // ---- bitonic sort of the prefix (padded to a power of two).  Each thread
+  // holds E = P2 / PNT elements (index tid + e * PNT) in registers: partner
+  // distances j < 32 exchange by warp shuffles, j >= PNT inside the thread,
+  // and only 32 <= j < PNT goes through shared memory (double-buffered, one
+  // barrier per stage).
+  uint32_t P2 = 1;
+  while (P2 < mt) P2 <<= 1;
+  if (P2 < 32) P2 = 32;
+  constexpr int EMAX = PF_SCAP / PNT;
+  const uint32_t E = P2 > PNT ? P2 / PNT : 1u;
+  unsigned long long v[EMAX];
+#pragma unroll
+  for (int e = 0; e < EMAX; ++e) {
+    const uint32_t idx = tid + e * PNT;
+    v[e] = (e < (int)E && idx < mt) ? sbuf[idx] : ~0ull;
+  }
+  __syncthreads();
+  int xp = 0;
+  for (uint32_t k = 2; k <= P2; k <<= 1) {
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      if (j < 32) {
+#pragma unroll
+        for (int e = 0; e < EMAX; ++e) {
+          if (e >= (int)E) break;
+          const unsigned long long pv = __shfl_xor_sync(FULL, v[e], j);
+          const uint32_t idx = tid + e * PNT;
+          const bool keep_min = ((idx & j) == 0) == ((idx & k) == 0);
+          v[e] = keep_min ? (pv < v[e] ? pv : v[e]) : (pv > v[e] ? pv : v[e]);
+        }
+      } else if (j < PNT) {
+        unsigned long long* xbuf = xp ? sbuf + PF_SCAP : sbuf;
+        xp ^= 1;
+#pragma unroll
+        for (int e = 0; e < EMAX; ++e)
+          if (e < (int)E) xbuf[tid + e * PNT] = v[e];
+        __syncthreads();
+#pragma unroll
+        for (int e = 0; e < EMAX; ++e) {
+          if (e >= (int)E) break;
+          const uint32_t idx = tid + e * PNT;
+          if (idx >= P2) continue;
+          const unsigned long long pv = xbuf[idx ^ j];
+          const bool keep_min = ((idx & j) == 0) == ((idx & k) == 0);
+          v[e] = keep_min ? (pv < v[e] ? pv : v[e]) : (pv > v[e] ? pv : v[e]);
+        }
+      } else {
+        // partner inside the thread: e ^ (j / PNT), unrolled so v stays in registers
+#pragma unroll
+        for (int bsh = 0; (1 << bsh) < EMAX; ++bsh) {
+          if (j != ((uint32_t)PNT << bsh)) continue;
+#pragma unroll
+          for (int e = 0; e < EMAX; ++e) {
+            const int e2 = e ^ (1 << bsh);
+            if (e2 <= e || e2 >= (int)E) continue;
+            const uint32_t idx = tid + e * PNT;
+            const bool up = (idx & k) == 0;
+            const unsigned long long x0 = v[e], x1 = v[e2];
+            if ((x0 > x1) == up) { v[e] = x1; v[e2] = x0; }
+          }
+        }
+      }
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int e = 0; e < EMAX; ++e) {
+    const uint32_t idx = tid + e * PNT;
+    if (e < (int)E && idx < P2) sbuf[idx] = v[e];
+  }
+  __syncthreads();
+  const uint32_t m = target;
+  // ---- a6 admission over the prefix (P_{j-1} < B, partial last, R17)
+  unsigned long long Prun = 0, gsum = 0;
+  uint32_t adm = 0;
+  for (uint32_t j0 = 0; j0 < m && (long long)Prun < B; j0 += PNT) {
+    const uint32_t j = j0 + tid;
+    unsigned long long d = 0;
+    uint32_t slot = 0;
+    if (j < m) {
+      slot = (uint32_t)sbuf[j] & SLOT_MASK;
+      d = slot_demand(S, slot, cfg.s_in);
+    }
+    unsigned long long tot;
+    const unsigned long long inc = block_incl_scan_u64<PNT>(d, wsum, &tot);
+    const unsigned long long ex = Prun + inc - d;
+    const bool in = j < m && (long long)ex < B;
+    if (in) {
+      const unsigned long long g = d < (unsigned long long)B - ex ? d : (unsigned long long)B - ex;
+      order[j] = slot;
+      keyout[j] = (uint32_t)(sbuf[j] >> PK_KEY);
+      grant[j] = (uint32_t)g;
+      gslot[slot] = (uint32_t)g;
+      gsum += g;
+    }
+    adm += __syncthreads_count(in);
+    Prun += tot;
+  }
+  unsigned long long need;
+  block_incl_scan_u64<PNT>(gsum, wsum, &need);
+  long long fr = cap - ld_ll(&S.A[0]) - ld_ll(&S.P[0]);
+  // ---- a7 resolution (rare; exact selections over every slot)
+  if ((long long)need > fr) {
+    if (tid == 0) freed = 0;
+    auto getp = [&](uint32_t x, uint64_t& key, uint32_t& w) {
+      const uint32_t stv = S.st[x];
+      const int32_t kv = S.kv[x];
+      if ((stv & 15) != ST_PAUSED || ((stv >> 4) & 3) != POL_P || kv <= 0) return false;
+      key = ((uint64_t)(0xFFFFFFFFu - (uint32_t)kv) << 24) | x;
+      w = (uint32_t)kv;
+      return true;
+    };
+    wselect<PNT>(sel, MA, (uint64_t)((long long)need - fr), 56, getp);
+    {
+      const bool f0 = sel.r.found != 0;
+      const uint64_t kd = sel.r.k;
+      for (uint32_t x = tid; x < MA; x += PNT) {
+        uint64_t key;
+        uint32_t w;
+        if (getp(x, key, w) && (!f0 || key <= kd)) {
+          atomicAdd(&freed, (unsigned long long)w);
+          S.kv[x] = 0;
+          S.st[x] = ST_PAUSED | ((uint32_t)POL_D << 4);
+        }
+      }
+    }
+    __syncthreads();
+    if (tid == 0) ledger_add(&S.P[0], -(long long)freed);
+    fr += (long long)freed;
+    if ((long long)need > fr) {
+      // from the tail of the order over queued entries with kv + g > 0
+      auto gete = [&](uint32_t x, uint64_t& key, uint32_t& w) {
+        const unsigned long long kx = k0[x];
+        if ((kx >> PK_TIER) >= 3) return false;
+        const uint32_t g = gslot[x];
+        w = (uint32_t)S.kv[x] + (g == 0xFFFFFFFFu ? 0u : g);
+        key = ~kx;
+        return w > 0;
+      };
+      wselect<PNT>(sel, MA, (uint64_t)((long long)need - fr), 64, gete);
+      const bool f1 = sel.r.found != 0;
+      const uint64_t k1 = sel.r.k;
+      __syncthreads();
+      long long dA = 0;
+      for (uint32_t x = tid; x < MA; x += PNT) {
+        uint64_t key;
+        uint32_t w;
+        if (gete(x, key, w) && (!f1 || key <= k1)) {
+          dA -= S.kv[x];
+          S.kv[x] = 0;
+          S.cpu[x] = 0;
+          S.st[x] = ST_WAIT | (S.st[x] & 0x30u);
+          if (gslot[x]) gslot[x] = 0xFFFFFFFFu;   // grant cancelled
+        }
+      }
+      if (dA) ledger_add(&S.A[0], dA);
+      __syncthreads();
+      for (uint32_t j = tid; j < adm; j += PNT)
+        if (gslot[order[j]] == 0xFFFFFFFFu) grant[j] = 0;
+    }
+  }
+  __syncthreads();
+  // ---- S9 + token accounting of the granted batch
+  unsigned long long dA = 0;
+  for (uint32_t j = tid; j < adm; j += PNT) {
+    const uint32_t g_slot = order[j];
+    gslot[g_slot] = 0;
+    const uint32_t gr = grant[j];
+    if (gr == 0) continue;
+    int32_t ctx = S.ctx[g_slot], kv = S.kv[g_slot], cpu = S.cpu[g_slot], pend = S.pend[g_slot];
+    if (cpu > 0) { cpu -= (int32_t)gr; kv += (int32_t)gr; }
+    else if ((ctx - kv) + pend > 0) {
+      const int32_t rc = (int32_t)gr < ctx - kv ? (int32_t)gr : ctx - kv;
+      kv += rc;
+      const int32_t pp = (int32_t)gr - rc;
+      pend -= pp; ctx += pp; kv += pp;
+    } else { ctx += 1; kv += 1; }
+    dA += gr;
+    S.ctx[g_slot] = ctx; S.kv[g_slot] = kv; S.cpu[g_slot] = cpu; S.pend[g_slot] = pend;
+    S.last[g_slot] = (uint32_t)now;
+    S.st[g_slot] = ST_RUN | (S.st[g_slot] & 0x30u);
+  }
+  unsigned long long tot;
+  block_incl_scan_u64<PNT>(dA, wsum, &tot);
+  if (tid == 0) {
+    admitted[0] = adm;
+    const long long a = ld_ll(&S.A[0]) + (long long)tot;
+    S.A[0] = a;
+    S.Aevt[0] = a;
+  }
+}
+
 }  // namespace
 
 // ====================================================================== host
@@ -673,7 +1050,7 @@ int step_ensure(StepState& st, uint32_t n_inst, uint32_t max_active, cudaStream_
   add(0, PK_KEY + 24, 10);
   for (uint32_t x = n_inst - 1, b = 0; x > 0; x >>= 8, ++b) add(2, (int)(8 * b), 8);
   if (hoff > STEP_HIST_WORDS) return set_error(AUGSCHED_E_CAPACITY, "step: too many sort passes");
-  const size_t zwords = (size_t)n_inst + STEP_HIST_WORDS + STEP_MAX_PASS;
+  const size_t zwords = (size_t)n_inst + STEP_HIST_WORDS + STEP_MAX_PASS + 8;
   int rc;
   if ((rc = salloc(st, &st.st, N)) || (rc = salloc(st, &st.V, N)) || (rc = salloc(st, &st.last, N)) ||
       (rc = salloc(st, &st.ctx, N)) || (rc = salloc(st, &st.kv, N)) || (rc = salloc(st, &st.cpu, N)) ||
@@ -686,13 +1063,17 @@ int step_ensure(StepState& st, uint32_t n_inst, uint32_t max_active, cudaStream_
       (rc = salloc(st, &st.grant, N)) || (rc = salloc(st, &st.key, N)) ||
       (rc = salloc(st, &st.k0, N)) || (rc = salloc(st, &st.k1, N)) ||
       (rc = salloc(st, &st.lb_status, (size_t)st.n_tiles << STEP_RB_MAX)) ||
-      (rc = salloc(st, &st.lb_gstatus, (size_t)st.n_tiles << STEP_RB_MAX)))
+      (rc = salloc(st, &st.lb_gstatus, (size_t)st.n_tiles << STEP_RB_MAX)) ||
+      (rc = salloc(st, &st.pf_A, PF_SCAP)) || (rc = salloc(st, &st.pf_C, N)) ||
+      (rc = salloc(st, &st.gslot, N)))
     return rc;
   // one memset per step clears the queue counts, histograms and tile counters
   st.zwords = zwords;
   st.n_active = st.zbuf;
   st.ghist = st.zbuf + n_inst;
   st.tile_ctr = st.ghist + STEP_HIST_WORDS;
+  st.pf_cnt = st.tile_ctr + STEP_MAX_PASS;
+  cudaMemsetAsync(st.gslot, 0, sizeof(uint32_t) * N, s);
   cudaMemsetAsync(st.st, 0, sizeof(uint32_t) * N, s);
   cudaMemsetAsync(st.ctx, 0, sizeof(int32_t) * N, s);
   cudaMemsetAsync(st.kv, 0, sizeof(int32_t) * N, s);
@@ -710,6 +1091,8 @@ int step_ensure(StepState& st, uint32_t n_inst, uint32_t max_active, cudaStream_
   int dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&st.sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaFuncSetAttribute(pf_admit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)(sizeof(unsigned long long) * 2 * PF_SCAP));
   st.epoch = 0;
   st.ready = true;
   return cuda_check(cudaGetLastError(), "step_ensure");
@@ -753,30 +1136,73 @@ int step_enqueue(StepState& st, uint32_t inst, const augsched_record_soa* r, uin
   return cuda_check(cudaGetLastError(), "enqueue");
 }
 
+namespace {
+// Engine events of the last forward, snapshot, returns / arrivals / imports.
+void run_records(StepState& st, const Slots& S, uint32_t* d_err, uint64_t now, cudaStream_t s,
+                 uint64_t* launches) {
+  if (!st.r_n) return;
+  const uint32_t ni = st.n_inst;
+  Rec r{st.r_kind, st.r_id, st.r_la, st.r_lb, st.r_lc, st.r_flags, st.r_last, st.r_ctx, st.r_kv,
+        st.r_cpu, st.r_pend, st.r_ta};
+  const uint32_t g = (st.r_n + 255) / 256;
+  rec_phaseA<<<g, 256, 0, s>>>(r, st.r_n, S, d_err);
+  snap_kernel<<<(ni + 255) / 256, 256, 0, s>>>(st.A, st.Asnap, ni);
+  rec_phaseBC<<<g, 256, 0, s>>>(r, st.r_n, S, now, d_err);
+  *launches += 3;
+  st.r_n = 0;
+}
+
+}  // namespace
+
+static size_t pf_smem_bytes() { return sizeof(unsigned long long) * 2 * PF_SCAP; }
+
+int step_run_prefix(StepState& st, const augsched_config& cfg, int64_t cap,
+                    const augsched_instance_params* d_ip, uint32_t* d_err, uint64_t now,
+                    augsched_step_out* out, cudaStream_t s, uint64_t* launches) {
+  // the prefix selection is single-instance and bounded by PF_SCAP
+  if (st.n_inst != 1 || st.max_limit > PF_SCAP)
+    return step_run(st, cfg, cap, d_ip, d_err, now, out, s, launches);
+  Slots S = slots_of(st, d_ip);
+  run_records(st, S, d_err, now, s, launches);
+  cudaMemsetAsync(st.zbuf, 0, sizeof(uint32_t) * st.zwords, s);
+  KeyArgs ka;
+  ka.S = S; ka.cfg = cfg; ka.cap = cap; ka.now = now; ka.k0 = st.k0;
+  ka.ghist = st.ghist; ka.n_active = st.n_active; ka.budget = st.budget; ka.npass = 1;
+  ka.passes[0] = PassDesc{0, 64 - PF_BITS, PF_BITS, 0};
+  ka.N = (uint32_t)st.N;
+  ka.pf_cnt = st.pf_cnt;
+  const size_t kblocks = (st.N + KNT * KU - 1) / (KNT * KU);
+  const int kgrid = (int)(kblocks < (size_t)st.sms * 4 ? kblocks : (size_t)st.sms * 4);
+  keys_kernel<<<kgrid, KNT, 0, s>>>(ka);
+  pf_collect_kernel<<<kgrid, KNT, 0, s>>>(st.k0, (uint32_t)st.N, st.pf_cnt, st.pf_A, st.pf_C);
+  pf_admit_kernel<<<1, PNT, pf_smem_bytes(), s>>>(S, cfg, cap, now, st.budget, st.n_active, st.k0, st.pf_A,
+                                                  st.pf_C, st.pf_cnt, st.order, st.key, st.grant,
+                                                  st.admitted, st.gslot);
+  *launches += 3;
+  out->budget = reinterpret_cast<const int64_t*>(st.budget);
+  out->n_active = st.n_active;
+  out->admitted = st.admitted;
+  out->order = st.order;
+  out->grant = st.grant;
+  out->key = st.key;
+  return cuda_check(cudaGetLastError(), "step_prefix");
+}
+
 int step_run(StepState& st, const augsched_config& cfg, int64_t cap,
              const augsched_instance_params* d_ip, uint32_t* d_err, uint64_t now,
              augsched_step_out* out, cudaStream_t s, uint64_t* launches) {
   Slots S = slots_of(st, d_ip);
   const uint32_t ni = st.n_inst;
-  if (st.r_n) {
-    Rec r{st.r_kind, st.r_id, st.r_la, st.r_lb, st.r_lc, st.r_flags, st.r_last, st.r_ctx, st.r_kv,
-          st.r_cpu, st.r_pend, st.r_ta};
-    const uint32_t g = (st.r_n + 255) / 256;
-    rec_phaseA<<<g, 256, 0, s>>>(r, st.r_n, S, d_err);
-    snap_kernel<<<(ni + 255) / 256, 256, 0, s>>>(st.A, st.Asnap, ni);
-    rec_phaseBC<<<g, 256, 0, s>>>(r, st.r_n, S, now, d_err);
-    *launches += 3;
-    st.r_n = 0;
-  }
+  run_records(st, S, d_err, now, s, launches);
   cudaMemsetAsync(st.zbuf, 0, sizeof(uint32_t) * st.zwords, s);
   KeyArgs ka;
   ka.S = S; ka.cfg = cfg; ka.cap = cap; ka.now = now; ka.k0 = st.k0;
   ka.ghist = st.ghist; ka.n_active = st.n_active; ka.budget = st.budget; ka.npass = st.npass;
   for (int p = 0; p < st.npass; ++p) ka.passes[p] = st.passes[p];
   ka.N = (uint32_t)st.N;
-  const size_t kblocks = (st.N + KNT - 1) / KNT;
-  // few fat blocks: each zeroes and flushes ~2K histogram bins once
-  const int kgrid = (int)(kblocks < (size_t)st.sms * 2 ? kblocks : (size_t)st.sms * 2);
+  ka.pf_cnt = nullptr;
+  const size_t kblocks = (st.N + KNT * KU - 1) / (KNT * KU);
+  const int kgrid = (int)(kblocks < (size_t)st.sms * 8 ? kblocks : (size_t)st.sms * 8);
   keys_kernel<<<kgrid, KNT, 0, s>>>(ka);
   *launches += 1;
   unsigned long long *kin = st.k0, *kout = st.k1;

@@ -22,7 +22,10 @@ namespace augsched {
 
 constexpr int STEP_MAX_PASS = 8;
 constexpr int STEP_RB_MAX = 10;                 // widest digit (bins = 1 << bits)
-constexpr int STEP_HIST_WORDS = 4 * 256 + 1024 + 3 * 256;  // bins over all passes (<= 8)
+constexpr int STEP_HIST_WORDS = 4096;          // bins over all passes (<= 8), or the prefix digit
+constexpr int PF_BITS = 12;                     // prefix step: top digit (tier:2 + key top 10 bits)
+constexpr uint32_t PF_SCAP = 8192;              // prefix step: admitted-prefix capacity (max limit)
+constexpr uint32_t PF_CCAP = 16384;             // prefix step: crossing-bucket entries kept on chip
 
 struct PassDesc {
   int src;    // 0: `bits` bits of the packed key at `shift`; 2: byte of the instance index
@@ -63,7 +66,11 @@ struct StepState {
   int npass = 0;
   PassDesc passes[STEP_MAX_PASS];
   uint32_t n_tiles = 0;
-  uint32_t* zbuf = nullptr;       // [n_inst | STEP_HIST_WORDS | STEP_MAX_PASS], zeroed every step
+  uint32_t* zbuf = nullptr;       // [n_inst | STEP_HIST_WORDS | STEP_MAX_PASS | 4], zeroed every step
+  uint32_t* pf_cnt = nullptr;     // prefix step: [|A|, |C|]
+  unsigned long long *pf_A = nullptr, *pf_C = nullptr;   // prefix step candidates (packed words)
+  uint32_t* gslot = nullptr;      // prefix step: grant by slot during resolution (kept zero)
+  uint32_t max_limit = 0;         // largest token limit any instance can get
   size_t zwords = 0;
   int sms = 148;
   void* alloc_list[64];
@@ -74,6 +81,9 @@ int step_ensure(StepState& st, uint32_t n_inst, uint32_t max_active, cudaStream_
                 const augsched_config& cfg, const augsched_instance_params* d_ip, uint64_t* launches);
 int step_enqueue(StepState& st, uint32_t inst, const augsched_record_soa* r, uint32_t n, int on_dev,
                  cudaStream_t s, uint32_t* d_err, uint64_t* launches);
+int step_run_prefix(StepState& st, const augsched_config& cfg, int64_t cap,
+                    const augsched_instance_params* d_ip, uint32_t* d_err, uint64_t now,
+                    augsched_step_out* out, cudaStream_t s, uint64_t* launches);
 int step_run(StepState& st, const augsched_config& cfg, int64_t cap,
              const augsched_instance_params* d_ip, uint32_t* d_err, uint64_t now,
              augsched_step_out* out, cudaStream_t s, uint64_t* launches);

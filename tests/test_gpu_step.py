@@ -16,16 +16,21 @@ if not torch.cuda.is_available():
 import paper_2512_04013_b200 as aug  # noqa: E402
 
 
-def compare(g, o, n_inst, label):
+def compare(g, o, n_inst, label, prefix=False):
+    """Step outputs equal the oracle's: limits, queue sizes, admitted counts,
+    and the order / keys / grants (the admitted prefix only when prefix)."""
     assert np.array_equal(g["B"], o["B"]), f"{label}: budget {g['B'][:4]} vs {o['B'][:4]}"
     assert np.array_equal(g["n_active"], o["n_active"]), f"{label}: n_active"
     assert np.array_equal(g["admitted"], o["admitted"]), f"{label}: admitted {g['admitted']} vs {o['admitted']}"
     for i in range(n_inst):
         n, a = int(o["n_active"][i]), int(o["admitted"][i])
+        if prefix:
+            n = a
         assert np.array_equal(g["order"][i, :n], o["order"][i, :n]), f"{label}: order inst {i}"
         assert np.array_equal(g["keys"][i, :n], o["keys"][i, :n]), f"{label}: keys inst {i}"
         assert np.array_equal(g["grant"][i, :a], o["grant"][i, :a]), f"{label}: grant inst {i}"
-        assert not o["grant"][i, a:n].any()
+        if not prefix:
+            assert not o["grant"][i, a:n].any()
 
 
 def test_G3_gpu():
@@ -126,4 +131,49 @@ def test_cfg4_one_million_queue():
         g = s.step_result(s.step(t0 + k))
         compare(g, o, 1, f"cfg4 step {k}")
         assert int(g["B"][0]) == 750 and int(g["n_active"][0]) == n - 16
+    s.close()
+
+
+@pytest.mark.parametrize("seed,cap,ranking", [(11, 10**6, 0), (12, 700, 0), (13, 350, 2), (14, 500, 1)])
+def test_prefix_step_event_stream(seed, cap, ranking):
+    """augsched_step_prefix on one instance (256 slots) over 60 steps of
+    random engine events: the admitted prefix, grants, limits and the slot
+    state after every step equal the oracle's full-order step; small caps
+    force the demotion / tail-eviction path."""
+    rng = np.random.default_rng(seed)
+    MA = 256
+    cfg = dict(tracegen.PRESET_G0, g_total=1000 + cap, g_model=1000)
+    ip = tracegen.inst_params(1, base=tracegen.INST_G0, ranking=ranking, budget_mode=0, target_max=100,
+                              alpha=1.5, rank_seed=seed)
+    st = oracle.Step(cfg, ip, MA)
+    s = aug.Scheduler(cfg, ip, 1, MA)
+    for t in range(60):
+        rec = random_events(rng, st.slots(0), t, p_new=0.4)
+        if rec is not None:
+            assert st.enqueue(0, rec) == 0
+            s.enqueue(0, rec)
+        o = st.step(t)
+        assert o["rc"] == 0
+        g = s.step_result(s.step(t, prefix=True))
+        compare(g, o, 1, f"prefix seed {seed} step {t}", prefix=True)
+    s.close()
+
+
+def test_prefix_step_cfg4_one_million_queue():
+    """Config 4 through augsched_step_prefix: 3 consecutive steps over the
+    1,000,000-request queue; the admitted prefix equals the oracle's order."""
+    n = 1_000_000
+    rec = tracegen.cfg4_records(n)
+    cfg = tracegen.PRESET_CFG4
+    ip = tracegen.inst_params(1)
+    st = oracle.Step(cfg, ip, n)
+    assert st.enqueue(0, rec) == 0
+    s = aug.Scheduler(cfg, ip, 1, n)
+    s.enqueue(0, rec)
+    t0 = 65536
+    for k in range(3):
+        o = st.step(t0 + k)
+        g = s.step_result(s.step(t0 + k, prefix=True))
+        compare(g, o, 1, f"cfg4 prefix step {k}", prefix=True)
+        assert int(g["admitted"][0]) > 0
     s.close()
