@@ -366,7 +366,7 @@ def run_gpu(args):
         line["step_1m_prefix"] = step_bench(args, dev, stream, peak, prefix=True)
         # size sweep of the prefix step: queues beyond L2 show the HBM-bound regime
         sweep = {}
-        for n_sw in (4_194_304, 16_777_216):
+        for n_sw in (4_194_304, 16_000_000):
             r_sw = step_bench(args, dev, stream, peak, prefix=True, n_override=n_sw)
             sweep[str(n_sw)] = {"value": r_sw["value"], "ms_per_step_cold_l2": r_sw["ms_per_step_cold_l2"],
                                 "roofline_frac": r_sw["roofline"]["frac"],
