@@ -227,12 +227,29 @@ def run_gpu(args):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     dist = None
+    # AUGSCHED_BENCH_BACKEND=gloo: a test mode that runs N ranks on however
+    # many GPUs the box has (device = local_rank mod count), collectives on
+    # host copies; the default is one rank per GPU over NCCL.
+    backend = os.environ.get("AUGSCHED_BENCH_BACKEND", "nccl")
     if world > 1:
         import torch.distributed as dist
+        local = local % torch.cuda.device_count()
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     else:
         torch.cuda.set_device(0)
+
+    def allreduce_(t, op):
+        if backend == "nccl":
+            dist.all_reduce(t, op=op)
+            return t
+        h = t.cpu()
+        dist.all_reduce(h, op=op)
+        t.copy_(h)
+        return t
     if rank == 0:
         _build.build()
     if dist:
@@ -281,9 +298,10 @@ def run_gpu(args):
     tm = torch.tensor([total_ms, dec, isteps], dtype=torch.float64, device=f"cuda:{dev}")
     if dist:
         mx = tm.clone()
-        dist.all_reduce(mx[:1], op=dist.ReduceOp.MAX)
-        dist.all_reduce(tm[1:], op=dist.ReduceOp.SUM)
-        tm[0] = mx[0]
+        allreduce_(mx, dist.ReduceOp.MAX)
+        tot = tm.clone()
+        allreduce_(tot, dist.ReduceOp.SUM)
+        tm = torch.stack([mx[0], tot[1], tot[2]])
         # final NCCL all-gather of the per-instance result records (north star)
         from paper_2512_04013_b200 import dist as adist
         g0 = time.perf_counter()
@@ -354,9 +372,10 @@ def run_gpu(args):
         et = torch.tensor([e_ms, dec_e], dtype=torch.float64, device=f"cuda:{dev}")
         if dist:
             m = et.clone()
-            dist.all_reduce(m[:1], op=dist.ReduceOp.MAX)
-            dist.all_reduce(et[1:], op=dist.ReduceOp.SUM)
-            et[0] = m[0]
+            allreduce_(m, dist.ReduceOp.MAX)
+            tot = et.clone()
+            allreduce_(tot, dist.ReduceOp.SUM)
+            et = torch.stack([m[0], tot[1]])
         line["e2e"] = {"value": float(et[1]) / (float(et[0]) / 1e3), "unit": UNIT,
                        "h2d_bytes_per_step": pinned.nbytes + 4 * n_inst,
                        "d2h_bytes_per_step": n_inst * aug.RESULT_DTYPE.itemsize}

@@ -56,6 +56,7 @@ def all_gather_records(local, world: int):
         out = torch.empty(world * local.numel(), dtype=local.dtype, device=local.device)
         dist.all_gather_into_tensor(out, local.contiguous())
         return out
-    parts = [torch.empty_like(local) for _ in range(world)]
-    dist.all_gather(parts, local.contiguous())
+    host = local.contiguous().cpu()   # gloo gathers host tensors
+    parts = [torch.empty_like(host) for _ in range(world)]
+    dist.all_gather(parts, host)
     return torch.cat(parts)
