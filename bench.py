@@ -154,7 +154,8 @@ def run_reference(args):
     # each step: the oracle on a bounded sample of the same workload
     vals, secs = [], []
     for s in range(args.warmup + args.steps):
-        cb = cpu_baseline(args, tr, ip, tid, args.window * (s + 1), sample=args.cpu_sample or 8)
+        cb = cpu_baseline(args, tr, ip, tid, args.window * (s + 1),
+                          sample=args.cpu_sample or max(8, os.cpu_count() or 1))
         if s >= args.warmup:
             vals.append(cb["value"])
             secs.append(cb["seconds"])
