@@ -249,6 +249,11 @@ int augsched_simulate(augsched_t* h, const augsched_trace* traces, const uint32_
         return fail(AUGSCHED_E_CAPACITY, "instance %u: trace %u has %u requests > max_active %u",
                     i, k, traces->req_off[k + 1] - traces->req_off[k], h->max_active);
     }
+    for (uint32_t r = 0; r < nr; ++r)   // segment lists inside the arrays, meta holds 8 bits
+      if (traces->n_seg[r] < 1 || traces->n_seg[r] > 255 ||
+          (uint64_t)traces->seg_off[r] + traces->n_seg[r] > ns)
+        return fail(AUGSCHED_E_INVALID, "request %u: n_seg %u / seg_off %u out of range", r,
+                    traces->n_seg[r], traces->seg_off[r]);
     const size_t b_req_off = sizeof(uint32_t) * (nt + 1), b64 = sizeof(uint64_t) * nr,
                  b32r = sizeof(uint32_t) * nr, b32s = sizeof(uint32_t) * ns,
                  btid = sizeof(uint32_t) * h->n_inst;

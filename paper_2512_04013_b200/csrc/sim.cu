@@ -53,7 +53,7 @@ struct __align__(16) SimShm {
   unsigned long long freed;
   unsigned int next_arr, n_r, n_w, n_pz, n_fin, wpos;
   unsigned int inst;
-  int run, idle;
+  int run, idle, abort;
 };
 
 enum : int {
@@ -189,7 +189,11 @@ __device__ void do_arrival(Ctx& c, uint32_t id, uint32_t pos, uint64_t t) {
   const double A = has_call ? (double)tr.dur_pred[s0] : 0.0;
   const double V = intake_stage1(c.k, c.ip.policy_mode, L, O, A, has_call, (uint64_t)c.s.A_snap);
   const uint32_t ns = tr.n_seg[rid];
-  if (ns == 0 || ns > 255) { err_set(c.p, 4u); c.s.cnt[AUGSCHED_R_ERR] |= 4; }  // meta holds 8 bits
+  if (ns == 0 || ns > 255) {   // meta holds 8 bits: stop this instance, report E_INVALID
+    err_set(c.p, 4u);
+    c.s.cnt[AUGSCHED_R_ERR] |= 4;
+    c.s.abort = 1;
+  }
   ReqState r;
   r.ctx = 0; r.kv = 0; r.cpu = 0; r.pend = (int32_t)L;
   r.meta = make_meta(0, ST_WAIT, POL_D, ns);
@@ -298,7 +302,7 @@ __device__ __noinline__ void select_cand(SimShm& s, int list, int m, uint64_t D,
 // Thread 0 prepares iteration s.t: stop rule, S1 snapshot, whether intake
 // or the idle jump must run, and (when no intake is due) the token limit.
 __device__ __noinline__ void prep_step(const SimParams& p, SimShm& s, uint32_t n) {
-  s.run = (s.n_fin < n) && (s.t < p.max_iters);
+  s.run = (s.n_fin < n) && (s.t < p.max_iters) && !s.abort;
   s.tT = s.t * p.cfg.t_fwd_ticks;
   s.A_snap = s.A;
   s.due = s.n_r + s.n_w == 0 || s.tT >= s.min_ret || s.tT >= s.next_tick;
@@ -364,6 +368,7 @@ __device__ void run_instance(const SimParams& p, SimShm& s, uint32_t inst) {
     s.t = H.t; s.A = H.A; s.P = H.P; s.min_ret = H.min_ret; s.next_arr = H.next_arr;
     s.n_r = H.n_r; s.n_w = H.n_w; s.n_pz = H.n_pz; s.n_fin = H.n_fin; s.w2 = H.w2;
     s.nholes[0] = s.nholes[1] = 0;
+    s.abort = 0;
     s.next_tick = s.next_arr < n ? p.tr.arr_tick[c.r0 + s.next_arr] : ~0ull;
   }
   for (int f = tid; f < AUGSCHED_R_NFIELD; f += SIM_NT) { s.cnt[f] = acc.f[f]; s.c32[f] = 0; }

@@ -196,3 +196,40 @@ def test_cfg5_bench_launch_sampled_parity():
     sub = {k: v[sample] for k, v in ip.items()}
     o = oracle.simulate(tracegen.PRESET_7B, sub, tr, tid[sample], max_iters=2 * W, threads=16)
     assert_equal_records(g[sample], o, "cfg5")
+
+
+def test_edge_cases_parity():
+    """Degenerate inputs against the oracle: an empty trace, a static limit of
+    0 (nothing is ever admitted, bounded by max_iters), a request with 255
+    segments (the largest n_seg), many one-token prompts under a large limit
+    (more than 32 admitted waiting entries per step: the radix-select
+    fallback of the pop rounds) and tight memory with a large running set
+    (more than 64 eviction candidates: the radix-select eviction)."""
+    reqs_empty = []
+    reqs_many_segs = [R(0, 5, [(1, 10_000, 0.01, 1)] * 254 + [(2,)])]
+    reqs_tiny = [R(1000 * i, 1, [(3,)]) for i in range(400)]
+    reqs_big_run = [R(0, 40, [(30,)]) for _ in range(160)]
+    tr = tracegen.from_requests([reqs_empty, reqs_many_segs, reqs_tiny, reqs_big_run])
+    cfg = dict(tracegen.PRESET_G0, g_total=1000 + 3000, g_model=1000)   # cap 3,000 tokens
+    ip = tracegen.inst_params(6, base=tracegen.INST_G0, budget_mode=[1, 1, 1, 0, 1, 0],
+                              l_static=[50, 0, 100, 0, 2000, 0], target_max=[50, 50, 50, 50, 50, 3000],
+                              alpha=[0.0, 0.0, 0.0, 2.0, 0.0, 1.0])
+    tid = np.array([0, 1, 1, 2, 2, 3], np.uint32)
+    g, _ = gpu_run(cfg, ip, tr, tid, max_iters=5000)
+    o = oracle.simulate(cfg, ip, tr, tid, max_iters=5000)
+    assert_equal_records(g, o, "edge")
+    d = [oracle.as_dict(x) for x in o]
+    assert d[0]["n_requests"] == 0 and d[0]["busy_steps"] == 0
+    assert d[1]["completed"] == 0 and d[1]["decisions"] > 0          # limit 0
+    assert d[2]["completed"] == 1                                     # 255 segments
+    assert d[3]["completed"] == 400 and d[4]["completed"] == 400      # tiny prompts
+    assert d[5]["evictions"] > 0
+
+
+def test_n_seg_above_255_is_rejected():
+    tr = tracegen.from_requests([[R(0, 5, [(1, 1000, 0.0, 1)] * 255 + [(1,)])]])
+    s = aug.Scheduler(tracegen.PRESET_G0, tracegen.inst_params(1, base=tracegen.INST_G0), 1, 4)
+    with pytest.raises(aug.AugschedError) as e:
+        s.simulate_host(tr, [0])
+    assert e.value.code == aug.E_INVALID
+    s.close()

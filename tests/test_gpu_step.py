@@ -177,3 +177,26 @@ def test_prefix_step_cfg4_one_million_queue():
         compare(g, o, 1, f"cfg4 prefix step {k}", prefix=True)
         assert int(g["admitted"][0]) > 0
     s.close()
+
+
+@pytest.mark.parametrize("n_inst,l_static", [(1, 20_000), (2, 150)])
+def test_prefix_step_falls_back_to_full_order(n_inst, l_static):
+    """Handles the prefix selection does not cover (a limit above 8,192, or
+    several instances) run the full step; the admitted prefix still equals
+    the oracle's."""
+    rng = np.random.default_rng(7)
+    MA = 128
+    cfg = dict(tracegen.PRESET_G0, g_total=1000 + 10**6, g_model=1000)
+    ip = tracegen.inst_params(n_inst, base=tracegen.INST_G0, budget_mode=1, l_static=l_static)
+    st = oracle.Step(cfg, ip, MA)
+    s = aug.Scheduler(cfg, ip, n_inst, MA)
+    for t in range(20):
+        for i in range(n_inst):
+            rec = random_events(rng, st.slots(i), t, p_new=0.5)
+            if rec is not None:
+                assert st.enqueue(i, rec) == 0
+                s.enqueue(i, rec)
+        o = st.step(t)
+        g = s.step_result(s.step(t, prefix=True))
+        compare(g, o, n_inst, f"fallback step {t}", prefix=True)
+    s.close()
