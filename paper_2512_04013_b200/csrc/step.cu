@@ -182,7 +182,13 @@ __device__ __forceinline__ uint32_t digit_of(unsigned long long x, const PassDes
 // pass (warp-aggregated shared atomics).
 constexpr int KCNT = 1024;   // per-block instance-count table of the keys kernel
 
-constexpr int KU = 4;   // slots in flight per thread in the keys kernel
+#ifndef AUGSCHED_KEYS_KU
+#define AUGSCHED_KEYS_KU 4
+#endif
+#ifndef AUGSCHED_KEYS_GRIDMUL
+#define AUGSCHED_KEYS_GRIDMUL 4
+#endif
+constexpr int KU = AUGSCHED_KEYS_KU;   // slots in flight per thread in the keys kernel
 
 // Shared histogram increment for bins that are heavily shared within a warp
 // (the top digits of similar scores): the lanes holding lane 0's bin add with
@@ -1172,7 +1178,8 @@ int step_run_prefix(StepState& st, const augsched_config& cfg, int64_t cap,
   ka.N = (uint32_t)st.N;
   ka.pf_cnt = st.pf_cnt;
   const size_t kblocks = (st.N + KNT * KU - 1) / (KNT * KU);
-  const int kgrid = (int)(kblocks < (size_t)st.sms * 4 ? kblocks : (size_t)st.sms * 4);
+  const size_t kmax = (size_t)st.sms * AUGSCHED_KEYS_GRIDMUL;
+  const int kgrid = (int)(kblocks < kmax ? kblocks : kmax);
   keys_kernel<<<kgrid, KNT, 0, s>>>(ka);
   pf_collect_kernel<<<kgrid, KNT, 0, s>>>(st.k0, (uint32_t)st.N, st.pf_cnt, st.pf_A, st.pf_C);
   pf_admit_kernel<<<1, PNT, pf_smem_bytes(), s>>>(S, cfg, cap, now, st.budget, st.n_active, st.k0, st.pf_A,

@@ -23,7 +23,10 @@ namespace augsched {
 constexpr int STEP_MAX_PASS = 8;
 constexpr int STEP_RB_MAX = 10;                 // widest digit (bins = 1 << bits)
 constexpr int STEP_HIST_WORDS = 4096;          // bins over all passes (<= 8), or the prefix digit
-constexpr int PF_BITS = 12;                     // prefix step: top digit (tier:2 + key top 10 bits)
+#ifndef AUGSCHED_PF_BITS
+#define AUGSCHED_PF_BITS 12
+#endif
+constexpr int PF_BITS = AUGSCHED_PF_BITS;       // prefix step: top digit (tier:2 + key top bits)
 constexpr uint32_t PF_SCAP = 8192;              // prefix step: admitted-prefix capacity (max limit)
 constexpr uint32_t PF_CCAP = 16384;             // prefix step: crossing-bucket entries kept on chip
 
