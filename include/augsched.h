@@ -130,6 +130,34 @@ typedef struct augsched_trace {
   uint32_t reserved;
 } augsched_trace;
 
+/* ---- table-driven workload generator --------------------
+ * W1/W2/W3 traces drawn on the device, identical to the host twin
+ * tracegen/tablegen.py: u = mix(mix(seed << 32 | trace) ^ (request << 12 |
+ * field)) with mix = the SplitMix64 output function; continuous
+ * distributions through 4,096-level quantile tables (index u >> 52); integer
+ * draws from u >> 32 (see tracegen/tablegen.py for every field).           */
+typedef struct augsched_gen_tables {
+  const double* gap;         /* [4096] unit-mean inter-arrival quantiles (exponential or gamma) */
+  const uint32_t* prompt;    /* [4096] prompt tokens */
+  const uint32_t* gen;       /* [4096] decoded tokens per segment */
+  const uint32_t* dur;       /* [4][4096] call duration (µs) per tool class */
+  const uint32_t* ret;       /* [4][4096] returned tokens per tool class */
+  const double* noise;       /* [4096] multiplicative duration-prediction noise */
+  uint32_t cls_th[3];        /* cumulative class-share thresholds on u >> 32 */
+  uint32_t calls_lo[4], calls_hi[4];
+  uint32_t edges[8], mids[8];/* bucket predictor: edges and reported midpoints */
+  uint32_t acc_th;           /* predictor hit iff u >> 32 < acc_th */
+  uint32_t nocall_th;        /* request without calls iff u >> 32 < nocall_th */
+  uint32_t oracle_pred;      /* 1: predictions = truth */
+  uint32_t reserved;
+} augsched_gen_tables;
+
+typedef struct augsched_gen_spec {
+  uint32_t seed, n_traces, n_max, reserved;
+  uint64_t horizon_ticks;    /* 0: W2 (exactly n_max requests per trace); else W1/W3 cut */
+  const double* scale;       /* device [n_traces]: 1e6 / (rate of trace k, req/s) */
+} augsched_gen_spec;
+
 /* Per-instance result record of augsched_simulate (fixed size, byte-comparable). */
 enum {
   AUGSCHED_R_NREQ = 0, AUGSCHED_R_ARRIVED, AUGSCHED_R_COMPLETED, AUGSCHED_R_SLO_OK,
@@ -237,6 +265,15 @@ AUGSCHED_API int augsched_step_prefix(augsched_t* h, uint64_t now_iter, augsched
  * device buffer.  E_CAPACITY if a trace is longer than the handle allows. */
 AUGSCHED_API int augsched_simulate(augsched_t* h, const augsched_trace* traces, const uint32_t* inst_trace_id,
                       uint64_t max_iters, augsched_result* results, uint32_t flags);
+
+/* Generate n_traces traces on the device into `out` (device arrays allocated
+ * by the caller: req_off [n_traces + 1], per-request arrays [req_cap],
+ * per-segment arrays [seg_cap]; `tables` points to device tables).  Sets
+ * out->n_traces / n_req / n_seg_total (the call synchronizes the handle's
+ * stream to read the totals).  E_CAPACITY if the traces need more than
+ * req_cap requests or seg_cap segments; E_INVALID for bad arguments. */
+AUGSCHED_API int augsched_generate(augsched_t* h, const augsched_gen_spec* spec, const augsched_gen_tables* tables,
+                      augsched_trace* out, uint32_t req_cap, uint32_t seg_cap);
 
 /* Wait for the handle's stream; returns a latched device error (E_STATE) if any. */
 AUGSCHED_API int augsched_sync(augsched_t* h);

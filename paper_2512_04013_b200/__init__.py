@@ -30,6 +30,7 @@ NBIN = 160
 RESULT_DTYPE = np.dtype([("f", np.uint64, (len(RESULT_FIELDS),)), ("hist_ttft", np.uint32, (NBIN,)),
                          ("hist_norm", np.uint32, (NBIN,))])
 EXPORTS = ["augsched_create", "augsched_enqueue", "augsched_step", "augsched_step_prefix", "augsched_simulate",
+           "augsched_generate",
            "augsched_sync", "augsched_launch_count", "augsched_destroy", "augsched_last_error"]
 
 
@@ -60,6 +61,18 @@ class RecordSoA(C.Structure):
                                           "ctx", "kv", "cpu", "pend")]
 
 
+class GenTables(C.Structure):
+    _fields_ = [(n, C.c_void_p) for n in ("gap", "prompt", "gen", "dur", "ret", "noise")] + \
+               [("cls_th", C.c_uint32 * 3), ("calls_lo", C.c_uint32 * 4), ("calls_hi", C.c_uint32 * 4),
+                ("edges", C.c_uint32 * 8), ("mids", C.c_uint32 * 8), ("acc_th", C.c_uint32),
+                ("nocall_th", C.c_uint32), ("oracle_pred", C.c_uint32), ("reserved", C.c_uint32)]
+
+
+class GenSpec(C.Structure):
+    _fields_ = [("seed", C.c_uint32), ("n_traces", C.c_uint32), ("n_max", C.c_uint32),
+                ("reserved", C.c_uint32), ("horizon_ticks", C.c_uint64), ("scale", C.c_void_p)]
+
+
 class StepOut(C.Structure):
     _fields_ = [(n, C.c_void_p) for n in ("budget", "n_active", "admitted", "order", "grant", "key")]
 
@@ -80,6 +93,8 @@ def lib():
         L.augsched_step.argtypes = [vp, u64, C.POINTER(StepOut)]
         L.augsched_step_prefix.argtypes = [vp, u64, C.POINTER(StepOut)]
         L.augsched_simulate.argtypes = [vp, C.POINTER(Trace), vp, u64, vp, u32]
+        L.augsched_generate.argtypes = [vp, C.POINTER(GenSpec), C.POINTER(GenTables), C.POINTER(Trace), u32, u32]
+        L.augsched_generate.restype = C.c_int
         L.augsched_sync.argtypes = [vp]
         L.augsched_launch_count.argtypes = [vp]
         L.augsched_launch_count.restype = u64
@@ -161,6 +176,53 @@ class DeviceTraces:
         s = Trace(**{k: self.t[k].data_ptr() for k in DeviceTraces._names})
         s.n_traces, s.n_req, s.n_seg_total = self.n_traces, self.n_req, self.n_seg_total
         return s
+
+
+class GeneratedTraces(DeviceTraces):
+    """A trace set drawn on the device by augsched_generate (the table-driven
+    W1/W2/W3 generator; tracegen/tablegen.py is its host twin).  `tables` is
+    the dict of tracegen.tablegen.build_tables (inputs only)."""
+
+    def __init__(self, sched, tables: dict, seed: int, n_traces: int, n_max: int, rates,
+                 horizon_ticks: int = 0, device="cuda"):
+        torch = _torch()
+        rates = list(rates) if hasattr(rates, "__len__") else [rates]
+        dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(device)
+        self._tb = {k: dev(tables[k].view(np.int32) if tables[k].dtype == np.uint32 else tables[k])
+                    for k in ("gap", "prompt", "gen", "dur", "ret", "noise")}
+        self._scale = dev(np.array([1e6 / float(rates[k % len(rates)]) for k in range(n_traces)], np.float64))
+        max_calls = int(np.max(tables["calls_hi"]))
+        req_cap = n_traces * n_max
+        seg_cap = req_cap * (max_calls + 1)
+        i32 = dict(dtype=torch.int32, device=device)
+        self.t = dict(req_off=torch.empty(n_traces + 1, **i32),
+                      arr_tick=torch.empty(req_cap, dtype=torch.int64, device=device),
+                      l_pre=torch.empty(req_cap, **i32), seg_off=torch.empty(req_cap, **i32),
+                      n_seg=torch.empty(req_cap, **i32), gen_true=torch.empty(seg_cap, **i32),
+                      gen_pred=torch.empty(seg_cap, **i32), dur_true=torch.empty(seg_cap, **i32),
+                      dur_pred=torch.empty(seg_cap, dtype=torch.float32, device=device),
+                      ret_len=torch.empty(seg_cap, **i32))
+        tb = GenTables(**{k: v.data_ptr() for k, v in self._tb.items()})
+        for k in ("cls_th", "calls_lo", "calls_hi", "edges", "mids"):
+            getattr(tb, k)[:] = [int(x) for x in tables[k]]
+        tb.acc_th, tb.nocall_th = int(tables["acc_th"]), int(tables["nocall_th"])
+        tb.oracle_pred = int(tables["oracle_pred"])
+        spec = GenSpec(int(seed), int(n_traces), int(n_max), 0, int(horizon_ticks), self._scale.data_ptr())
+        out = Trace(**{k: self.t[k].data_ptr() for k in DeviceTraces._names})
+        _check(sched.L.augsched_generate(sched.h, C.byref(spec), C.byref(tb), C.byref(out), req_cap, seg_cap))
+        self.n_traces, self.n_req, self.n_seg_total = n_traces, int(out.n_req), int(out.n_seg_total)
+
+    def to_numpy(self):
+        """Copy the generated arrays to host numpy (same dtypes as tracegen.Traces)."""
+        u = lambda x, n: x[:n].cpu().numpy()
+        nr, ns = self.n_req, self.n_seg_total
+        return dict(req_off=u(self.t["req_off"], self.n_traces + 1).view(np.uint32),
+                    arr_tick=u(self.t["arr_tick"], nr).view(np.uint64),
+                    l_pre=u(self.t["l_pre"], nr).view(np.uint32), seg_off=u(self.t["seg_off"], nr).view(np.uint32),
+                    n_seg=u(self.t["n_seg"], nr).view(np.uint32), gen_true=u(self.t["gen_true"], ns).view(np.uint32),
+                    gen_pred=u(self.t["gen_pred"], ns).view(np.uint32),
+                    dur_true=u(self.t["dur_true"], ns).view(np.uint32), dur_pred=u(self.t["dur_pred"], ns),
+                    ret_len=u(self.t["ret_len"], ns).view(np.uint32))
 
 
 class PinnedTraces:

@@ -8,7 +8,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libaugsched.so")
-SOURCES = ["sim.cu", "step.cu", "api.cu"]
+SOURCES = ["sim.cu", "step.cu", "gen.cu", "api.cu"]
 HEADERS = ["model.cuh", "sim.cuh", "step.cuh", "select.cuh"]
 
 NVCC_FLAGS = [

@@ -16,6 +16,9 @@ namespace augsched {
 size_t sim_smem_bytes();
 const void* sim_kernel_ptr();
 cudaError_t launch_sim(const SimParams& p, int grid, size_t smem, cudaStream_t st);
+int launch_generate(const augsched_gen_tables& tb, const augsched_gen_spec& sp, const augsched_trace& out,
+                    uint32_t req_cap, uint32_t seg_cap, uint32_t* scratch, uint32_t* totals, uint32_t* err,
+                    cudaStream_t s);
 }  // namespace augsched
 
 using namespace augsched;
@@ -73,6 +76,9 @@ struct augsched_handle {
   void* d_trace_buf = nullptr;
   size_t d_trace_cap = 0;
   uint32_t* d_inst_trace = nullptr;
+  // workload generator scratch
+  uint32_t* gen_scratch = nullptr;
+  size_t gen_scratch_words = 0;
   // step mode
   StepState st{};
   bool step_ready = false;
@@ -209,8 +215,47 @@ void augsched_destroy(augsched_t* h) {
   cudaStreamSynchronize(h->stream);
   for (void* p : h->allocs) cudaFree(p);
   if (h->d_trace_buf) cudaFree(h->d_trace_buf);
+  if (h->gen_scratch) cudaFree(h->gen_scratch);
   step_free(h->st);
   delete h;
+}
+
+int augsched_generate(augsched_t* h, const augsched_gen_spec* spec, const augsched_gen_tables* tables,
+                      augsched_trace* out, uint32_t req_cap, uint32_t seg_cap) {
+  if (!h || !spec || !tables || !out || !spec->scale) return fail(AUGSCHED_E_INVALID, "generate: NULL argument");
+  if (spec->n_traces < 1 || spec->n_max < 1) return fail(AUGSCHED_E_INVALID, "generate: empty spec");
+  for (int c = 0; c < 4; ++c)
+    if (tables->calls_lo[c] > tables->calls_hi[c] || tables->calls_hi[c] > 254)
+      return fail(AUGSCHED_E_INVALID, "generate: calls per request of class %d outside [lo, 254]", c);
+  const void* ptrs[] = {tables->gap, tables->prompt, tables->gen, tables->dur, tables->ret, tables->noise,
+                        out->req_off, out->arr_tick, out->l_pre, out->seg_off, out->n_seg, out->gen_true,
+                        out->gen_pred, out->dur_true, out->dur_pred, out->ret_len};
+  for (const void* q : ptrs)
+    if (!q) return fail(AUGSCHED_E_INVALID, "generate: NULL table or output array");
+  CUDA_TRY(cudaSetDevice(h->device));
+  const size_t words = 4 * (size_t)spec->n_traces + 2 + 2;
+  if (words > h->gen_scratch_words) {
+    if (h->gen_scratch) cudaFree(h->gen_scratch);
+    h->gen_scratch = nullptr;
+    h->gen_scratch_words = 0;
+    CUDA_TRY(cudaMalloc(&h->gen_scratch, words * sizeof(uint32_t)));
+    h->gen_scratch_words = words;
+  }
+  uint32_t* totals = h->gen_scratch + words - 2;
+  CUDA_TRY(cudaMemsetAsync(h->d_err, 0, sizeof(uint32_t), h->stream));
+  h->launches += launch_generate(*tables, *spec, *out, req_cap, seg_cap, h->gen_scratch, totals, h->d_err,
+                                 h->stream);
+  CUDA_TRY(cudaGetLastError());
+  uint32_t tot[2] = {0, 0}, err = 0;
+  CUDA_TRY(cudaMemcpyAsync(tot, totals, sizeof(tot), cudaMemcpyDeviceToHost, h->stream));
+  CUDA_TRY(cudaMemcpyAsync(&err, h->d_err, sizeof(err), cudaMemcpyDeviceToHost, h->stream));
+  CUDA_TRY(cudaStreamSynchronize(h->stream));
+  if (err & 2u) return fail(AUGSCHED_E_CAPACITY, "generate: %u requests / %u segments exceed %u / %u",
+                            tot[0], tot[1], req_cap, seg_cap);
+  out->n_traces = spec->n_traces;
+  out->n_req = tot[0];
+  out->n_seg_total = tot[1];
+  return AUGSCHED_OK;
 }
 
 int augsched_sync(augsched_t* h) {
