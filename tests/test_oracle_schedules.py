@@ -339,3 +339,24 @@ def test_ablation_directions():
     assert good["fcfs_dyn"] > good["fcfs_static"]
     assert good["augserve"] > good["aug_static"]
     assert good["augserve"] > good["fcfs_dyn"]
+
+
+def test_cv_robustness_direction():
+    """SPEC acceptance 7 / tab:cv: on W3 arrivals (Gamma, 30-minute
+    horizon) at 2 req/s, raising the coefficient of variation from 1 to 2
+    costs FCFS a larger relative share of its goodput than AugServe, and
+    AugServe's goodput stays far above FCFS's."""
+    from tracegen import tablegen as tg
+    H = 1800 * 10**6
+    good = {}
+    for cv in (1.0, 2.0):
+        tr = tg.generate(tg.build_tables(cv=cv), 31, 2, 20000, [2.0, 2.0], horizon_ticks=H)
+        tid = np.arange(2, dtype=np.uint32)
+        for mode, kw in (("fcfs", dict(ranking=1, budget_mode=1, l_static=500)),
+                         ("aug", dict(ranking=0, budget_mode=0))):
+            ip = tracegen.inst_params(2, **kw)
+            d = [oracle.as_dict(x) for x in oracle.simulate(tracegen.PRESET_7B, ip, tr, tid, threads=2)]
+            good[(cv, mode)] = sum(x["slo_ok"] for x in d)
+    loss = {m: 1 - good[(2.0, m)] / good[(1.0, m)] for m in ("fcfs", "aug")}
+    assert loss["fcfs"] > loss["aug"]
+    assert good[(2.0, "aug")] > 5 * good[(2.0, "fcfs")]
