@@ -736,46 +736,19 @@ __global__ void __launch_bounds__(KNT) pf_collect_kernel(const unsigned long lon
 
 constexpr int PNT = 1024;
 
-__global__ void __launch_bounds__(PNT) pf_admit_kernel(Slots S, augsched_config cfg, int64_t cap, uint64_t now,
-                                                       const long long* budget, const uint32_t* n_active,
-                                                       const unsigned long long* k0,
-                                                       const unsigned long long* A,
-                                                       const unsigned long long* C, const uint32_t* cnt,
-                                                       uint32_t* order, uint32_t* keyout, uint32_t* grant,
-                                                       uint32_t* admitted, uint32_t* gslot) {
-  extern __shared__ __align__(16) unsigned long long pf_sm[];
-  unsigned long long* sbuf = pf_sm;              // [2 * PF_SCAP] the prefix + exchange buffer
-  __shared__ SelShm sel;
-  __shared__ unsigned long long wsum[PNT / 32];
-  __shared__ unsigned long long freed;
-  __shared__ uint32_t m_s;
+// The admitted prefix of instance `inst` from `mt` candidate words in sbuf
+// (which hold its first `target` order entries): bitonic sort, admission
+// (R17), resolution by exact selections over the instance's slots (R20),
+// grant accounting.  `keys` are the instance's packed words (local slot in
+// the low bits; tier 3 = not queued); `xch` is a second buffer of the same
+// size as sbuf for the sort's shared-memory exchanges.
+__device__ void pf_finish(const Slots& S, const augsched_config& cfg, int64_t cap, uint64_t now, uint32_t inst,
+                          size_t base, const unsigned long long* keys, unsigned long long* sbuf,
+                          unsigned long long* xch, uint32_t mt, uint32_t target, long long B, uint32_t* order,
+                          uint32_t* keyout, uint32_t* grant, uint32_t* admitted, uint32_t* gslot, SelShm& sel,
+                          unsigned long long* wsum, unsigned long long& freed) {
   const int tid = threadIdx.x;
   const uint32_t MA = S.MA;
-  const long long B = budget[0];
-  const uint32_t target = pf_target(B, n_active[0]);
-  const uint32_t nA = cnt[0], nC = cnt[1];
-  // ---- the first `target` entries of the order: A, plus the smallest of C
-  for (uint32_t i = tid; i < nA; i += PNT) sbuf[i] = A[i];
-  if (tid == 0) m_s = nA;
-  const uint32_t needC = target > nA ? target - nA : 0u;
-  if (needC > 0 && nA + nC <= PF_SCAP) {
-    // the whole crossing bucket fits beside A: sort them all, keep `target`
-    for (uint32_t i = tid; i < nC; i += PNT) sbuf[nA + i] = C[i];
-    if (tid == 0) m_s = nA + nC;
-  } else if (needC > 0) {
-    // large crossing bucket: select its (target - |A|) smallest in place
-    const unsigned long long* cb = C;
-    __syncthreads();
-    wselect<PNT>(sel, nC, needC, 64, [&](uint32_t i, uint64_t& key, uint32_t& w) {
-      key = cb[i]; w = 1u; return true; });
-    const unsigned long long tau = sel.r.found ? sel.r.k : ~0ull;
-    for (uint32_t i = tid; i < nC; i += PNT) {
-      const unsigned long long x = cb[i];
-      if (x <= tau) sbuf[atomicAdd(&m_s, 1u)] = x;
-    }
-  }
-  __syncthreads();
-  const uint32_t mt = m_s;  // >= target entries, the first `target` of the order among them
   // ---- bitonic sort of the prefix (padded to a power of two).  Each thread
   // holds E = P2 / PNT elements (index tid + e * PNT) in registers: partner
   // distances j < 32 exchange by warp shuffles, j >= PNT inside the thread,
@@ -806,11 +779,11 @@ __global__ void __launch_bounds__(PNT) pf_admit_kernel(Slots S, augsched_config 
           v[e] = keep_min ? (pv < v[e] ? pv : v[e]) : (pv > v[e] ? pv : v[e]);
         }
       } else if (j < PNT) {
-        unsigned long long* xbuf = xp ? sbuf + PF_SCAP : sbuf;
+        unsigned long long* xbuf = xp ? xch : sbuf;
         xp ^= 1;
 #pragma unroll
         for (int e = 0; e < EMAX; ++e)
-          if (e < (int)E) xbuf[tid + e * PNT] = v[e];
+          if (e < (int)E && tid + e * PNT < P2) xbuf[tid + e * PNT] = v[e];
         __syncthreads();
 #pragma unroll
         for (int e = 0; e < EMAX; ++e) {
@@ -856,7 +829,7 @@ __global__ void __launch_bounds__(PNT) pf_admit_kernel(Slots S, augsched_config 
     uint32_t slot = 0;
     if (j < m) {
       slot = (uint32_t)sbuf[j] & SLOT_MASK;
-      d = slot_demand(S, slot, cfg.s_in);
+      d = slot_demand(S, (uint32_t)(base + slot), cfg.s_in);
     }
     unsigned long long tot;
     const unsigned long long inc = block_incl_scan_u64<PNT>(d, wsum, &tot);
@@ -864,10 +837,10 @@ __global__ void __launch_bounds__(PNT) pf_admit_kernel(Slots S, augsched_config 
     const bool in = j < m && (long long)ex < B;
     if (in) {
       const unsigned long long g = d < (unsigned long long)B - ex ? d : (unsigned long long)B - ex;
-      order[j] = slot;
-      keyout[j] = (uint32_t)(sbuf[j] >> PK_KEY);
-      grant[j] = (uint32_t)g;
-      gslot[slot] = (uint32_t)g;
+      order[base + j] = slot;
+      keyout[base + j] = (uint32_t)(sbuf[j] >> PK_KEY);
+      grant[base + j] = (uint32_t)g;
+      gslot[base + slot] = (uint32_t)g;
       gsum += g;
     }
     adm += __syncthreads_count(in);
@@ -875,13 +848,13 @@ __global__ void __launch_bounds__(PNT) pf_admit_kernel(Slots S, augsched_config 
   }
   unsigned long long need;
   block_incl_scan_u64<PNT>(gsum, wsum, &need);
-  long long fr = cap - ld_ll(&S.A[0]) - ld_ll(&S.P[0]);
+  long long fr = cap - ld_ll(&S.A[inst]) - ld_ll(&S.P[inst]);
   // ---- a7 resolution (rare; exact selections over every slot)
   if ((long long)need > fr) {
     if (tid == 0) freed = 0;
     auto getp = [&](uint32_t x, uint64_t& key, uint32_t& w) {
-      const uint32_t stv = S.st[x];
-      const int32_t kv = S.kv[x];
+      const uint32_t stv = S.st[base + x];
+      const int32_t kv = S.kv[base + x];
       if ((stv & 15) != ST_PAUSED || ((stv >> 4) & 3) != POL_P || kv <= 0) return false;
       key = ((uint64_t)(0xFFFFFFFFu - (uint32_t)kv) << 24) | x;
       w = (uint32_t)kv;
@@ -896,21 +869,21 @@ __global__ void __launch_bounds__(PNT) pf_admit_kernel(Slots S, augsched_config 
         uint32_t w;
         if (getp(x, key, w) && (!f0 || key <= kd)) {
           atomicAdd(&freed, (unsigned long long)w);
-          S.kv[x] = 0;
-          S.st[x] = ST_PAUSED | ((uint32_t)POL_D << 4);
+          S.kv[base + x] = 0;
+          S.st[base + x] = ST_PAUSED | ((uint32_t)POL_D << 4);
         }
       }
     }
     __syncthreads();
-    if (tid == 0) ledger_add(&S.P[0], -(long long)freed);
+    if (tid == 0) ledger_add(&S.P[inst], -(long long)freed);
     fr += (long long)freed;
     if ((long long)need > fr) {
       // from the tail of the order over queued entries with kv + g > 0
       auto gete = [&](uint32_t x, uint64_t& key, uint32_t& w) {
-        const unsigned long long kx = k0[x];
+        const unsigned long long kx = keys[x];
         if ((kx >> PK_TIER) >= 3) return false;
-        const uint32_t g = gslot[x];
-        w = (uint32_t)S.kv[x] + (g == 0xFFFFFFFFu ? 0u : g);
+        const uint32_t g = gslot[base + x];
+        w = (uint32_t)S.kv[base + x] + (g == 0xFFFFFFFFu ? 0u : g);
         key = ~kx;
         return w > 0;
       };
@@ -923,26 +896,26 @@ __global__ void __launch_bounds__(PNT) pf_admit_kernel(Slots S, augsched_config 
         uint64_t key;
         uint32_t w;
         if (gete(x, key, w) && (!f1 || key <= k1)) {
-          dA -= S.kv[x];
-          S.kv[x] = 0;
-          S.cpu[x] = 0;
-          S.st[x] = ST_WAIT | (S.st[x] & 0x30u);
-          if (gslot[x]) gslot[x] = 0xFFFFFFFFu;   // grant cancelled
+          dA -= S.kv[base + x];
+          S.kv[base + x] = 0;
+          S.cpu[base + x] = 0;
+          S.st[base + x] = ST_WAIT | (S.st[base + x] & 0x30u);
+          if (gslot[base + x]) gslot[base + x] = 0xFFFFFFFFu;   // grant cancelled
         }
       }
-      if (dA) ledger_add(&S.A[0], dA);
+      if (dA) ledger_add(&S.A[inst], dA);
       __syncthreads();
       for (uint32_t j = tid; j < adm; j += PNT)
-        if (gslot[order[j]] == 0xFFFFFFFFu) grant[j] = 0;
+        if (gslot[base + order[base + j]] == 0xFFFFFFFFu) grant[base + j] = 0;
     }
   }
   __syncthreads();
   // ---- S9 + token accounting of the granted batch
   unsigned long long dA = 0;
   for (uint32_t j = tid; j < adm; j += PNT) {
-    const uint32_t g_slot = order[j];
+    const size_t g_slot = base + order[base + j];
     gslot[g_slot] = 0;
-    const uint32_t gr = grant[j];
+    const uint32_t gr = grant[base + j];
     if (gr == 0) continue;
     int32_t ctx = S.ctx[g_slot], kv = S.kv[g_slot], cpu = S.cpu[g_slot], pend = S.pend[g_slot];
     if (cpu > 0) { cpu -= (int32_t)gr; kv += (int32_t)gr; }
@@ -960,11 +933,110 @@ __global__ void __launch_bounds__(PNT) pf_admit_kernel(Slots S, augsched_config 
   unsigned long long tot;
   block_incl_scan_u64<PNT>(dA, wsum, &tot);
   if (tid == 0) {
-    admitted[0] = adm;
-    const long long a = ld_ll(&S.A[0]) + (long long)tot;
-    S.A[0] = a;
-    S.Aevt[0] = a;
+    admitted[inst] = adm;
+    const long long a = ld_ll(&S.A[inst]) + (long long)tot;
+    S.A[inst] = a;
+    S.Aevt[inst] = a;
   }
+}
+
+__global__ void __launch_bounds__(PNT) pf_admit_kernel(Slots S, augsched_config cfg, int64_t cap, uint64_t now,
+                                                       const long long* budget, const uint32_t* n_active,
+                                                       const unsigned long long* k0,
+                                                       const unsigned long long* A,
+                                                       const unsigned long long* C, const uint32_t* cnt,
+                                                       uint32_t* order, uint32_t* keyout, uint32_t* grant,
+                                                       uint32_t* admitted, uint32_t* gslot) {
+  extern __shared__ __align__(16) unsigned long long pf_sm[];
+  unsigned long long* sbuf = pf_sm;              // [2 * PF_SCAP] the prefix + exchange buffer
+  __shared__ SelShm sel;
+  __shared__ unsigned long long wsum[PNT / 32];
+  __shared__ unsigned long long freed;
+  __shared__ uint32_t m_s;
+  const int tid = threadIdx.x;
+  const uint32_t MA = S.MA;
+  const long long B = budget[0];
+  const uint32_t target = pf_target(B, n_active[0]);
+  const uint32_t nA = cnt[0], nC = cnt[1];
+  // ---- the first `target` entries of the order: A, plus the smallest of C
+  for (uint32_t i = tid; i < nA; i += PNT) sbuf[i] = A[i];
+  if (tid == 0) m_s = nA;
+  const uint32_t needC = target > nA ? target - nA : 0u;
+  if (needC > 0 && nA + nC <= PF_SCAP) {
+    // the whole crossing bucket fits beside A: sort them all, keep `target`
+    for (uint32_t i = tid; i < nC; i += PNT) sbuf[nA + i] = C[i];
+    if (tid == 0) m_s = nA + nC;
+  } else if (needC > 0) {
+    // large crossing bucket: select its (target - |A|) smallest in place
+    const unsigned long long* cb = C;
+    __syncthreads();
+    wselect<PNT>(sel, nC, needC, 64, [&](uint32_t i, uint64_t& key, uint32_t& w) {
+      key = cb[i]; w = 1u; return true; });
+    const unsigned long long tau = sel.r.found ? sel.r.k : ~0ull;
+    for (uint32_t i = tid; i < nC; i += PNT) {
+      const unsigned long long x = cb[i];
+      if (x <= tau) sbuf[atomicAdd(&m_s, 1u)] = x;
+    }
+  }
+  __syncthreads();
+  const uint32_t mt = m_s;  // >= target entries, the first `target` of the order among them
+  pf_finish(S, cfg, cap, now, 0, 0, k0, sbuf, sbuf + PF_SCAP, mt, target, B, order, keyout, grant, admitted,
+            gslot, sel, wsum, freed);
+}
+
+
+// Prefix step of a multi-instance handle: one CTA per instance keeps the
+// instance's packed words in shared memory, selects its first min(B, n)
+// order entries by a count-weighted radix select, then pf_finish.
+__global__ void __launch_bounds__(PNT) pf_multi_kernel(Slots S, augsched_config cfg, int64_t cap, uint64_t now,
+                                                       long long* budget, uint32_t* n_active, uint32_t* order,
+                                                       uint32_t* keyout, uint32_t* grant, uint32_t* admitted,
+                                                       uint32_t* gslot, uint32_t sbuf_cap) {
+  extern __shared__ __align__(16) unsigned long long pf_sm[];
+  const uint32_t MA = S.MA;
+  unsigned long long* kbuf = pf_sm;             // [MA] packed words of the instance
+  unsigned long long* sbuf = pf_sm + MA;        // [sbuf_cap] the prefix
+  unsigned long long* xch = sbuf + sbuf_cap;    // [sbuf_cap] sort exchange buffer
+  __shared__ SelShm sel;
+  __shared__ unsigned long long wsum[PNT / 32];
+  __shared__ unsigned long long freed;
+  __shared__ uint32_t m_s;
+  __shared__ long long B_s;
+  const int tid = threadIdx.x;
+  const uint32_t inst = blockIdx.x;
+  const size_t base = (size_t)inst * MA;
+  const Coef& k = S.coef[inst];
+  const augsched_instance_params& ip = S.ip[inst];
+  if (tid == 0) {
+    B_s = token_limit(cfg, k, ip, cap, ld_ll(&S.A[inst]), ld_ll(&S.P[inst]));
+    budget[inst] = B_s;
+    m_s = 0;
+  }
+  unsigned long long myq = 0;
+  for (uint32_t x = tid; x < MA; x += PNT) {
+    const uint32_t stv = S.st[base + x] & 15;
+    const uint32_t tier = (stv >= ST_RUN && stv <= ST_WAIT) ? stv - ST_RUN : 3u;
+    const uint32_t key = tier < 3 ? rank_key(k, ip, S.V[base + x], now, S.last[base + x], x) : 0u;
+    kbuf[x] = ((unsigned long long)tier << PK_TIER) | ((unsigned long long)key << PK_KEY) | x;
+    myq += tier < 3;
+  }
+  unsigned long long nq;
+  block_incl_scan_u64<PNT>(myq, wsum, &nq);   // syncs
+  const long long B = B_s;
+  const uint32_t target = pf_target(B, (uint32_t)nq);
+  if (tid == 0) n_active[inst] = (uint32_t)nq;
+  if (target > 0) {
+    wselect<PNT>(sel, MA, target, 64, [&](uint32_t i, uint64_t& key, uint32_t& w) {
+      key = kbuf[i]; w = 1u; return (key >> PK_TIER) < 3; });
+    const unsigned long long tau = sel.r.found ? sel.r.k : ~0ull;
+    for (uint32_t x = tid; x < MA; x += PNT) {
+      const unsigned long long kx = kbuf[x];
+      if ((kx >> PK_TIER) < 3 && kx <= tau) sbuf[atomicAdd(&m_s, 1u)] = kx;
+    }
+  }
+  __syncthreads();
+  pf_finish(S, cfg, cap, now, inst, base, kbuf, sbuf, xch, m_s, target, B, order, keyout, grant, admitted,
+            gslot, sel, wsum, freed);
 }
 
 }  // namespace
@@ -1099,6 +1171,7 @@ int step_ensure(StepState& st, uint32_t n_inst, uint32_t max_active, cudaStream_
   cudaDeviceGetAttribute(&st.sms, cudaDevAttrMultiProcessorCount, dev);
   cudaFuncSetAttribute(pf_admit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)(sizeof(unsigned long long) * 2 * PF_SCAP));
+  cudaFuncSetAttribute(pf_multi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PF_MULTI_SMEM);
   st.epoch = 0;
   st.ready = true;
   return cuda_check(cudaGetLastError(), "step_ensure");
@@ -1165,11 +1238,27 @@ static size_t pf_smem_bytes() { return sizeof(unsigned long long) * 2 * PF_SCAP;
 int step_run_prefix(StepState& st, const augsched_config& cfg, int64_t cap,
                     const augsched_instance_params* d_ip, uint32_t* d_err, uint64_t now,
                     augsched_step_out* out, cudaStream_t s, uint64_t* launches) {
-  // the prefix selection is single-instance and bounded by PF_SCAP
-  if (st.n_inst != 1 || st.max_limit > PF_SCAP)
+  // the prefix selection is bounded by PF_SCAP; several instances need their
+  // slots on chip (one CTA per instance)
+  uint32_t scap = 32;
+  while (scap < st.max_limit) scap <<= 1;
+  const size_t msmem = sizeof(unsigned long long) * ((size_t)st.max_active + 2 * (size_t)scap);
+  if (st.max_limit > PF_SCAP || (st.n_inst > 1 && msmem > PF_MULTI_SMEM))
     return step_run(st, cfg, cap, d_ip, d_err, now, out, s, launches);
   Slots S = slots_of(st, d_ip);
   run_records(st, S, d_err, now, s, launches);
+  if (st.n_inst > 1) {
+    pf_multi_kernel<<<st.n_inst, PNT, msmem, s>>>(S, cfg, cap, now, st.budget, st.n_active, st.order, st.key,
+                                                  st.grant, st.admitted, st.gslot, scap);
+    *launches += 1;
+    out->budget = reinterpret_cast<const int64_t*>(st.budget);
+    out->n_active = st.n_active;
+    out->admitted = st.admitted;
+    out->order = st.order;
+    out->grant = st.grant;
+    out->key = st.key;
+    return cuda_check(cudaGetLastError(), "step_prefix");
+  }
   cudaMemsetAsync(st.zbuf, 0, sizeof(uint32_t) * st.zwords, s);
   KeyArgs ka;
   ka.S = S; ka.cfg = cfg; ka.cap = cap; ka.now = now; ka.k0 = st.k0;

@@ -29,6 +29,7 @@ constexpr int STEP_HIST_WORDS = 4096;          // bins over all passes (<= 8), o
 constexpr int PF_BITS = AUGSCHED_PF_BITS;       // prefix step: top digit (tier:2 + key top bits)
 constexpr uint32_t PF_SCAP = 8192;              // prefix step: admitted-prefix capacity (max limit)
 constexpr uint32_t PF_CCAP = 16384;             // prefix step: crossing-bucket entries kept on chip
+constexpr size_t PF_MULTI_SMEM = 200 * 1024;    // prefix step, several instances: shared memory per CTA
 
 struct PassDesc {
   int src;    // 0: `bits` bits of the packed key at `shift`; 2: byte of the instance index

@@ -179,7 +179,7 @@ def test_prefix_step_cfg4_one_million_queue():
     s.close()
 
 
-@pytest.mark.parametrize("n_inst,l_static", [(1, 20_000), (2, 150)])
+@pytest.mark.parametrize("n_inst,l_static", [(1, 20_000), (2, 150), (3, 9000)])
 def test_prefix_step_falls_back_to_full_order(n_inst, l_static):
     """Handles the prefix selection does not cover (a limit above 8,192, or
     several instances) run the full step; the admitted prefix still equals
@@ -199,4 +199,31 @@ def test_prefix_step_falls_back_to_full_order(n_inst, l_static):
         o = st.step(t)
         g = s.step_result(s.step(t, prefix=True))
         compare(g, o, n_inst, f"fallback step {t}", prefix=True)
+    s.close()
+
+
+@pytest.mark.parametrize("seed,cap", [(21, 10**6), (22, 900), (23, 400)])
+def test_prefix_step_multi_instance_event_stream(seed, cap):
+    """augsched_step_prefix on a 4-instance handle (one CTA per instance:
+    keys in shared memory, count-weighted radix select, sort, admission,
+    resolution, apply): 40 steps of random events, value / FCFS / random
+    ranking, small caps forcing demotion and tail eviction."""
+    rng = np.random.default_rng(seed)
+    n_inst, MA = 4, 64
+    cfg = dict(tracegen.PRESET_G0, g_total=1000 + cap, g_model=1000)
+    ip = tracegen.inst_params(n_inst, base=tracegen.INST_G0, ranking=[0, 1, 0, 2], budget_mode=[1, 0, 0, 0],
+                              l_static=150, target_max=[50, 200, 120, 90], alpha=[0.0, 0.0, 3.0, 0.0],
+                              rank_seed=[0, 0, 0, 99 + seed])
+    st = oracle.Step(cfg, ip, MA)
+    s = aug.Scheduler(cfg, ip, n_inst, MA)
+    for t in range(40):
+        for i in range(n_inst):
+            rec = random_events(rng, st.slots(i), t)
+            if rec is not None:
+                assert st.enqueue(i, rec) == 0
+                s.enqueue(i, rec)
+        o = st.step(t)
+        assert o["rc"] == 0
+        g = s.step_result(s.step(t, prefix=True))
+        compare(g, o, n_inst, f"multi prefix seed {seed} step {t}", prefix=True)
     s.close()
