@@ -742,6 +742,7 @@ constexpr int PNT = 1024;
 // grant accounting.  `keys` are the instance's packed words (local slot in
 // the low bits; tier 3 = not queued); `xch` is a second buffer of the same
 // size as sbuf for the sort's shared-memory exchanges.
+template <int NT, int EM>
 __device__ void pf_finish(const Slots& S, const augsched_config& cfg, int64_t cap, uint64_t now, uint32_t inst,
                           size_t base, const unsigned long long* keys, unsigned long long* sbuf,
                           unsigned long long* xch, uint32_t mt, uint32_t target, long long B, uint32_t* order,
@@ -750,19 +751,19 @@ __device__ void pf_finish(const Slots& S, const augsched_config& cfg, int64_t ca
   const int tid = threadIdx.x;
   const uint32_t MA = S.MA;
   // ---- bitonic sort of the prefix (padded to a power of two).  Each thread
-  // holds E = P2 / PNT elements (index tid + e * PNT) in registers: partner
-  // distances j < 32 exchange by warp shuffles, j >= PNT inside the thread,
-  // and only 32 <= j < PNT goes through shared memory (double-buffered, one
+  // holds E = P2 / NT elements (index tid + e * NT) in registers: partner
+  // distances j < 32 exchange by warp shuffles, j >= NT inside the thread,
+  // and only 32 <= j < NT goes through shared memory (double-buffered, one
   // barrier per stage).
   uint32_t P2 = 1;
   while (P2 < mt) P2 <<= 1;
   if (P2 < 32) P2 = 32;
-  constexpr int EMAX = PF_SCAP / PNT;
-  const uint32_t E = P2 > PNT ? P2 / PNT : 1u;
+  constexpr int EMAX = EM;
+  const uint32_t E = P2 > NT ? P2 / NT : 1u;
   unsigned long long v[EMAX];
 #pragma unroll
   for (int e = 0; e < EMAX; ++e) {
-    const uint32_t idx = tid + e * PNT;
+    const uint32_t idx = tid + e * NT;
     v[e] = (e < (int)E && idx < mt) ? sbuf[idx] : ~0ull;
   }
   __syncthreads();
@@ -774,36 +775,36 @@ __device__ void pf_finish(const Slots& S, const augsched_config& cfg, int64_t ca
         for (int e = 0; e < EMAX; ++e) {
           if (e >= (int)E) break;
           const unsigned long long pv = __shfl_xor_sync(FULL, v[e], j);
-          const uint32_t idx = tid + e * PNT;
+          const uint32_t idx = tid + e * NT;
           const bool keep_min = ((idx & j) == 0) == ((idx & k) == 0);
           v[e] = keep_min ? (pv < v[e] ? pv : v[e]) : (pv > v[e] ? pv : v[e]);
         }
-      } else if (j < PNT) {
+      } else if (j < NT) {
         unsigned long long* xbuf = xp ? xch : sbuf;
         xp ^= 1;
 #pragma unroll
         for (int e = 0; e < EMAX; ++e)
-          if (e < (int)E && tid + e * PNT < P2) xbuf[tid + e * PNT] = v[e];
+          if (e < (int)E && tid + e * NT < P2) xbuf[tid + e * NT] = v[e];
         __syncthreads();
 #pragma unroll
         for (int e = 0; e < EMAX; ++e) {
           if (e >= (int)E) break;
-          const uint32_t idx = tid + e * PNT;
+          const uint32_t idx = tid + e * NT;
           if (idx >= P2) continue;
           const unsigned long long pv = xbuf[idx ^ j];
           const bool keep_min = ((idx & j) == 0) == ((idx & k) == 0);
           v[e] = keep_min ? (pv < v[e] ? pv : v[e]) : (pv > v[e] ? pv : v[e]);
         }
       } else {
-        // partner inside the thread: e ^ (j / PNT), unrolled so v stays in registers
+        // partner inside the thread: e ^ (j / NT), unrolled so v stays in registers
 #pragma unroll
         for (int bsh = 0; (1 << bsh) < EMAX; ++bsh) {
-          if (j != ((uint32_t)PNT << bsh)) continue;
+          if (j != ((uint32_t)NT << bsh)) continue;
 #pragma unroll
           for (int e = 0; e < EMAX; ++e) {
             const int e2 = e ^ (1 << bsh);
             if (e2 <= e || e2 >= (int)E) continue;
-            const uint32_t idx = tid + e * PNT;
+            const uint32_t idx = tid + e * NT;
             const bool up = (idx & k) == 0;
             const unsigned long long x0 = v[e], x1 = v[e2];
             if ((x0 > x1) == up) { v[e] = x1; v[e2] = x0; }
@@ -815,7 +816,7 @@ __device__ void pf_finish(const Slots& S, const augsched_config& cfg, int64_t ca
   __syncthreads();
 #pragma unroll
   for (int e = 0; e < EMAX; ++e) {
-    const uint32_t idx = tid + e * PNT;
+    const uint32_t idx = tid + e * NT;
     if (e < (int)E && idx < P2) sbuf[idx] = v[e];
   }
   __syncthreads();
@@ -823,7 +824,7 @@ __device__ void pf_finish(const Slots& S, const augsched_config& cfg, int64_t ca
   // ---- a6 admission over the prefix (P_{j-1} < B, partial last, R17)
   unsigned long long Prun = 0, gsum = 0;
   uint32_t adm = 0;
-  for (uint32_t j0 = 0; j0 < m && (long long)Prun < B; j0 += PNT) {
+  for (uint32_t j0 = 0; j0 < m && (long long)Prun < B; j0 += NT) {
     const uint32_t j = j0 + tid;
     unsigned long long d = 0;
     uint32_t slot = 0;
@@ -832,7 +833,7 @@ __device__ void pf_finish(const Slots& S, const augsched_config& cfg, int64_t ca
       d = slot_demand(S, (uint32_t)(base + slot), cfg.s_in);
     }
     unsigned long long tot;
-    const unsigned long long inc = block_incl_scan_u64<PNT>(d, wsum, &tot);
+    const unsigned long long inc = block_incl_scan_u64<NT>(d, wsum, &tot);
     const unsigned long long ex = Prun + inc - d;
     const bool in = j < m && (long long)ex < B;
     if (in) {
@@ -847,7 +848,7 @@ __device__ void pf_finish(const Slots& S, const augsched_config& cfg, int64_t ca
     Prun += tot;
   }
   unsigned long long need;
-  block_incl_scan_u64<PNT>(gsum, wsum, &need);
+  block_incl_scan_u64<NT>(gsum, wsum, &need);
   long long fr = cap - ld_ll(&S.A[inst]) - ld_ll(&S.P[inst]);
   // ---- a7 resolution (rare; exact selections over every slot)
   if ((long long)need > fr) {
@@ -860,11 +861,11 @@ __device__ void pf_finish(const Slots& S, const augsched_config& cfg, int64_t ca
       w = (uint32_t)kv;
       return true;
     };
-    wselect<PNT>(sel, MA, (uint64_t)((long long)need - fr), 56, getp);
+    wselect<NT>(sel, MA, (uint64_t)((long long)need - fr), 56, getp);
     {
       const bool f0 = sel.r.found != 0;
       const uint64_t kd = sel.r.k;
-      for (uint32_t x = tid; x < MA; x += PNT) {
+      for (uint32_t x = tid; x < MA; x += NT) {
         uint64_t key;
         uint32_t w;
         if (getp(x, key, w) && (!f0 || key <= kd)) {
@@ -887,12 +888,12 @@ __device__ void pf_finish(const Slots& S, const augsched_config& cfg, int64_t ca
         key = ~kx;
         return w > 0;
       };
-      wselect<PNT>(sel, MA, (uint64_t)((long long)need - fr), 64, gete);
+      wselect<NT>(sel, MA, (uint64_t)((long long)need - fr), 64, gete);
       const bool f1 = sel.r.found != 0;
       const uint64_t k1 = sel.r.k;
       __syncthreads();
       long long dA = 0;
-      for (uint32_t x = tid; x < MA; x += PNT) {
+      for (uint32_t x = tid; x < MA; x += NT) {
         uint64_t key;
         uint32_t w;
         if (gete(x, key, w) && (!f1 || key <= k1)) {
@@ -905,14 +906,14 @@ __device__ void pf_finish(const Slots& S, const augsched_config& cfg, int64_t ca
       }
       if (dA) ledger_add(&S.A[inst], dA);
       __syncthreads();
-      for (uint32_t j = tid; j < adm; j += PNT)
+      for (uint32_t j = tid; j < adm; j += NT)
         if (gslot[base + order[base + j]] == 0xFFFFFFFFu) grant[base + j] = 0;
     }
   }
   __syncthreads();
   // ---- S9 + token accounting of the granted batch
   unsigned long long dA = 0;
-  for (uint32_t j = tid; j < adm; j += PNT) {
+  for (uint32_t j = tid; j < adm; j += NT) {
     const size_t g_slot = base + order[base + j];
     gslot[g_slot] = 0;
     const uint32_t gr = grant[base + j];
@@ -931,7 +932,7 @@ __device__ void pf_finish(const Slots& S, const augsched_config& cfg, int64_t ca
     S.st[g_slot] = ST_RUN | (S.st[g_slot] & 0x30u);
   }
   unsigned long long tot;
-  block_incl_scan_u64<PNT>(dA, wsum, &tot);
+  block_incl_scan_u64<NT>(dA, wsum, &tot);
   if (tid == 0) {
     admitted[inst] = adm;
     const long long a = ld_ll(&S.A[inst]) + (long long)tot;
@@ -980,15 +981,16 @@ __global__ void __launch_bounds__(PNT) pf_admit_kernel(Slots S, augsched_config 
   }
   __syncthreads();
   const uint32_t mt = m_s;  // >= target entries, the first `target` of the order among them
-  pf_finish(S, cfg, cap, now, 0, 0, k0, sbuf, sbuf + PF_SCAP, mt, target, B, order, keyout, grant, admitted,
-            gslot, sel, wsum, freed);
+  pf_finish<PNT, PF_SCAP / PNT>(S, cfg, cap, now, 0, 0, k0, sbuf, sbuf + PF_SCAP, mt, target, B, order, keyout,
+                                grant, admitted, gslot, sel, wsum, freed);
 }
 
 
 // Prefix step of a multi-instance handle: one CTA per instance keeps the
 // instance's packed words in shared memory, selects its first min(B, n)
 // order entries by a count-weighted radix select, then pf_finish.
-__global__ void __launch_bounds__(PNT) pf_multi_kernel(Slots S, augsched_config cfg, int64_t cap, uint64_t now,
+template <int NT, int EM>
+__global__ void __launch_bounds__(NT) pf_multi_kernel(Slots S, augsched_config cfg, int64_t cap, uint64_t now,
                                                        long long* budget, uint32_t* n_active, uint32_t* order,
                                                        uint32_t* keyout, uint32_t* grant, uint32_t* admitted,
                                                        uint32_t* gslot, uint32_t sbuf_cap) {
@@ -998,7 +1000,7 @@ __global__ void __launch_bounds__(PNT) pf_multi_kernel(Slots S, augsched_config 
   unsigned long long* sbuf = pf_sm + MA;        // [sbuf_cap] the prefix
   unsigned long long* xch = sbuf + sbuf_cap;    // [sbuf_cap] sort exchange buffer
   __shared__ SelShm sel;
-  __shared__ unsigned long long wsum[PNT / 32];
+  __shared__ unsigned long long wsum[NT / 32];
   __shared__ unsigned long long freed;
   __shared__ uint32_t m_s;
   __shared__ long long B_s;
@@ -1013,7 +1015,7 @@ __global__ void __launch_bounds__(PNT) pf_multi_kernel(Slots S, augsched_config 
     m_s = 0;
   }
   unsigned long long myq = 0;
-  for (uint32_t x = tid; x < MA; x += PNT) {
+  for (uint32_t x = tid; x < MA; x += NT) {
     const uint32_t stv = S.st[base + x] & 15;
     const uint32_t tier = (stv >= ST_RUN && stv <= ST_WAIT) ? stv - ST_RUN : 3u;
     const uint32_t key = tier < 3 ? rank_key(k, ip, S.V[base + x], now, S.last[base + x], x) : 0u;
@@ -1021,22 +1023,22 @@ __global__ void __launch_bounds__(PNT) pf_multi_kernel(Slots S, augsched_config 
     myq += tier < 3;
   }
   unsigned long long nq;
-  block_incl_scan_u64<PNT>(myq, wsum, &nq);   // syncs
+  block_incl_scan_u64<NT>(myq, wsum, &nq);   // syncs
   const long long B = B_s;
   const uint32_t target = pf_target(B, (uint32_t)nq);
   if (tid == 0) n_active[inst] = (uint32_t)nq;
   if (target > 0) {
-    wselect<PNT>(sel, MA, target, 64, [&](uint32_t i, uint64_t& key, uint32_t& w) {
+    wselect<NT>(sel, MA, target, 64, [&](uint32_t i, uint64_t& key, uint32_t& w) {
       key = kbuf[i]; w = 1u; return (key >> PK_TIER) < 3; });
     const unsigned long long tau = sel.r.found ? sel.r.k : ~0ull;
-    for (uint32_t x = tid; x < MA; x += PNT) {
+    for (uint32_t x = tid; x < MA; x += NT) {
       const unsigned long long kx = kbuf[x];
       if ((kx >> PK_TIER) < 3 && kx <= tau) sbuf[atomicAdd(&m_s, 1u)] = kx;
     }
   }
   __syncthreads();
-  pf_finish(S, cfg, cap, now, inst, base, kbuf, sbuf, xch, m_s, target, B, order, keyout, grant, admitted,
-            gslot, sel, wsum, freed);
+  pf_finish<NT, EM>(S, cfg, cap, now, inst, base, kbuf, sbuf, xch, m_s, target, B, order, keyout, grant,
+                    admitted, gslot, sel, wsum, freed);
 }
 
 }  // namespace
@@ -1171,7 +1173,9 @@ int step_ensure(StepState& st, uint32_t n_inst, uint32_t max_active, cudaStream_
   cudaDeviceGetAttribute(&st.sms, cudaDevAttrMultiProcessorCount, dev);
   cudaFuncSetAttribute(pf_admit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)(sizeof(unsigned long long) * 2 * PF_SCAP));
-  cudaFuncSetAttribute(pf_multi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PF_MULTI_SMEM);
+  cudaFuncSetAttribute(pf_multi_kernel<256, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PF_MULTI_SMEM);
+  cudaFuncSetAttribute(pf_multi_kernel<PNT, PF_SCAP / PNT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)PF_MULTI_SMEM);
   st.epoch = 0;
   st.ready = true;
   return cuda_check(cudaGetLastError(), "step_ensure");
@@ -1248,8 +1252,13 @@ int step_run_prefix(StepState& st, const augsched_config& cfg, int64_t cap,
   Slots S = slots_of(st, d_ip);
   run_records(st, S, d_err, now, s, launches);
   if (st.n_inst > 1) {
-    pf_multi_kernel<<<st.n_inst, PNT, msmem, s>>>(S, cfg, cap, now, st.budget, st.n_active, st.order, st.key,
-                                                  st.grant, st.admitted, st.gslot, scap);
+    if (scap <= 4 * 256)   // small limits: 256-thread CTAs, more instances resident per SM
+      pf_multi_kernel<256, 4><<<st.n_inst, 256, msmem, s>>>(S, cfg, cap, now, st.budget, st.n_active, st.order,
+                                                             st.key, st.grant, st.admitted, st.gslot, scap);
+    else
+      pf_multi_kernel<PNT, PF_SCAP / PNT><<<st.n_inst, PNT, msmem, s>>>(S, cfg, cap, now, st.budget, st.n_active,
+                                                                        st.order, st.key, st.grant, st.admitted,
+                                                                        st.gslot, scap);
     *launches += 1;
     out->budget = reinterpret_cast<const int64_t*>(st.budget);
     out->n_active = st.n_active;
