@@ -941,7 +941,8 @@ __device__ void pf_finish(const Slots& S, const augsched_config& cfg, int64_t ca
   }
 }
 
-__global__ void __launch_bounds__(PNT) pf_admit_kernel(Slots S, augsched_config cfg, int64_t cap, uint64_t now,
+template <int NT, int EM>
+__global__ void __launch_bounds__(NT) pf_admit_kernel(Slots S, augsched_config cfg, int64_t cap, uint64_t now,
                                                        const long long* budget, const uint32_t* n_active,
                                                        const unsigned long long* k0,
                                                        const unsigned long long* A,
@@ -951,7 +952,7 @@ __global__ void __launch_bounds__(PNT) pf_admit_kernel(Slots S, augsched_config 
   extern __shared__ __align__(16) unsigned long long pf_sm[];
   unsigned long long* sbuf = pf_sm;              // [2 * PF_SCAP] the prefix + exchange buffer
   __shared__ SelShm sel;
-  __shared__ unsigned long long wsum[PNT / 32];
+  __shared__ unsigned long long wsum[NT / 32];
   __shared__ unsigned long long freed;
   __shared__ uint32_t m_s;
   const int tid = threadIdx.x;
@@ -960,29 +961,29 @@ __global__ void __launch_bounds__(PNT) pf_admit_kernel(Slots S, augsched_config 
   const uint32_t target = pf_target(B, n_active[0]);
   const uint32_t nA = cnt[0], nC = cnt[1];
   // ---- the first `target` entries of the order: A, plus the smallest of C
-  for (uint32_t i = tid; i < nA; i += PNT) sbuf[i] = A[i];
+  for (uint32_t i = tid; i < nA; i += NT) sbuf[i] = A[i];
   if (tid == 0) m_s = nA;
   const uint32_t needC = target > nA ? target - nA : 0u;
   if (needC > 0 && nA + nC <= PF_SCAP) {
     // the whole crossing bucket fits beside A: sort them all, keep `target`
-    for (uint32_t i = tid; i < nC; i += PNT) sbuf[nA + i] = C[i];
+    for (uint32_t i = tid; i < nC; i += NT) sbuf[nA + i] = C[i];
     if (tid == 0) m_s = nA + nC;
   } else if (needC > 0) {
     // large crossing bucket: select its (target - |A|) smallest in place
     const unsigned long long* cb = C;
     __syncthreads();
-    wselect<PNT>(sel, nC, needC, 64, [&](uint32_t i, uint64_t& key, uint32_t& w) {
+    wselect<NT>(sel, nC, needC, 64, [&](uint32_t i, uint64_t& key, uint32_t& w) {
       key = cb[i]; w = 1u; return true; });
     const unsigned long long tau = sel.r.found ? sel.r.k : ~0ull;
-    for (uint32_t i = tid; i < nC; i += PNT) {
+    for (uint32_t i = tid; i < nC; i += NT) {
       const unsigned long long x = cb[i];
       if (x <= tau) sbuf[atomicAdd(&m_s, 1u)] = x;
     }
   }
   __syncthreads();
   const uint32_t mt = m_s;  // >= target entries, the first `target` of the order among them
-  pf_finish<PNT, PF_SCAP / PNT>(S, cfg, cap, now, 0, 0, k0, sbuf, sbuf + PF_SCAP, mt, target, B, order, keyout,
-                                grant, admitted, gslot, sel, wsum, freed);
+  pf_finish<NT, EM>(S, cfg, cap, now, 0, 0, k0, sbuf, sbuf + PF_SCAP, mt, target, B, order, keyout,
+                    grant, admitted, gslot, sel, wsum, freed);
 }
 
 
@@ -1171,7 +1172,7 @@ int step_ensure(StepState& st, uint32_t n_inst, uint32_t max_active, cudaStream_
   int dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&st.sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaFuncSetAttribute(pf_admit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaFuncSetAttribute(pf_admit_kernel<PNT, PF_SCAP / PNT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)(sizeof(unsigned long long) * 2 * PF_SCAP));
   cudaFuncSetAttribute(pf_multi_kernel<256, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PF_MULTI_SMEM);
   cudaFuncSetAttribute(pf_multi_kernel<PNT, PF_SCAP / PNT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1280,9 +1281,10 @@ int step_run_prefix(StepState& st, const augsched_config& cfg, int64_t cap,
   const int kgrid = (int)(kblocks < kmax ? kblocks : kmax);
   keys_kernel<<<kgrid, KNT, 0, s>>>(ka);
   pf_collect_kernel<<<kgrid, KNT, 0, s>>>(st.k0, (uint32_t)st.N, st.pf_cnt, st.pf_A, st.pf_C);
-  pf_admit_kernel<<<1, PNT, pf_smem_bytes(), s>>>(S, cfg, cap, now, st.budget, st.n_active, st.k0, st.pf_A,
-                                                  st.pf_C, st.pf_cnt, st.order, st.key, st.grant,
-                                                  st.admitted, st.gslot);
+  pf_admit_kernel<PNT, PF_SCAP / PNT><<<1, PNT, pf_smem_bytes(), s>>>(S, cfg, cap, now, st.budget, st.n_active,
+                                                                      st.k0, st.pf_A, st.pf_C, st.pf_cnt,
+                                                                      st.order, st.key, st.grant, st.admitted,
+                                                                      st.gslot);
   *launches += 3;
   out->budget = reinterpret_cast<const int64_t*>(st.budget);
   out->n_active = st.n_active;
