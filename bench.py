@@ -218,6 +218,38 @@ def step_bench(args, dev, stream, peak, prefix=False, n_override=None):
                          "note": what + "; 32 B/decision, whole step, L2 flushed before each step"}}
 
 
+def step_multi_bench(args, dev, stream, peak, n_inst=4096, ma=2048):
+    """The batched scheduler: one augsched_step / augsched_step_prefix call
+    for n_inst serving instances of `ma` slots each (cfg4-shaped queues),
+    L2 flushed before each step."""
+    import torch
+    import paper_2512_04013_b200 as aug
+    rec = tracegen.cfg4_records(ma, n_running=16, n_swapped=16, n_paused=4)
+    flush = torch.empty(512 * 2**20, dtype=torch.uint8, device=f"cuda:{dev}")
+    res = {"workload": f"{n_inst} instances x {ma} slots (cfg4-shaped queues), one step call for all"}
+    for prefix in (False, True):
+        s = aug.Scheduler(tracegen.PRESET_CFG4, tracegen.inst_params(n_inst), n_inst, ma, device=dev, stream=stream)
+        for i in range(n_inst):
+            s.enqueue(i, rec)
+        t = 65536
+        for _ in range(args.warmup):
+            s.step(t, prefix=prefix); t += 1
+        ms = []
+        for _ in range(args.steps):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream); s.step(t, prefix=prefix); b.record(stream); t += 1
+            torch.cuda.synchronize()
+            ms.append(a.elapsed_time(b))
+        s.close()
+        m = float(np.median(ms))
+        n = n_inst * ma
+        res["prefix" if prefix else "full_order"] = {
+            "value": n / (m / 1e3), "unit": UNIT, "ms_per_step_cold_l2": m,
+            "roofline_frac": round(32.0 * n / (m / 1e3) / 1e9 / peak, 4)}
+    return res
+
+
 # ----------------------------------------------------------------------------- GPU arm
 def run_gpu(args):
     import torch
@@ -392,6 +424,7 @@ def run_gpu(args):
                                 "roofline_frac": r_sw["roofline"]["frac"],
                                 "achieved_gbs": r_sw["roofline"]["achieved"]}
         line["step_1m_prefix"]["size_sweep"] = sweep
+        line["step_multi"] = step_multi_bench(args, dev, stream, peak)
     if rank == 0 and world == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline(args, tr, ip, tid, W * (args.warmup + args.steps),
                                             sample=args.cpu_sample or None)
