@@ -206,7 +206,9 @@ def step_bench(args, dev, stream, peak, prefix=False, n_override=None):
     s.close()
     ms = float(np.median(cold))
     ach = 32.0 * n / (ms / 1e3) / 1e9
-    what = ("augsched_step_prefix: keys + top-digit histogram, collect, one-block select/sort/admit/apply"
+    what = ("augsched_step_prefix: one cooperative kernel (streaming pass: Eq.26 key of every slot, words at "
+            "or below the previous step's anchor kept as candidates; one CTA sorts them and admits/resolves/"
+            "applies; histogram fallback when the anchor fails) + one memset"
             if prefix else "augsched_step: keys + 4 LSD sort passes + admit/resolve/apply")
     return {"workload": f"cfg4: one queue of {n} requests (512 running, 512 swapped, rest waiting "
                         "80% Stage I / 20% Stage II), " + ("admitted prefix" if prefix else "full stable order") +

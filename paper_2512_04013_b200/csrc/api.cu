@@ -170,6 +170,7 @@ int augsched_create(const augsched_config* cfg, const augsched_instance_params* 
   if (rc) return rc;
   std::vector<augsched_instance_params> ip(n_instances);
   uint32_t max_limit = 0;
+  bool any_random = false;
   for (uint32_t i = 0; i < n_instances; ++i) {
     ip[i] = per_inst ? per_inst[i] : cfg->defaults;
     if ((rc = validate_params(ip[i], i))) return rc;
@@ -177,6 +178,7 @@ int augsched_create(const augsched_config* cfg, const augsched_instance_params* 
     if (hi > (double)(1u << 26)) return fail(AUGSCHED_E_INVALID, "instance %u: token limit too large", i);
     const uint32_t lim = ip[i].budget_mode == AUGSCHED_BUDGET_STATIC ? ip[i].l_static : (uint32_t)hi;
     max_limit = lim > max_limit ? lim : max_limit;
+    any_random = any_random || ip[i].ranking == AUGSCHED_RANK_RANDOM;
   }
   int ndev = 0;
   CUDA_TRY(cudaGetDeviceCount(&ndev));
@@ -188,6 +190,7 @@ int augsched_create(const augsched_config* cfg, const augsched_instance_params* 
   h->n_inst = n_instances;
   h->max_active = max_active_per_instance;
   h->st.max_limit = max_limit;
+  h->st.pf_spec = !any_random;   // a fresh shuffle every iteration leaves no anchor
   h->device = device;
   h->stream = reinterpret_cast<cudaStream_t>(cuda_stream);
   h->cap = (int64_t)((cfg->g_total - (cfg->g_model + cfg->g_runtime + cfg->g_safety)) /

@@ -63,6 +63,7 @@ struct Slots {
   const Coef* coef;
   const augsched_instance_params* ip;
   uint32_t MA;
+  uint32_t* wkv;   // sticky: an IMPORT created a KV holder outside running / swapped / Preserve-paused
 };
 
 __device__ __forceinline__ void ledger_add(long long* x, long long d) {
@@ -145,6 +146,7 @@ __global__ void rec_phaseBC(Rec r, uint32_t n, Slots S, uint64_t now, uint32_t* 
   S.last[g] = r.last[j];
   S.ctx[g] = (int32_t)r.ctx[j]; S.kv[g] = (int32_t)r.kv[j]; S.cpu[g] = (int32_t)r.cpu[j];
   S.pend[g] = (int32_t)r.pend[j];
+  if (r.kv[j] > 0 && !(ns == ST_RUN || ns == ST_SWAP || (ns == ST_PAUSED && pol == POL_P))) atomicOr(S.wkv, 1u);
   if (ns == ST_PAUSED && pol == POL_P) ledger_add(&S.P[inst], (long long)r.kv[j]);
   else ledger_add(&S.A[inst], (long long)r.kv[j]);
 }
@@ -162,7 +164,6 @@ struct KeyArgs {
   int npass;
   PassDesc passes[STEP_MAX_PASS];
   uint32_t N;
-  uint32_t* pf_cnt;   // prefix step: [|A|, |C|, b*, below, blocks done]; nullptr otherwise
 };
 
 // Packed sort word of one slot: tier:2 | key:32 | slot:30 (tier 3 = not queued).
@@ -205,9 +206,7 @@ __device__ __forceinline__ void hist_add(uint32_t* h, int d) {
 __global__ void __launch_bounds__(KNT) keys_kernel(KeyArgs a) {
   __shared__ uint32_t h[STEP_HIST_WORDS];
   __shared__ uint32_t qcnt[KCNT];
-  __shared__ uint32_t wsum[KNT / 32];
-  __shared__ uint32_t ticket;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x, lane = tid & 31;
   const int hw = a.passes[a.npass - 1].hoff + (1 << a.passes[a.npass - 1].bits);
   for (int b = tid; b < hw; b += KNT) h[b] = 0;
   for (int b = tid; b < KCNT; b += KNT) qcnt[b] = 0;
@@ -308,38 +307,6 @@ __global__ void __launch_bounds__(KNT) keys_kernel(KeyArgs a) {
   if (local_cnt)
     for (uint32_t b = tid; b <= (c1 - 1) / MA - i0; b += KNT)
       if (qcnt[b]) atomicAdd(&a.n_active[i0 + b], qcnt[b]);
-  if (!a.pf_cnt) return;
-  // prefix step: the last block locates the bucket b* of the top digit that
-  // holds the target-th smallest entry (target = min(B, queued))
-  __threadfence();
-  __syncthreads();
-  if (tid == 0) ticket = atomicAdd(&a.pf_cnt[4], 1u);
-  __syncthreads();
-  if (ticket != gridDim.x - 1) return;
-  __threadfence();
-  constexpr int NB = 1 << PF_BITS, PER = NB / KNT;
-  const long long B = ld_ll(a.budget);
-  const uint32_t nq = __ldcg(&a.n_active[0]);
-  const uint32_t target = B <= 0 ? 0u : ((unsigned long long)B < nq ? (uint32_t)B : nq);
-  uint32_t loc[PER], sum = 0;
-#pragma unroll
-  for (int j = 0; j < PER; ++j) { loc[j] = __ldcg(&a.ghist[tid * PER + j]); sum += loc[j]; }
-  uint32_t inc = sum;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t y = __shfl_up_sync(FULL, inc, o);
-    if (lane >= o) inc += y;
-  }
-  if (lane == 31) wsum[warp] = inc;
-  if (tid == 0) { a.pf_cnt[2] = NB; a.pf_cnt[3] = 0; }
-  __syncthreads();
-  uint32_t run = inc - sum;
-  for (int w = 0; w < warp; ++w) run += wsum[w];
-#pragma unroll
-  for (int j = 0; j < PER; ++j) {
-    if (target > 0 && run < target && run + loc[j] >= target) { a.pf_cnt[2] = tid * PER + j; a.pf_cnt[3] = run; }
-    run += loc[j];
-  }
 }
 
 // ------------------------------------------------------------------ sort pass
@@ -523,6 +490,8 @@ template <int NT>
 __device__ __forceinline__ unsigned long long block_incl_scan_u64(unsigned long long x,
                                                                   unsigned long long* wsum,
                                                                   unsigned long long* total) {
+  // warp scans, then warp 0 scans the warp totals (wsum holds NT/32 + 1 words:
+  // exclusive warp offsets and the block total)
   constexpr int NW = NT / 32;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   unsigned long long inc = x;
@@ -533,13 +502,20 @@ __device__ __forceinline__ unsigned long long block_incl_scan_u64(unsigned long 
   }
   if (lane == 31) wsum[warp] = inc;
   __syncthreads();
-  unsigned long long base = 0, tot = 0;
-  for (int w = 0; w < NW; ++w) {
-    const unsigned long long v = wsum[w];
-    if (w < warp) base += v;
-    tot += v;
+  if (warp == 0) {
+    const unsigned long long t = lane < NW ? wsum[lane] : 0ull;
+    unsigned long long c = t;
+#pragma unroll
+    for (int o = 1; o < NW; o <<= 1) {
+      const unsigned long long y = __shfl_up_sync(FULL, c, o);
+      if (lane >= o) c += y;
+    }
+    if (lane < NW) wsum[lane] = c - t;
+    if (lane == NW - 1) wsum[NW] = c;
   }
-  *total = tot;
+  __syncthreads();
+  const unsigned long long base = wsum[warp];
+  *total = wsum[NW];
   __syncthreads();
   return base + inc;
 }
@@ -562,7 +538,7 @@ __global__ void __launch_bounds__(ANT) admit_kernel(Slots S, augsched_config cfg
                                                     const long long* budget, const uint32_t* n_active,
                                                     const uint32_t* order, uint32_t* grant,
                                                     uint32_t* admitted) {
-  __shared__ unsigned long long wsum[ANW];
+  __shared__ unsigned long long wsum[ANW + 1];
   __shared__ SelShm sel;
   __shared__ unsigned long long freed;
   const uint32_t i = blockIdx.x;
@@ -684,57 +660,65 @@ __global__ void __launch_bounds__(ANT) admit_kernel(Slots S, augsched_config cfg
 // ====================================================================== prefix step
 // augsched_step_prefix: the same decision round, producing the order only
 // for the admitted prefix.  Every queued request has demand >= 1, so the
-// admitted prefix lies within the first min(B, n) entries of the order; it
-// is found by a count-based selection instead of a full sort:
-//   keys_kernel   packed words + histogram of the top 12-bit digit
-//   pf_collect    every block locates the bucket b* holding the target-th
-//                 entry; words below b* -> A (< target of them), in b* -> C
-//   pf_admit      one block: the (target - |A|) smallest of C by a weighted
-//                 radix select (weights 1), bitonic sort of the prefix in
-//                 shared memory, admission (R17), resolution (R20, exact:
-//                 selections over all slots), grant accounting.
+// admitted prefix lies within the first min(B, n) entries of the order
+// (target = min(B, n)); it is found by selection instead of a full sort.
+//
+// Single-instance handle: one cooperative kernel (pf_step_kernel), one CTA
+// of 1,024 threads per SM.
+//   phase 1  (speculative) one streaming pass over the slots: packed word
+//            of every slot (Eq.26 key), queue size, and every word <= theta
+//            appended to a candidate list.  theta is the current word of an
+//            anchor slot chosen by the previous step a margin beyond its
+//            admitted prefix: every unscheduled score falls by the same
+//            alpha*T per iteration (Eq.26), so the anchor keeps about the
+//            same rank and the list holds about target + margin words.
+//            Exact whenever target <= |list| <= PF_SCAP: the target
+//            smallest words are then all <= theta.  The last CTA checks
+//            that and, if it holds, finishes the step alone.
+//   phase 2  (fallback: first step, a random shuffle, records that moved
+//            the anchor, ...) packed words to k0 + histogram of the top
+//            12-bit digit; the last CTA locates the bucket b* of the
+//            target-th word;
+//   phase 3  words below b* -> A (< target of them), in b* -> C; the last
+//            CTA selects the smallest of C and finishes.
+//   finish   bitonic sort of the candidates in shared memory, admission
+//            (R17), resolution (R20, exact selections over all slots),
+//            grant accounting, and the next anchor.
+// Multi-instance handles: pf_multi_kernel (one CTA per instance).
 
 __device__ __forceinline__ uint32_t pf_target(long long B, uint32_t n) {
   if (B <= 0) return 0u;
   return (unsigned long long)B < n ? (uint32_t)B : n;
 }
 
-__global__ void __launch_bounds__(KNT) pf_collect_kernel(const unsigned long long* k0, uint32_t N,
-                                                         uint32_t* cnt, unsigned long long* A,
-                                                         unsigned long long* C) {
-  const int tid = threadIdx.x, lane = tid & 31;
-  constexpr int NB = 1 << PF_BITS;
-  const uint32_t bstar = cnt[2];   // written by the last keys_kernel block
-  if (bstar >= NB) return;         // nothing to admit
-  const unsigned lt = (1u << lane) - 1;
-  for (uint32_t base = blockIdx.x * KNT * KU; base < N; base += gridDim.x * KNT * KU) {
-    unsigned long long x[KU];
-#pragma unroll
-    for (int u = 0; u < KU; ++u) {
-      const uint32_t s = base + u * KNT + tid;
-      x[u] = s < N ? k0[s] : ~0ull;
-    }
-#pragma unroll
-    for (int u = 0; u < KU; ++u) {
-      const uint32_t d = (uint32_t)(x[u] >> (64 - PF_BITS));
-      const bool queued = (x[u] >> PK_TIER) < 3;
-      const bool inA = queued && d < bstar, inC = queued && d == bstar;
-      const unsigned ma = __ballot_sync(FULL, inA), mc = __ballot_sync(FULL, inC);
-      if (!(ma | mc)) continue;
-      uint32_t ba = 0, bc = 0;
-      if (lane == 0) {
-        if (ma) ba = atomicAdd(&cnt[0], (unsigned)__popc(ma));
-        if (mc) bc = atomicAdd(&cnt[1], (unsigned)__popc(mc));
-      }
-      ba = __shfl_sync(FULL, ba, 0);
-      bc = __shfl_sync(FULL, bc, 0);
-      if (inA) A[ba + __popc(ma & lt)] = x[u];
-      if (inC) C[bc + __popc(mc & lt)] = x[u];
-    }
-  }
+// Packed word of local slot x of an instance (tier 3 = not queued).
+__device__ __forceinline__ unsigned long long slot_word(const Coef& k, const augsched_instance_params& ip,
+                                                        uint32_t stv, double V, uint32_t last, uint64_t now,
+                                                        uint32_t x) {
+  stv &= 15;
+  const uint32_t tier = (stv >= ST_RUN && stv <= ST_WAIT) ? stv - ST_RUN : 3u;
+  const uint32_t key = tier < 3 ? rank_key(k, ip, V, now, last, x) : 0u;
+  return ((unsigned long long)tier << PK_TIER) | ((unsigned long long)key << PK_KEY) | x;
 }
 
+#ifdef AUGSCHED_PF_TIMING
+// phase timestamps of the prefix-step kernel (profiling builds only)
+__device__ unsigned long long g_pf_t[8];
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define PF_T(i, first) do { if (threadIdx.x == 0) { if (first) atomicMin(&g_pf_t[i], gtime()); else atomicMax(&g_pf_t[i], gtime()); } } while (0)
+#else
+#define PF_T(i, first) do {} while (0)
+#endif
+
 constexpr int PNT = 1024;
+#ifndef AUGSCHED_PF_SORT_E
+#define AUGSCHED_PF_SORT_E 4
+#endif
+constexpr int PF_SORT_E = AUGSCHED_PF_SORT_E;   // elements per sorting thread (the sort's thread count follows)
 
 // The admitted prefix of instance `inst` from `mt` candidate words in sbuf
 // (which hold its first `target` order entries): bitonic sort, admission
@@ -742,84 +726,142 @@ constexpr int PNT = 1024;
 // grant accounting.  `keys` are the instance's packed words (local slot in
 // the low bits; tier 3 = not queued); `xch` is a second buffer of the same
 // size as sbuf for the sort's shared-memory exchanges.
+__device__ __forceinline__ void bar_named(uint32_t nthreads) {
+  asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
+}
+
+// Bitonic sort of 2^LOGP words, one per thread (threads 0 .. 2^LOGP - 1),
+// the network fully unrolled: partner distances below 32 by warp shuffles,
+// the others through a double-buffered shared exchange.
+template <int LOGP>
+__device__ __forceinline__ unsigned long long bitonic1(unsigned long long v, unsigned long long* b0,
+                                                       unsigned long long* b1) {
+  constexpr uint32_t P = 1u << LOGP;
+  const uint32_t t = threadIdx.x;
+  int xp = 0;
+#pragma unroll
+  for (int lk = 1; lk <= LOGP; ++lk) {
+#pragma unroll
+    for (int lj = lk - 1; lj >= 0; --lj) {
+      const uint32_t k = 1u << lk, j = 1u << lj;
+      unsigned long long pv;
+      if (j < 32) {
+        pv = __shfl_xor_sync(FULL, v, j);
+      } else {
+        unsigned long long* xb = xp ? b1 : b0;
+        xp ^= 1;
+        xb[t] = v;
+        bar_named(P);
+        pv = xb[t ^ j];
+      }
+      const bool keep_min = ((t & j) == 0) == ((t & k) == 0);
+      const bool lt = pv < v;
+      v = (keep_min == lt) ? pv : v;
+    }
+  }
+  return v;
+}
+
 template <int NT, int EM>
 __device__ void pf_finish(const Slots& S, const augsched_config& cfg, int64_t cap, uint64_t now, uint32_t inst,
                           size_t base, const unsigned long long* keys, unsigned long long* sbuf,
                           unsigned long long* xch, uint32_t mt, uint32_t target, long long B, uint32_t* order,
                           uint32_t* keyout, uint32_t* grant, uint32_t* admitted, uint32_t* gslot, SelShm& sel,
-                          unsigned long long* wsum, unsigned long long& freed) {
+                          unsigned long long* wsum, unsigned long long& freed,
+                          const unsigned long long* H = nullptr, uint32_t nH = 0) {
   const int tid = threadIdx.x;
   const uint32_t MA = S.MA;
-  // ---- bitonic sort of the prefix (padded to a power of two).  Each thread
-  // holds E = P2 / NT elements (index tid + e * NT) in registers: partner
-  // distances j < 32 exchange by warp shuffles, j >= NT inside the thread,
-  // and only 32 <= j < NT goes through shared memory (double-buffered, one
-  // barrier per stage).
+  // ---- bitonic sort of the prefix (padded to a power of two P2) by the
+  // first ST threads, ST = P2 / E (E elements per thread, at most EMAX; at
+  // least one warp): a bitonic network does P2 log^2 P2 / 4 compare-exchanges
+  // whatever the thread count, but every partner outside the thread is
+  // evaluated twice, so few threads with many elements each issue the fewest
+  // instructions.  Thread t holds indices t + e * ST: partner distances
+  // j < 32 exchange by warp shuffles, j >= ST inside the thread, and only
+  // 32 <= j < ST through shared memory (double-buffered, one named barrier
+  // over the ST threads per stage).
   uint32_t P2 = 1;
   while (P2 < mt) P2 <<= 1;
   if (P2 < 32) P2 = 32;
-  constexpr int EMAX = EM;
-  const uint32_t E = P2 > NT ? P2 / NT : 1u;
-  unsigned long long v[EMAX];
+  constexpr int EMAX = EM < PF_SORT_E ? EM : PF_SORT_E;
+  const uint32_t ST = P2 / EMAX > 32 ? (P2 / EMAX < (uint32_t)NT ? P2 / EMAX : (uint32_t)NT) : 32u;
+  const uint32_t E = P2 / ST;
+  if (P2 <= (uint32_t)NT && P2 <= 1024u) {
+    // one word per thread: the unrolled network
+    if ((uint32_t)tid < P2) {
+      unsigned long long v = (uint32_t)tid < mt ? sbuf[tid] : ~0ull;
+      bar_named(P2);
+      switch (P2) {
+        case 32: v = bitonic1<5>(v, sbuf, xch); break;
+        case 64: v = bitonic1<6>(v, sbuf, xch); break;
+        case 128: v = bitonic1<7>(v, sbuf, xch); break;
+        case 256: v = bitonic1<8>(v, sbuf, xch); break;
+        case 512: v = bitonic1<9>(v, sbuf, xch); break;
+        default: v = bitonic1<10>(v, sbuf, xch); break;
+      }
+      bar_named(P2);
+      sbuf[tid] = v;
+    }
+  } else if ((uint32_t)tid < ST) {
+    unsigned long long v[EMAX];
 #pragma unroll
-  for (int e = 0; e < EMAX; ++e) {
-    const uint32_t idx = tid + e * NT;
-    v[e] = (e < (int)E && idx < mt) ? sbuf[idx] : ~0ull;
-  }
-  __syncthreads();
-  int xp = 0;
-  for (uint32_t k = 2; k <= P2; k <<= 1) {
-    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
-      if (j < 32) {
-#pragma unroll
-        for (int e = 0; e < EMAX; ++e) {
-          if (e >= (int)E) break;
-          const unsigned long long pv = __shfl_xor_sync(FULL, v[e], j);
-          const uint32_t idx = tid + e * NT;
-          const bool keep_min = ((idx & j) == 0) == ((idx & k) == 0);
-          v[e] = keep_min ? (pv < v[e] ? pv : v[e]) : (pv > v[e] ? pv : v[e]);
-        }
-      } else if (j < NT) {
-        unsigned long long* xbuf = xp ? xch : sbuf;
-        xp ^= 1;
-#pragma unroll
-        for (int e = 0; e < EMAX; ++e)
-          if (e < (int)E && tid + e * NT < P2) xbuf[tid + e * NT] = v[e];
-        __syncthreads();
-#pragma unroll
-        for (int e = 0; e < EMAX; ++e) {
-          if (e >= (int)E) break;
-          const uint32_t idx = tid + e * NT;
-          if (idx >= P2) continue;
-          const unsigned long long pv = xbuf[idx ^ j];
-          const bool keep_min = ((idx & j) == 0) == ((idx & k) == 0);
-          v[e] = keep_min ? (pv < v[e] ? pv : v[e]) : (pv > v[e] ? pv : v[e]);
-        }
-      } else {
-        // partner inside the thread: e ^ (j / NT), unrolled so v stays in registers
-#pragma unroll
-        for (int bsh = 0; (1 << bsh) < EMAX; ++bsh) {
-          if (j != ((uint32_t)NT << bsh)) continue;
+    for (int e = 0; e < EMAX; ++e) {
+      const uint32_t idx = tid + e * ST;
+      v[e] = (e < (int)E && idx < mt) ? sbuf[idx] : ~0ull;
+    }
+    asm volatile("bar.sync 1, %0;" ::"r"(ST) : "memory");
+    int xp = 0;
+    for (uint32_t k = 2; k <= P2; k <<= 1) {
+      for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+        if (j < 32) {
 #pragma unroll
           for (int e = 0; e < EMAX; ++e) {
-            const int e2 = e ^ (1 << bsh);
-            if (e2 <= e || e2 >= (int)E) continue;
-            const uint32_t idx = tid + e * NT;
-            const bool up = (idx & k) == 0;
-            const unsigned long long x0 = v[e], x1 = v[e2];
-            if ((x0 > x1) == up) { v[e] = x1; v[e2] = x0; }
+            if (e >= (int)E) break;
+            const unsigned long long pv = __shfl_xor_sync(FULL, v[e], j);
+            const uint32_t idx = tid + e * ST;
+            const bool keep_min = ((idx & j) == 0) == ((idx & k) == 0);
+            v[e] = keep_min ? (pv < v[e] ? pv : v[e]) : (pv > v[e] ? pv : v[e]);
+          }
+        } else if (j < ST) {
+          unsigned long long* xbuf = xp ? xch : sbuf;
+          xp ^= 1;
+#pragma unroll
+          for (int e = 0; e < EMAX; ++e)
+            if (e < (int)E) xbuf[tid + e * ST] = v[e];
+          asm volatile("bar.sync 1, %0;" ::"r"(ST) : "memory");
+#pragma unroll
+          for (int e = 0; e < EMAX; ++e) {
+            if (e >= (int)E) break;
+            const uint32_t idx = tid + e * ST;
+            const unsigned long long pv = xbuf[idx ^ j];
+            const bool keep_min = ((idx & j) == 0) == ((idx & k) == 0);
+            v[e] = keep_min ? (pv < v[e] ? pv : v[e]) : (pv > v[e] ? pv : v[e]);
+          }
+        } else {
+          // partner inside the thread: e ^ (j / ST), unrolled so v stays in registers
+#pragma unroll
+          for (int bsh = 0; (1 << bsh) < EMAX; ++bsh) {
+            if (j != (ST << bsh)) continue;
+#pragma unroll
+            for (int e = 0; e < EMAX; ++e) {
+              const int e2 = e ^ (1 << bsh);
+              if (e2 <= e || e2 >= (int)E) continue;
+              const uint32_t idx = tid + e * ST;
+              const bool up = (idx & k) == 0;
+              const unsigned long long x0 = v[e], x1 = v[e2];
+              if ((x0 > x1) == up) { v[e] = x1; v[e2] = x0; }
+            }
           }
         }
       }
     }
-  }
-  __syncthreads();
+    asm volatile("bar.sync 1, %0;" ::"r"(ST) : "memory");
 #pragma unroll
-  for (int e = 0; e < EMAX; ++e) {
-    const uint32_t idx = tid + e * NT;
-    if (e < (int)E && idx < P2) sbuf[idx] = v[e];
+    for (int e = 0; e < EMAX; ++e)
+      if (e < (int)E) sbuf[tid + e * ST] = v[e];
   }
   __syncthreads();
+  PF_T(4, false);
   const uint32_t m = target;
   // ---- a6 admission over the prefix (P_{j-1} < B, partial last, R17)
   unsigned long long Prun = 0, gsum = 0;
@@ -834,6 +876,7 @@ __device__ void pf_finish(const Slots& S, const augsched_config& cfg, int64_t ca
     }
     unsigned long long tot;
     const unsigned long long inc = block_incl_scan_u64<NT>(d, wsum, &tot);
+    PF_T(7, false);
     const unsigned long long ex = Prun + inc - d;
     const bool in = j < m && (long long)ex < B;
     if (in) {
@@ -849,11 +892,24 @@ __device__ void pf_finish(const Slots& S, const augsched_config& cfg, int64_t ca
   }
   unsigned long long need;
   block_incl_scan_u64<NT>(gsum, wsum, &need);
+  PF_T(5, false);
   long long fr = cap - ld_ll(&S.A[inst]) - ld_ll(&S.P[inst]);
-  // ---- a7 resolution (rare; exact selections over every slot)
+  // ---- a7 resolution (rare).  Candidates: every slot of the instance, or,
+  // with the holder list H (single-instance prefix step), the slots that can
+  // hold KV: H's running / swapped words, H's Preserve-paused slots (tier-3
+  // words) and the granted waiting entries of the prefix.  Both index sets
+  // give the same candidate sets, so the same selections.
   if ((long long)need > fr) {
     if (tid == 0) freed = 0;
-    auto getp = [&](uint32_t x, uint64_t& key, uint32_t& w) {
+    auto pslot = [&](uint32_t i, uint32_t& x) -> bool {
+      if (!H) { x = i; return true; }
+      const unsigned long long hx = H[i];
+      x = (uint32_t)hx & SLOT_MASK;
+      return (hx >> PK_TIER) == 3;
+    };
+    auto getp = [&](uint32_t i, uint64_t& key, uint32_t& w) {
+      uint32_t x;
+      if (!pslot(i, x)) return false;
       const uint32_t stv = S.st[base + x];
       const int32_t kv = S.kv[base + x];
       if ((stv & 15) != ST_PAUSED || ((stv >> 4) & 3) != POL_P || kv <= 0) return false;
@@ -861,14 +917,16 @@ __device__ void pf_finish(const Slots& S, const augsched_config& cfg, int64_t ca
       w = (uint32_t)kv;
       return true;
     };
-    wselect<NT>(sel, MA, (uint64_t)((long long)need - fr), 56, getp);
+    const uint32_t np = H ? nH : MA;
+    wselect<NT>(sel, np, (uint64_t)((long long)need - fr), 56, getp);
     {
       const bool f0 = sel.r.found != 0;
       const uint64_t kd = sel.r.k;
-      for (uint32_t x = tid; x < MA; x += NT) {
+      for (uint32_t i = tid; i < np; i += NT) {
         uint64_t key;
         uint32_t w;
-        if (getp(x, key, w) && (!f0 || key <= kd)) {
+        if (getp(i, key, w) && (!f0 || key <= kd)) {
+          const uint32_t x = (uint32_t)key & 0xFFFFFFu;
           atomicAdd(&freed, (unsigned long long)w);
           S.kv[base + x] = 0;
           S.st[base + x] = ST_PAUSED | ((uint32_t)POL_D << 4);
@@ -880,23 +938,36 @@ __device__ void pf_finish(const Slots& S, const augsched_config& cfg, int64_t ca
     fr += (long long)freed;
     if ((long long)need > fr) {
       // from the tail of the order over queued entries with kv + g > 0
-      auto gete = [&](uint32_t x, uint64_t& key, uint32_t& w) {
-        const unsigned long long kx = keys[x];
-        if ((kx >> PK_TIER) >= 3) return false;
+      auto eword = [&](uint32_t v, unsigned long long& kx) -> bool {
+        if (H) {
+          if (v < nH) { kx = H[v]; return (kx >> PK_TIER) < 3; }
+          kx = sbuf[v - nH];           // granted entries; the running / swapped ones are in H
+          return (kx >> PK_TIER) == 2;
+        }
+        kx = keys ? keys[v]
+                  : slot_word(S.coef[inst], S.ip[inst], S.st[base + v], S.V[base + v], S.last[base + v], now, v);
+        return (kx >> PK_TIER) < 3;
+      };
+      auto gete = [&](uint32_t v, uint64_t& key, uint32_t& w) {
+        unsigned long long kx;
+        if (!eword(v, kx)) return false;
+        const uint32_t x = (uint32_t)kx & SLOT_MASK;
         const uint32_t g = gslot[base + x];
         w = (uint32_t)S.kv[base + x] + (g == 0xFFFFFFFFu ? 0u : g);
         key = ~kx;
         return w > 0;
       };
-      wselect<NT>(sel, MA, (uint64_t)((long long)need - fr), 64, gete);
+      const uint32_t ne = H ? nH + adm : MA;
+      wselect<NT>(sel, ne, (uint64_t)((long long)need - fr), 64, gete);
       const bool f1 = sel.r.found != 0;
       const uint64_t k1 = sel.r.k;
       __syncthreads();
       long long dA = 0;
-      for (uint32_t x = tid; x < MA; x += NT) {
+      for (uint32_t v = tid; v < ne; v += NT) {
         uint64_t key;
         uint32_t w;
-        if (gete(x, key, w) && (!f1 || key <= k1)) {
+        if (gete(v, key, w) && (!f1 || key <= k1)) {
+          const uint32_t x = (uint32_t)~key & SLOT_MASK;
           dA -= S.kv[base + x];
           S.kv[base + x] = 0;
           S.cpu[base + x] = 0;
@@ -911,6 +982,7 @@ __device__ void pf_finish(const Slots& S, const augsched_config& cfg, int64_t ca
     }
   }
   __syncthreads();
+  PF_T(6, false);
   // ---- S9 + token accounting of the granted batch
   unsigned long long dA = 0;
   for (uint32_t j = tid; j < adm; j += NT) {
@@ -941,49 +1013,379 @@ __device__ void pf_finish(const Slots& S, const augsched_config& cfg, int64_t ca
   }
 }
 
-template <int NT, int EM>
-__global__ void __launch_bounds__(NT) pf_admit_kernel(Slots S, augsched_config cfg, int64_t cap, uint64_t now,
-                                                       const long long* budget, const uint32_t* n_active,
-                                                       const unsigned long long* k0,
-                                                       const unsigned long long* A,
-                                                       const unsigned long long* C, const uint32_t* cnt,
-                                                       uint32_t* order, uint32_t* keyout, uint32_t* grant,
-                                                       uint32_t* admitted, uint32_t* gslot) {
+// ---- single-instance prefix step (see the comment above pf_target)
+enum : int {
+  PC_A = 0, PC_C, PC_BSTAR, PC_BELOW, PC_SPEC, PC_ARR1, PC_STATE, PC_ARR2, PC_REL2, PC_ARR3, PC_TARGET, PC_H,
+  PF_NCNT = 16
+};
+constexpr uint32_t PF_HCAP = 65536;   // holder-list capacity (running, swapped, Preserve-paused slots)
+constexpr int FNT = 1024;   // threads per CTA
+#ifndef AUGSCHED_PF_KU
+#define AUGSCHED_PF_KU 8
+#endif
+constexpr int FKU = AUGSCHED_PF_KU;   // slots in flight per thread
+
+struct PfArgs {
+  Slots S;
+  augsched_config cfg;
+  int64_t cap;
+  uint64_t now;
+  uint32_t N;
+  int spec;                       // 1: phase 1 (speculative pass) first
+  unsigned long long* k0;         // [N] packed words (fallback)
+  unsigned long long* A;          // [PF_SCAP] phase-1 candidates, then words below b*
+  unsigned long long* C;          // [N] words in b*
+  unsigned long long* theta;      // [2] anchor word, anchor slot (kept across steps)
+  unsigned long long* H;          // [PF_HCAP] words of the slots that can hold KV (resolution candidates)
+  uint32_t* ghist;                // [1 << PF_BITS]
+  uint32_t* cnt;                  // [PF_NCNT], zeroed every step
+  uint32_t* n_active;
+  long long* budget;
+  uint32_t *order, *keyout, *grant, *admitted, *gslot;
+};
+
+__device__ __forceinline__ uint32_t vld(const uint32_t* p) { return *(volatile const uint32_t*)p; }
+__device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+
+// candidates kept beyond the prefix for the next step's anchor
+__device__ __forceinline__ uint32_t pf_margin(uint32_t target) { return target / 2 > 256u ? target / 2 : 256u; }
+
+// Arrive at a grid-wide counter; true in the CTA that arrives last.  The
+// caller's global writes are visible to that CTA.
+__device__ __forceinline__ bool pf_arrive_last(uint32_t* ctr, uint32_t G, uint32_t& flag) {
+  __syncthreads();   // the CTA's writes happen before thread 0's release (cumulative fence)
+  if (threadIdx.x == 0) {
+    __threadfence();
+    flag = atomicAdd(ctr, 1u) == G - 1;
+    if (flag) __threadfence();
+  }
+  __syncthreads();
+  return flag != 0;
+}
+
+__device__ __forceinline__ uint32_t pf_wait(const uint32_t* w, uint32_t& flag) {
+  if (threadIdx.x == 0) {
+    uint32_t v;
+    while ((v = vld(w)) == 0) __nanosleep(32);
+    flag = v;
+  }
+  __syncthreads();
+  return flag;
+}
+
+
+__global__ void __launch_bounds__(FNT, 1) pf_step_kernel(const __grid_constant__ PfArgs a) {
   extern __shared__ __align__(16) unsigned long long pf_sm[];
-  unsigned long long* sbuf = pf_sm;              // [2 * PF_SCAP] the prefix + exchange buffer
+  unsigned long long* sbuf = pf_sm;   // [2 * PF_SCAP]: the prefix + the sort's exchange buffer
+  constexpr int NB = 1 << PF_BITS;
+  __shared__ uint32_t h[NB];
   __shared__ SelShm sel;
-  __shared__ unsigned long long wsum[NT / 32];
-  __shared__ unsigned long long freed;
-  __shared__ uint32_t m_s;
-  const int tid = threadIdx.x;
-  const uint32_t MA = S.MA;
-  const long long B = budget[0];
-  const uint32_t target = pf_target(B, n_active[0]);
-  const uint32_t nA = cnt[0], nC = cnt[1];
-  // ---- the first `target` entries of the order: A, plus the smallest of C
-  for (uint32_t i = tid; i < nA; i += NT) sbuf[i] = A[i];
+  __shared__ unsigned long long wsum[FNT / 32 + 1];
+  __shared__ unsigned long long freed, th_s;
+  __shared__ uint32_t m_s, flag_s, q_s;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const uint32_t G = gridDim.x, N = a.N;
+  const Slots& S = a.S;
+  const Coef k = S.coef[0];
+  const augsched_instance_params ip = S.ip[0];
+  const unsigned lt = (1u << lane) - 1;
+  // a contiguous range of slots per CTA (one pass of FKU loads per thread at 1 M slots)
+  const uint32_t chunk = ((N + G - 1) / G + 31) & ~31u;
+  const uint32_t c0 = blockIdx.x * chunk < N ? blockIdx.x * chunk : N;
+  const uint32_t c1 = c0 + chunk < N ? c0 + chunk : N;
+  uint32_t* cnt = a.cnt;
+  PF_T(0, true);
+  PF_T(1, false);
+  __shared__ long long B_s;
+  __shared__ uint32_t tgt_s, nH_s, wkv_s;
+  auto finish = [&](uint32_t mt, const unsigned long long* keys) {
+    const long long B = B_s;
+    const uint32_t target = tgt_s, nH = nH_s;
+    PF_T(3, false);
+    const bool use_h = nH <= PF_HCAP && wkv_s == 0;
+    pf_finish<FNT, PF_SCAP / FNT>(S, a.cfg, a.cap, a.now, 0, 0, keys, sbuf, sbuf + PF_SCAP, mt, target, B,
+                                  a.order, a.keyout, a.grant, a.admitted, a.gslot, sel, wsum, freed,
+                                  use_h ? a.H : nullptr, nH);
+    // next anchor: the K-th smallest word, K a margin beyond the prefix
+    if (tid == 0) {
+      const uint32_t K = target + pf_margin(target) < mt ? target + pf_margin(target) : mt;
+#ifdef AUGSCHED_PF_TIMING
+      const unsigned long long t5 = gtime();
+      printf("pf_t state %u mt %u target %u nH %u K %u | ns: start..%llu arrive %llu finish %llu sorted %llu "
+             "admitted %llu resolved %llu end %llu\n", __ldcg(&cnt[PC_STATE]), mt, target, __ldcg(&cnt[PC_H]), K,
+             g_pf_t[1] - g_pf_t[0], g_pf_t[2] - g_pf_t[0], g_pf_t[3] - g_pf_t[0], g_pf_t[4] - g_pf_t[0],
+             g_pf_t[5] - g_pf_t[0], g_pf_t[6] - g_pf_t[0], t5 - g_pf_t[0]);
+      printf("pf_t gathered+scanned %llu\n", g_pf_t[7] - g_pf_t[0]);
+      g_pf_t[0] = ~0ull;
+      for (int q = 1; q < 8; ++q) g_pf_t[q] = 0;
+#endif
+      a.theta[0] = K > 0 ? sbuf[K - 1] : ~0ull;
+      a.theta[1] = K > 0 ? (sbuf[K - 1] & SLOT_MASK) : ~0ull;
+    }
+  };
+  // slots that can hold KV: running, swapped, Preserve-paused (the
+  // resolution candidates besides the granted waiting entries)
+  auto add_holder = [&](uint32_t stv, unsigned long long w, bool valid) {
+    const uint32_t s4 = stv & 15;
+    const bool hold = valid && (s4 == ST_RUN || s4 == ST_SWAP || (s4 == ST_PAUSED && ((stv >> 4) & 3) == POL_P));
+    const unsigned m = __ballot_sync(FULL, hold);
+    if (m) {
+      const int ld = __ffs(m) - 1;
+      uint32_t b = 0;
+      if (lane == ld) b = atomicAdd(&cnt[PC_H], (unsigned)__popc(m));
+      b = __shfl_sync(FULL, b, ld) + __popc(m & lt);
+      if (hold && b < PF_HCAP) a.H[b] = w;
+    }
+  };
+  auto count_queued = [&](uint32_t myq) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) myq += __shfl_xor_sync(FULL, myq, o);
+    if (tid == 0) q_s = 0;
+    __syncthreads();
+    if (lane == 0 && myq) atomicAdd(&q_s, myq);
+    __syncthreads();
+    if (tid == 0 && q_s) atomicAdd(a.n_active, q_s);
+  };
+  // target = min(B, n) once the queue size is complete (last CTA only)
+  // thread 0 of the deciding CTA: limit, target = min(B, n), holder count
+  // (independent loads issued together)
+  auto set_target = [&]() -> uint32_t {
+    const long long A0 = __ldcg(&S.A[0]), P0 = __ldcg(&S.P[0]);
+    const uint32_t nq = __ldcg(a.n_active), nh = __ldcg(&cnt[PC_H]), wk = __ldcg(S.wkv);
+    const long long B = token_limit(a.cfg, k, ip, a.cap, A0, P0);
+    const uint32_t target = pf_target(B, nq);
+    a.budget[0] = B;
+    cnt[PC_TARGET] = target;
+    B_s = B; tgt_s = target; nH_s = nh; wkv_s = wk;
+    return target;
+  };
+
+  if (a.spec) {
+    // ---- phase 1: speculative pass against the anchor word
+    unsigned long long th = 0;
+    bool have_th = false;
+    uint32_t myq = 0;
+    for (uint32_t b0 = c0; b0 < c1; b0 += FNT * FKU) {   // block-uniform trip count
+      uint32_t stv[FKU], lst[FKU];
+      double V[FKU];
+#pragma unroll
+      for (int u = 0; u < FKU; ++u) {
+        const uint32_t s = b0 + u * FNT + tid;
+        stv[u] = 0u; lst[u] = 0u; V[u] = 0.0;
+        if (s < c1) { stv[u] = S.st[s]; V[u] = S.V[s]; lst[u] = S.last[s]; }
+      }
+      if (!have_th) {
+        // the anchor's current word, fetched while the first loads are in flight
+        if (tid == 0) {
+          unsigned long long t0 = a.theta[0];
+          const unsigned long long sg = a.theta[1];
+          if (sg < N) {
+            const unsigned long long w = slot_word(k, ip, S.st[sg], S.V[sg], S.last[sg], a.now, (uint32_t)sg);
+            if ((w >> PK_TIER) < 3) t0 = w;
+          }
+          th_s = t0;
+        }
+        __syncthreads();
+        th = th_s;
+        have_th = true;
+      }
+      // words, then one atomic per warp and list for all its appends (the
+      // holders and candidates cluster in a few CTAs: per-item atomics would
+      // chain their round trips)
+      unsigned long long wv[FKU];
+      unsigned cm[FKU], hm[FKU];
+      uint32_t nc = 0, nh = 0;
+#pragma unroll
+      for (int u = 0; u < FKU; ++u) {
+        const uint32_t s = b0 + u * FNT + tid;
+        const unsigned long long w = slot_word(k, ip, stv[u], V[u], lst[u], a.now, s);
+        const bool q = s < c1 && (w >> PK_TIER) < 3;
+        const uint32_t s4 = stv[u] & 15;
+        const bool hold = s < c1 && (s4 == ST_RUN || s4 == ST_SWAP ||
+                                     (s4 == ST_PAUSED && ((stv[u] >> 4) & 3) == POL_P));
+        myq += q;
+        wv[u] = w;
+        cm[u] = __ballot_sync(FULL, q && w <= th);
+        hm[u] = __ballot_sync(FULL, hold);
+        nc += __popc(cm[u]);
+        nh += __popc(hm[u]);
+      }
+      if (nc | nh) {
+        uint32_t bc = 0, bh = 0;
+        if (lane == 0) {
+          if (nc) bc = atomicAdd(&cnt[PC_SPEC], nc);
+          if (nh) bh = atomicAdd(&cnt[PC_H], nh);
+        }
+        bc = __shfl_sync(FULL, bc, 0);
+        bh = __shfl_sync(FULL, bh, 0);
+#pragma unroll
+        for (int u = 0; u < FKU; ++u) {
+          const uint32_t s = b0 + u * FNT + tid;
+          if ((cm[u] >> lane) & 1u) {
+            const uint32_t b = bc + __popc(cm[u] & lt);
+            if (b < PF_SCAP) {
+              a.A[b] = wv[u];
+              // the admission reads this slot's token state: start bringing it to L2
+              prefetch_l2(&S.ctx[s]); prefetch_l2(&S.kv[s]); prefetch_l2(&S.cpu[s]); prefetch_l2(&S.pend[s]);
+            }
+          }
+          if ((hm[u] >> lane) & 1u) {
+            const uint32_t b = bh + __popc(hm[u] & lt);
+            if (b < PF_HCAP) a.H[b] = wv[u];
+          }
+          bc += __popc(cm[u]);
+          bh += __popc(hm[u]);
+        }
+      }
+    }
+    count_queued(myq);
+    PF_T(2, false);
+    if (pf_arrive_last(&cnt[PC_ARR1], G, flag_s)) {
+      if (tid == 0) {
+        const uint32_t nc = __ldcg(&cnt[PC_SPEC]);
+        const uint32_t target = set_target();
+        const bool ok = target == 0 || (nc >= target && nc <= PF_SCAP);
+        m_s = ok ? (target == 0 ? 0u : nc) : 0xFFFFFFFFu;
+        __threadfence();
+        atomicExch(&cnt[PC_STATE], ok ? 1u : 2u);
+      }
+      __syncthreads();
+      const uint32_t mt = m_s;
+      if (mt != 0xFFFFFFFFu) {
+        for (uint32_t i = tid; i < mt; i += FNT) sbuf[i] = __ldcg(&a.A[i]);
+        __syncthreads();
+        finish(mt, nullptr);
+        return;
+      }
+    } else if (pf_wait(&cnt[PC_STATE], flag_s) == 1) {
+      return;
+    }
+  }
+  // ---- phase 2: packed words + histogram of the top digit
+  for (int b = tid; b < NB; b += FNT) h[b] = 0;
+  __syncthreads();
+  {
+    uint32_t myq = 0;
+    for (uint32_t b0 = c0; b0 < c1; b0 += FNT * FKU) {
+      uint32_t stv[FKU], lst[FKU];
+      double V[FKU];
+#pragma unroll
+      for (int u = 0; u < FKU; ++u) {
+        const uint32_t s = b0 + u * FNT + tid;
+        stv[u] = 0u; lst[u] = 0u; V[u] = 0.0;
+        if (s < c1) { stv[u] = S.st[s]; V[u] = S.V[s]; lst[u] = S.last[s]; }
+      }
+#pragma unroll
+      for (int u = 0; u < FKU; ++u) {
+        const uint32_t s = b0 + u * FNT + tid;
+        const unsigned long long w = slot_word(k, ip, stv[u], V[u], lst[u], a.now, s);
+        const bool q = s < c1 && (w >> PK_TIER) < 3;
+        if (s < c1) a.k0[s] = w;
+        if (!a.spec) add_holder(stv[u], w, s < c1);
+        myq += q;
+        hist_add(h, q ? (int)(w >> (64 - PF_BITS)) : -1);
+      }
+    }
+    __syncthreads();
+    for (int b = tid; b < NB; b += FNT)
+      if (h[b]) atomicAdd(&a.ghist[b], h[b]);
+    if (!a.spec) count_queued(myq);
+  }
+  if (pf_arrive_last(&cnt[PC_ARR2], G, flag_s)) {
+    // locate b*: the bucket holding the target-th word
+    __shared__ uint32_t tgt2_s, wtot[FNT / 32];
+    if (tid == 0) tgt2_s = a.spec ? __ldcg(&cnt[PC_TARGET]) : set_target();
+    __syncthreads();
+    const uint32_t target = tgt2_s;
+    constexpr int PER = NB / FNT;
+    uint32_t loc[PER], sum = 0;
+#pragma unroll
+    for (int j = 0; j < PER; ++j) { loc[j] = __ldcg(&a.ghist[tid * PER + j]); sum += loc[j]; }
+    uint32_t inc = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(FULL, inc, o);
+      if (lane >= o) inc += y;
+    }
+    if (lane == 31) wtot[tid >> 5] = inc;
+    if (tid == 0) { cnt[PC_BSTAR] = NB; cnt[PC_BELOW] = 0; }
+    __syncthreads();
+    uint32_t run = inc - sum;
+    for (int w = 0; w < (tid >> 5); ++w) run += wtot[w];
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+      if (target > 0 && run < target && run + loc[j] >= target) { cnt[PC_BSTAR] = tid * PER + j; cnt[PC_BELOW] = run; }
+      run += loc[j];
+    }
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) atomicExch(&cnt[PC_REL2], 1u);
+  } else {
+    pf_wait(&cnt[PC_REL2], flag_s);
+  }
+  // ---- phase 3: words below b* -> A, in b* -> C
+  const uint32_t bstar = __ldcg(&cnt[PC_BSTAR]);
+  if (bstar < NB) {
+    for (uint32_t b0 = c0; b0 < c1; b0 += FNT * FKU) {
+      unsigned long long x[FKU];
+#pragma unroll
+      for (int u = 0; u < FKU; ++u) {
+        const uint32_t s = b0 + u * FNT + tid;
+        x[u] = s < c1 ? __ldcg(&a.k0[s]) : ~0ull;
+      }
+#pragma unroll
+      for (int u = 0; u < FKU; ++u) {
+        const uint32_t d = (uint32_t)(x[u] >> (64 - PF_BITS));
+        const bool queued = (x[u] >> PK_TIER) < 3;
+        const bool inA = queued && d < bstar, inC = queued && d == bstar;
+        const unsigned ma = __ballot_sync(FULL, inA), mc = __ballot_sync(FULL, inC);
+        if (!(ma | mc)) continue;
+        uint32_t ba = 0, bc = 0;
+        if (lane == 0) {
+          if (ma) ba = atomicAdd(&cnt[PC_A], (unsigned)__popc(ma));
+          if (mc) bc = atomicAdd(&cnt[PC_C], (unsigned)__popc(mc));
+        }
+        ba = __shfl_sync(FULL, ba, 0);
+        bc = __shfl_sync(FULL, bc, 0);
+        if (inA) a.A[ba + __popc(ma & lt)] = x[u];
+        if (inC) a.C[bc + __popc(mc & lt)] = x[u];
+      }
+    }
+  }
+  if (!pf_arrive_last(&cnt[PC_ARR3], G, flag_s)) return;
+  // ---- the last CTA: the first `target` words (+ a margin) and the finish
+  if (tid == 0) {
+    const uint32_t nq = __ldcg(a.n_active), nh = __ldcg(&cnt[PC_H]), wk = __ldcg(S.wkv);
+    const long long B = ld_ll(a.budget);
+    B_s = B; tgt_s = pf_target(B, nq); nH_s = nh; wkv_s = wk;
+  }
+  __syncthreads();
+  const uint32_t target = tgt_s;
+  const uint32_t nA = __ldcg(&cnt[PC_A]), nC = __ldcg(&cnt[PC_C]);
+  for (uint32_t i = tid; i < nA; i += FNT) sbuf[i] = __ldcg(&a.A[i]);
   if (tid == 0) m_s = nA;
-  const uint32_t needC = target > nA ? target - nA : 0u;
+  uint32_t needC = target > nA ? target - nA : 0u;
   if (needC > 0 && nA + nC <= PF_SCAP) {
-    // the whole crossing bucket fits beside A: sort them all, keep `target`
-    for (uint32_t i = tid; i < nC; i += NT) sbuf[nA + i] = C[i];
+    // the whole crossing bucket fits beside A
+    for (uint32_t i = tid; i < nC; i += FNT) sbuf[nA + i] = __ldcg(&a.C[i]);
     if (tid == 0) m_s = nA + nC;
   } else if (needC > 0) {
-    // large crossing bucket: select its (target - |A|) smallest in place
-    const unsigned long long* cb = C;
+    // large crossing bucket: its needC (+ margin) smallest
+    needC += pf_margin(target);
+    needC = needC < nC ? needC : nC;
+    needC = needC < PF_SCAP - nA ? needC : PF_SCAP - nA;
+    const unsigned long long* cb = a.C;
     __syncthreads();
-    wselect<NT>(sel, nC, needC, 64, [&](uint32_t i, uint64_t& key, uint32_t& w) {
-      key = cb[i]; w = 1u; return true; });
+    wselect<FNT>(sel, nC, needC, 64, [&](uint32_t i, uint64_t& key, uint32_t& w) {
+      key = __ldcg(&cb[i]); w = 1u; return true; });
     const unsigned long long tau = sel.r.found ? sel.r.k : ~0ull;
-    for (uint32_t i = tid; i < nC; i += NT) {
-      const unsigned long long x = cb[i];
+    for (uint32_t i = tid; i < nC; i += FNT) {
+      const unsigned long long x = __ldcg(&cb[i]);
       if (x <= tau) sbuf[atomicAdd(&m_s, 1u)] = x;
     }
   }
   __syncthreads();
-  const uint32_t mt = m_s;  // >= target entries, the first `target` of the order among them
-  pf_finish<NT, EM>(S, cfg, cap, now, 0, 0, k0, sbuf, sbuf + PF_SCAP, mt, target, B, order, keyout,
-                    grant, admitted, gslot, sel, wsum, freed);
+  finish(m_s, a.k0);
 }
 
 
@@ -1001,7 +1403,7 @@ __global__ void __launch_bounds__(NT) pf_multi_kernel(Slots S, augsched_config c
   unsigned long long* sbuf = pf_sm + MA;        // [sbuf_cap] the prefix
   unsigned long long* xch = sbuf + sbuf_cap;    // [sbuf_cap] sort exchange buffer
   __shared__ SelShm sel;
-  __shared__ unsigned long long wsum[NT / 32];
+  __shared__ unsigned long long wsum[NT / 32 + 1];
   __shared__ unsigned long long freed;
   __shared__ uint32_t m_s;
   __shared__ long long B_s;
@@ -1102,10 +1504,12 @@ int grow_records(StepState& st, uint32_t need, cudaStream_t s) {
 
 Slots slots_of(StepState& st, const augsched_instance_params* d_ip) {
   return Slots{st.st, st.V, st.last, st.ctx, st.kv, st.cpu, st.pend, st.A, st.P, st.Aevt, st.Asnap,
-               st.coef, d_ip, st.max_active};
+               st.coef, d_ip, st.max_active, st.wkv};
 }
 
 }  // namespace
+
+static size_t pf_smem_bytes() { return sizeof(unsigned long long) * 2 * PF_SCAP; }
 
 int step_ensure(StepState& st, uint32_t n_inst, uint32_t max_active, cudaStream_t s,
                 const augsched_config& cfg, const augsched_instance_params* d_ip, uint64_t* launches) {
@@ -1131,7 +1535,7 @@ int step_ensure(StepState& st, uint32_t n_inst, uint32_t max_active, cudaStream_
   add(0, PK_KEY + 24, 10);
   for (uint32_t x = n_inst - 1, b = 0; x > 0; x >>= 8, ++b) add(2, (int)(8 * b), 8);
   if (hoff > STEP_HIST_WORDS) return set_error(AUGSCHED_E_CAPACITY, "step: too many sort passes");
-  const size_t zwords = (size_t)n_inst + STEP_HIST_WORDS + STEP_MAX_PASS + 8;
+  const size_t zwords = (size_t)n_inst + STEP_HIST_WORDS + STEP_MAX_PASS + PF_NCNT;
   int rc;
   if ((rc = salloc(st, &st.st, N)) || (rc = salloc(st, &st.V, N)) || (rc = salloc(st, &st.last, N)) ||
       (rc = salloc(st, &st.ctx, N)) || (rc = salloc(st, &st.kv, N)) || (rc = salloc(st, &st.cpu, N)) ||
@@ -1146,8 +1550,11 @@ int step_ensure(StepState& st, uint32_t n_inst, uint32_t max_active, cudaStream_
       (rc = salloc(st, &st.lb_status, (size_t)st.n_tiles << STEP_RB_MAX)) ||
       (rc = salloc(st, &st.lb_gstatus, (size_t)st.n_tiles << STEP_RB_MAX)) ||
       (rc = salloc(st, &st.pf_A, PF_SCAP)) || (rc = salloc(st, &st.pf_C, N)) ||
-      (rc = salloc(st, &st.gslot, N)))
+      (rc = salloc(st, &st.gslot, N)) || (rc = salloc(st, &st.pf_theta, 2)) ||
+      (rc = salloc(st, &st.pf_H, PF_HCAP)) || (rc = salloc(st, &st.wkv, 1)))
     return rc;
+  cudaMemsetAsync(st.wkv, 0, sizeof(uint32_t), s);
+  cudaMemsetAsync(st.pf_theta, 0xFF, 2 * sizeof(unsigned long long), s);   // no anchor: every slot
   // one memset per step clears the queue counts, histograms and tile counters
   st.zwords = zwords;
   st.n_active = st.zbuf;
@@ -1172,8 +1579,12 @@ int step_ensure(StepState& st, uint32_t n_inst, uint32_t max_active, cudaStream_
   int dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&st.sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaFuncSetAttribute(pf_admit_kernel<PNT, PF_SCAP / PNT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)(sizeof(unsigned long long) * 2 * PF_SCAP));
+  cudaFuncSetAttribute(pf_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pf_smem_bytes());
+  {
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pf_step_kernel, FNT, pf_smem_bytes());
+    st.pf_grid = st.sms * (occ > 0 ? occ : 1);
+  }
   cudaFuncSetAttribute(pf_multi_kernel<256, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PF_MULTI_SMEM);
   cudaFuncSetAttribute(pf_multi_kernel<PNT, PF_SCAP / PNT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)PF_MULTI_SMEM);
@@ -1238,7 +1649,6 @@ void run_records(StepState& st, const Slots& S, uint32_t* d_err, uint64_t now, c
 
 }  // namespace
 
-static size_t pf_smem_bytes() { return sizeof(unsigned long long) * 2 * PF_SCAP; }
 
 int step_run_prefix(StepState& st, const augsched_config& cfg, int64_t cap,
                     const augsched_instance_params* d_ip, uint32_t* d_err, uint64_t now,
@@ -1270,22 +1680,16 @@ int step_run_prefix(StepState& st, const augsched_config& cfg, int64_t cap,
     return cuda_check(cudaGetLastError(), "step_prefix");
   }
   cudaMemsetAsync(st.zbuf, 0, sizeof(uint32_t) * st.zwords, s);
-  KeyArgs ka;
-  ka.S = S; ka.cfg = cfg; ka.cap = cap; ka.now = now; ka.k0 = st.k0;
-  ka.ghist = st.ghist; ka.n_active = st.n_active; ka.budget = st.budget; ka.npass = 1;
-  ka.passes[0] = PassDesc{0, 64 - PF_BITS, PF_BITS, 0};
-  ka.N = (uint32_t)st.N;
-  ka.pf_cnt = st.pf_cnt;
-  const size_t kblocks = (st.N + KNT * KU - 1) / (KNT * KU);
-  const size_t kmax = (size_t)st.sms * AUGSCHED_KEYS_GRIDMUL;
-  const int kgrid = (int)(kblocks < kmax ? kblocks : kmax);
-  keys_kernel<<<kgrid, KNT, 0, s>>>(ka);
-  pf_collect_kernel<<<kgrid, KNT, 0, s>>>(st.k0, (uint32_t)st.N, st.pf_cnt, st.pf_A, st.pf_C);
-  pf_admit_kernel<PNT, PF_SCAP / PNT><<<1, PNT, pf_smem_bytes(), s>>>(S, cfg, cap, now, st.budget, st.n_active,
-                                                                      st.k0, st.pf_A, st.pf_C, st.pf_cnt,
-                                                                      st.order, st.key, st.grant, st.admitted,
-                                                                      st.gslot);
-  *launches += 3;
+  PfArgs pa;
+  pa.S = S; pa.cfg = cfg; pa.cap = cap; pa.now = now; pa.N = (uint32_t)st.N; pa.spec = st.pf_spec ? 1 : 0;
+  pa.k0 = st.k0; pa.A = st.pf_A; pa.C = st.pf_C; pa.theta = st.pf_theta; pa.H = st.pf_H; pa.ghist = st.ghist;
+  pa.cnt = st.pf_cnt; pa.n_active = st.n_active; pa.budget = st.budget;
+  pa.order = st.order; pa.keyout = st.key; pa.grant = st.grant; pa.admitted = st.admitted; pa.gslot = st.gslot;
+  void* args[] = {&pa};
+  cudaError_t e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(&pf_step_kernel), st.pf_grid, FNT,
+                                              args, pf_smem_bytes(), s);
+  if (e != cudaSuccess) return cuda_check(e, "step_prefix: cooperative launch");
+  *launches += 1;
   out->budget = reinterpret_cast<const int64_t*>(st.budget);
   out->n_active = st.n_active;
   out->admitted = st.admitted;
@@ -1307,7 +1711,6 @@ int step_run(StepState& st, const augsched_config& cfg, int64_t cap,
   ka.ghist = st.ghist; ka.n_active = st.n_active; ka.budget = st.budget; ka.npass = st.npass;
   for (int p = 0; p < st.npass; ++p) ka.passes[p] = st.passes[p];
   ka.N = (uint32_t)st.N;
-  ka.pf_cnt = nullptr;
   const size_t kblocks = (st.N + KNT * KU - 1) / (KNT * KU);
   const int kgrid = (int)(kblocks < (size_t)st.sms * 8 ? kblocks : (size_t)st.sms * 8);
   keys_kernel<<<kgrid, KNT, 0, s>>>(ka);

@@ -74,6 +74,11 @@ struct StepState {
   uint32_t* pf_cnt = nullptr;     // prefix step: [|A|, |C|]
   unsigned long long *pf_A = nullptr, *pf_C = nullptr;   // prefix step candidates (packed words)
   uint32_t* gslot = nullptr;      // prefix step: grant by slot during resolution (kept zero)
+  unsigned long long* pf_theta = nullptr;   // prefix step: anchor word and slot (kept across steps)
+  unsigned long long* pf_H = nullptr;       // prefix step: holder list (resolution candidates)
+  uint32_t* wkv = nullptr;                  // sticky flag: KV held outside running / swapped / Preserve-paused
+  int pf_grid = 0;                // prefix step: co-resident CTAs of the cooperative kernel
+  bool pf_spec = true;            // prefix step: speculative pass (off when any instance shuffles)
   uint32_t max_limit = 0;         // largest token limit any instance can get
   size_t zwords = 0;
   int sms = 148;

@@ -159,9 +159,39 @@ def test_prefix_step_event_stream(seed, cap, ranking):
     s.close()
 
 
+@pytest.mark.parametrize("seed,cap,ranking", [(31, 10**6, 0), (32, 500, 0), (33, 10**6, 1)])
+def test_prefix_step_anchor_event_stream(seed, cap, ranking):
+    """A single-instance queue larger than the candidate capacity (12,000
+    slots > 8,192): the first step takes the histogram fallback, later steps
+    the speculative pass against the previous step's anchor slot; random
+    NEW/CALL/RETURN/FINISH events move entries across the anchor and small
+    caps force demotion and tail eviction.  Every step equals the oracle's
+    full-order step on the admitted prefix."""
+    rng = np.random.default_rng(seed)
+    MA = 12_000
+    cfg = dict(tracegen.PRESET_G0, g_total=1000 + cap, g_model=1000)
+    ip = tracegen.inst_params(1, base=tracegen.INST_G0, ranking=ranking, budget_mode=0, target_max=300,
+                              alpha=1.5)
+    st = oracle.Step(cfg, ip, MA)
+    s = aug.Scheduler(cfg, ip, 1, MA)
+    for t in range(24):
+        rec = random_events(rng, st.slots(0), t, p_new=0.85 if t == 0 else 0.05)
+        if rec is not None:
+            assert st.enqueue(0, rec) == 0
+            s.enqueue(0, rec)
+        o = st.step(t)
+        assert o["rc"] == 0
+        g = s.step_result(s.step(t, prefix=True))
+        compare(g, o, 1, f"anchor seed {seed} step {t}", prefix=True)
+        assert int(o["n_active"][0]) > 8192 or t > 0
+    s.close()
+
+
 def test_prefix_step_cfg4_one_million_queue():
-    """Config 4 through augsched_step_prefix: 3 consecutive steps over the
-    1,000,000-request queue; the admitted prefix equals the oracle's order."""
+    """Config 4 through augsched_step_prefix: 6 consecutive steps over the
+    1,000,000-request queue (the first through the histogram fallback, the
+    rest through the anchored speculative pass); the admitted prefix equals
+    the oracle's order."""
     n = 1_000_000
     rec = tracegen.cfg4_records(n)
     cfg = tracegen.PRESET_CFG4
@@ -171,7 +201,7 @@ def test_prefix_step_cfg4_one_million_queue():
     s = aug.Scheduler(cfg, ip, 1, n)
     s.enqueue(0, rec)
     t0 = 65536
-    for k in range(3):
+    for k in range(6):
         o = st.step(t0 + k)
         g = s.step_result(s.step(t0 + k, prefix=True))
         compare(g, o, 1, f"cfg4 prefix step {k}", prefix=True)

@@ -1,0 +1,31 @@
+"""Run only bench.py's cfg4 step measurements (same code path and timing:
+L2 flushed before each step, CUDA events on the scheduler's stream)."""
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import torch  # noqa: E402
+import bench  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--steps", type=int, default=20)
+ap.add_argument("--warmup", type=int, default=5)
+ap.add_argument("--step-n", type=int, default=1_000_000)
+ap.add_argument("--sizes", default="1000000,4194304,16000000")
+ap.add_argument("--full", action="store_true", help="also the full-order step")
+a = ap.parse_args()
+torch.cuda.set_device(0)
+stream = torch.cuda.current_stream()
+peak = bench.hbm_peak() if hasattr(bench, "hbm_peak") else 6539.2
+out = {}
+for n in [int(x) for x in a.sizes.split(",")]:
+    r = bench.step_bench(a, 0, stream, peak, prefix=True, n_override=n)
+    out[n] = {k: r[k] for k in ("value", "ms_per_step_cold_l2", "ms_per_step_warm_l2", "launches_per_step")}
+    out[n]["frac"] = r["roofline"]["frac"]
+    if a.full:
+        r = bench.step_bench(a, 0, stream, peak, prefix=False, n_override=n)
+        out[n]["full_ms_cold"] = r["ms_per_step_cold_l2"]
+print(json.dumps(out, indent=1))
