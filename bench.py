@@ -361,7 +361,7 @@ def run_gpu(args):
     achieved = per_launch_bytes / (total_ms / args.steps / 1e3) / 1e9
     roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
             "frac": round(achieved / peak, 4), "traffic": None,
-            "kernel": "sim_kernel (persistent, one CTA per instance)", "peak_source": peak_src,
+            "kernel": "sim_kernel (persistent; 16 one-warp instances per CTA advancing in step)", "peak_source": peak_src,
             "algorithmic_bytes_per_decision": 32}
     # DRAM bytes per launch of the same kernel on the same workload, from one
     # ncu capture of bench.py's timed launches (tools/traffic.py)

@@ -141,7 +141,7 @@ int ensure_sim(augsched_t* h) {
   CUDA_TRY(cudaFuncSetAttribute(sim_kernel_ptr(), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)h->sim_smem));
   int per_sm = 0, sms = 0;
-  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sim_kernel_ptr(), SIM_NT,
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sim_kernel_ptr(), SIM_NT * SIM_WPC,
                                                          h->sim_smem));
   CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
   if (per_sm < 1) return fail(AUGSCHED_E_CUDA, "simulate kernel does not fit on an SM");
@@ -356,7 +356,8 @@ int augsched_simulate(augsched_t* h, const augsched_trace* traces, const uint32_
   p.max_active = h->max_active;
   p.work = h->d_work;
   p.err = h->d_err;
-  const int grid = (int)(h->n_inst < (uint32_t)h->sim_grid ? h->n_inst : (uint32_t)h->sim_grid);
+  const uint32_t ctas = (h->n_inst + SIM_WPC - 1) / SIM_WPC;   // SIM_WPC instances in flight per CTA
+  const int grid = (int)(ctas < (uint32_t)h->sim_grid ? ctas : (uint32_t)h->sim_grid);
   CUDA_TRY(launch_sim(p, grid, h->sim_smem, h->stream));
   h->launches += 1;
   if (flags & AUGSCHED_HOST_RESULTS) {

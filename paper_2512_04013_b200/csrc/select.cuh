@@ -17,7 +17,19 @@
 #pragma once
 #include <cstdint>
 
+#ifndef AUGSCHED_SIM_WPC
+#define AUGSCHED_SIM_WPC 16   // instances per simulate CTA (same default as sim.cuh)
+#endif
+
 namespace augsched {
+
+// The selection group is NT threads: the whole CTA, or (NT == 32 in a
+// simulate CTA that runs several one-warp instances) one warp.
+template <int NT>
+__device__ __forceinline__ void sel_sync() {
+  if (NT == 32 && AUGSCHED_SIM_WPC > 1) __syncwarp();
+  else __syncthreads();
+}
 
 template <int RB>
 struct SelBinsT {
@@ -47,15 +59,15 @@ __device__ void wselect(SelBinsT<RB>& sb, SelRes& s, uint32_t n, uint64_t D, int
   constexpr unsigned FULL = 0xffffffffu;
   constexpr int NB = 1 << RB;
   static_assert(NB >= 32 && NB % 32 == 0, "one warp scans the bins in 32-wide chunks");
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x % NT, lane = tid & 31, warp = tid >> 5;
   const uint32_t Dc = (uint32_t)(D < (1ull << 26) ? D : (1ull << 26));
-  __syncthreads();
+  sel_sync<NT>();
   if (tid == 0) {
     s.prefix = 0; s.mask = 0; s.wbelow = 0; s.found = 0; s.done = 0; s.total = 0; s.cnt = 0;
     s.k = 0;
   }
   for (int b = tid; b < NB; b += NT) { sb.wbin[0][b] = 0; sb.cbin[0][b] = 0; }
-  __syncthreads();
+  sel_sync<NT>();
   int hi = nbits, pb = 0;
   while (hi > 0) {
     const int lo = hi > RB ? hi - RB : 0;
@@ -87,7 +99,7 @@ __device__ void wselect(SelBinsT<RB>& sb, SelRes& s, uint32_t n, uint64_t D, int
         }
       }
     }
-    __syncthreads();
+    sel_sync<NT>();
     if (warp == 0) {
       unsigned long long run = s.wbelow;
       int bin = -1;
@@ -125,7 +137,7 @@ __device__ void wselect(SelBinsT<RB>& sb, SelRes& s, uint32_t n, uint64_t D, int
         }
       }
     }
-    __syncthreads();
+    sel_sync<NT>();
     if (s.done) break;
     hi = lo;
     pb ^= 1;
@@ -154,7 +166,7 @@ struct CandShmT {
 template <int NT, int C>
 __device__ void rank_select(CandShmT<C>& c, int list, SelRes& r, int m, uint64_t D, uint64_t w0) {
   constexpr unsigned FULL = 0xffffffffu;
-  const int tid = threadIdx.x, lane = tid & 31;
+  const int tid = threadIdx.x % NT, lane = tid & 31;
   const unsigned long long* ck = c.ck[list];
   const unsigned int* cw = c.cw[list];
   for (int a = tid; a < m; a += NT) {
@@ -164,7 +176,7 @@ __device__ void rank_select(CandShmT<C>& c, int list, SelRes& r, int m, uint64_t
     c.rk[rk] = key;
     c.rw[rk] = cw[a];
   }
-  __syncthreads();
+  sel_sync<NT>();
   if (tid < 32) {
     unsigned long long run = w0;
     int hit = -1;
@@ -192,7 +204,7 @@ __device__ void rank_select(CandShmT<C>& c, int list, SelRes& r, int m, uint64_t
       else { r.found = 1; r.k = c.rk[hit]; r.wbelow = wb; }
     }
   }
-  __syncthreads();
+  sel_sync<NT>();
 }
 
 }  // namespace augsched

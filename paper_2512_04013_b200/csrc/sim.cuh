@@ -32,14 +32,23 @@ constexpr int SIM_RB = SIM_NT >= 256 ? 8 : 5;   // radix bits of the fallback se
 #endif
 constexpr int SIM_CAND = AUGSCHED_SIM_CAND;      // small-candidate list capacity
 #ifndef AUGSCHED_SIM_MINB
-#define AUGSCHED_SIM_MINB 24
+#define AUGSCHED_SIM_MINB 32
 #endif
 #ifndef AUGSCHED_SIM_UNROLL
 #define AUGSCHED_SIM_UNROLL 2
 #endif
-constexpr int SIM_MINB = AUGSCHED_SIM_MINB;   // CTAs per SM the kernel is register-bounded for
+constexpr int SIM_MINB = AUGSCHED_SIM_MINB;   // resident instances (warps) per SM the registers are bounded for
 constexpr int SIM_UNROLL = AUGSCHED_SIM_UNROLL;  // queue entries in flight per thread in the key pass
 constexpr int SIM_NW = SIM_NT / 32;
+// One-warp instances per CTA.  Above 1 the CTA's instances advance in step
+// (one CTA barrier per iteration) so its warps run the same phase of the
+// step at the same time and share the instruction stream (the step's code
+// far exceeds the SM's 32 KB instruction cache).
+#ifndef AUGSCHED_SIM_WPC
+#define AUGSCHED_SIM_WPC 16
+#endif
+constexpr int SIM_WPC = AUGSCHED_SIM_WPC;
+static_assert(SIM_WPC == 1 || SIM_NT == 32, "several instances per CTA need one-warp instances");
 constexpr int KBITS = 50;                 // tier(2) | key(32) | id(16)
 constexpr uint64_t KMASK = (1ull << KBITS) - 1;
 constexpr uint64_t KEVICT = 1ull << 63;   // marks an evicted entry in the K array
