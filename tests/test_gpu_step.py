@@ -159,19 +159,20 @@ def test_prefix_step_event_stream(seed, cap, ranking):
     s.close()
 
 
-@pytest.mark.parametrize("seed,cap,ranking", [(31, 10**6, 0), (32, 500, 0), (33, 10**6, 1)])
+@pytest.mark.parametrize("seed,cap,ranking", [(31, 10**6, 0), (32, 500, 0), (33, 10**6, 1), (34, 500, 2)])
 def test_prefix_step_anchor_event_stream(seed, cap, ranking):
     """A single-instance queue larger than the candidate capacity (12,000
     slots > 8,192): the first step takes the histogram fallback, later steps
     the speculative pass against the previous step's anchor slot; random
     NEW/CALL/RETURN/FINISH events move entries across the anchor and small
-    caps force demotion and tail eviction.  Every step equals the oracle's
-    full-order step on the admitted prefix."""
+    caps force demotion and tail eviction; random ranking (a fresh shuffle
+    every step, so no anchor) takes the histogram path on every step.  Every
+    step equals the oracle's full-order step on the admitted prefix."""
     rng = np.random.default_rng(seed)
     MA = 12_000
     cfg = dict(tracegen.PRESET_G0, g_total=1000 + cap, g_model=1000)
     ip = tracegen.inst_params(1, base=tracegen.INST_G0, ranking=ranking, budget_mode=0, target_max=300,
-                              alpha=1.5)
+                              alpha=1.5, rank_seed=seed)
     st = oracle.Step(cfg, ip, MA)
     s = aug.Scheduler(cfg, ip, 1, MA)
     for t in range(24):
