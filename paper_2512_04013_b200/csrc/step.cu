@@ -1663,7 +1663,10 @@ int step_run_prefix(StepState& st, const augsched_config& cfg, int64_t cap,
   Slots S = slots_of(st, d_ip);
   run_records(st, S, d_err, now, s, launches);
   if (st.n_inst > 1) {
-    if (scap <= 4 * 256)   // small limits: 256-thread CTAs, more instances resident per SM
+#ifndef AUGSCHED_PF_MULTI_SMALL
+#define AUGSCHED_PF_MULTI_SMALL (4 * 256)
+#endif
+    if (scap <= AUGSCHED_PF_MULTI_SMALL)   // small limits: 256-thread CTAs, more instances resident per SM
       pf_multi_kernel<256, 4><<<st.n_inst, 256, msmem, s>>>(S, cfg, cap, now, st.budget, st.n_active, st.order,
                                                              st.key, st.grant, st.admitted, st.gslot, scap);
     else

@@ -16,11 +16,15 @@ ap.add_argument("--warmup", type=int, default=5)
 ap.add_argument("--step-n", type=int, default=1_000_000)
 ap.add_argument("--sizes", default="1000000,4194304,16000000")
 ap.add_argument("--full", action="store_true", help="also the full-order step")
+ap.add_argument("--multi", action="store_true", help="the batched step (4,096 instances x 2,048 slots) only")
 a = ap.parse_args()
 torch.cuda.set_device(0)
 stream = torch.cuda.current_stream()
 peak = bench.hbm_peak() if hasattr(bench, "hbm_peak") else 6539.2
 out = {}
+if a.multi:
+    print(json.dumps(bench.step_multi_bench(a, 0, stream, peak), indent=1))
+    sys.exit(0)
 for n in [int(x) for x in a.sizes.split(",")]:
     r = bench.step_bench(a, 0, stream, peak, prefix=True, n_override=n)
     out[n] = {k: r[k] for k in ("value", "ms_per_step_cold_l2", "ms_per_step_warm_l2", "launches_per_step")}
