@@ -1038,8 +1038,11 @@ struct PfArgs {
   unsigned long long* theta;      // [2] anchor word, anchor slot (kept across steps)
   unsigned long long* H;          // [PF_HCAP] words of the slots that can hold KV (resolution candidates)
   uint32_t* ghist;                // [1 << PF_BITS]
-  uint32_t* cnt;                  // [PF_NCNT], zeroed every step
-  uint32_t* n_active;
+  uint32_t* cnt;                  // [PF_NCNT]: append counts (zero at entry, zeroed again by the
+                                  // finishing CTA), arrival counts (cumulative, mod G), epoch-tagged flags
+  uint32_t ep;                    // this call's epoch tag (1 .. 2^30 - 1)
+  uint32_t* n_active;             // this call's queue-size word (zero at entry)
+  uint32_t* n_active_next;        // the other one: the previous call's output, zeroed for the next call
   long long* budget;
   uint32_t *order, *keyout, *grant, *admitted, *gslot;
 };
@@ -1052,22 +1055,31 @@ __device__ __forceinline__ uint32_t pf_margin(uint32_t target) { return target /
 
 // Arrive at a grid-wide counter; true in the CTA that arrives last.  The
 // caller's global writes are visible to that CTA.
+// Arrive at a grid-wide counter; true in the CTA that arrives last.  The
+// counter is never reset: every call adds exactly G arrivals, so the last
+// arrival is the one that makes it a multiple of G.
 __device__ __forceinline__ bool pf_arrive_last(uint32_t* ctr, uint32_t G, uint32_t& flag) {
   __syncthreads();   // the CTA's writes happen before thread 0's release (cumulative fence)
   if (threadIdx.x == 0) {
     __threadfence();
-    flag = atomicAdd(ctr, 1u) == G - 1;
+    flag = (atomicAdd(ctr, 1u) + 1u) % G == 0;
     if (flag) __threadfence();
   }
   __syncthreads();
   return flag != 0;
 }
 
-__device__ __forceinline__ uint32_t pf_wait(const uint32_t* w, uint32_t& flag) {
+// Epoch-tagged flag word: (epoch << 2) | value.  Wait until this call's
+// epoch shows; returns the value.
+__device__ __forceinline__ void pf_post(uint32_t* w, uint32_t ep, uint32_t v) {
+  __threadfence();
+  atomicExch(w, (ep << 2) | v);
+}
+__device__ __forceinline__ uint32_t pf_wait(const uint32_t* w, uint32_t ep, uint32_t& flag) {
   if (threadIdx.x == 0) {
     uint32_t v;
-    while ((v = vld(w)) == 0) __nanosleep(32);
-    flag = v;
+    while (((v = vld(w)) >> 2) != ep) __nanosleep(32);
+    flag = v & 3u;
   }
   __syncthreads();
   return flag;
@@ -1121,6 +1133,10 @@ __global__ void __launch_bounds__(FNT, 1) pf_step_kernel(const __grid_constant__
 #endif
       a.theta[0] = K > 0 ? sbuf[K - 1] : ~0ull;
       a.theta[1] = K > 0 ? (sbuf[K - 1] & SLOT_MASK) : ~0ull;
+      // every other CTA is done with the append counters: clear them (and the
+      // next call's queue-size word) for the next call
+      cnt[PC_SPEC] = 0; cnt[PC_H] = 0; cnt[PC_A] = 0; cnt[PC_C] = 0;
+      *a.n_active_next = 0;
     }
   };
   // slots that can hold KV: running, swapped, Preserve-paused (the
@@ -1246,8 +1262,7 @@ __global__ void __launch_bounds__(FNT, 1) pf_step_kernel(const __grid_constant__
         const uint32_t target = set_target();
         const bool ok = target == 0 || (nc >= target && nc <= PF_SCAP);
         m_s = ok ? (target == 0 ? 0u : nc) : 0xFFFFFFFFu;
-        __threadfence();
-        atomicExch(&cnt[PC_STATE], ok ? 1u : 2u);
+        pf_post(&cnt[PC_STATE], a.ep, ok ? 1u : 2u);
       }
       __syncthreads();
       const uint32_t mt = m_s;
@@ -1257,7 +1272,7 @@ __global__ void __launch_bounds__(FNT, 1) pf_step_kernel(const __grid_constant__
         finish(mt, nullptr);
         return;
       }
-    } else if (pf_wait(&cnt[PC_STATE], flag_s) == 1) {
+    } else if (pf_wait(&cnt[PC_STATE], a.ep, flag_s) == 1) {
       return;
     }
   }
@@ -1300,7 +1315,11 @@ __global__ void __launch_bounds__(FNT, 1) pf_step_kernel(const __grid_constant__
     constexpr int PER = NB / FNT;
     uint32_t loc[PER], sum = 0;
 #pragma unroll
-    for (int j = 0; j < PER; ++j) { loc[j] = __ldcg(&a.ghist[tid * PER + j]); sum += loc[j]; }
+    for (int j = 0; j < PER; ++j) {
+      loc[j] = __ldcg(&a.ghist[tid * PER + j]);
+      sum += loc[j];
+      a.ghist[tid * PER + j] = 0;   // all CTAs have added theirs: clear for the next call
+    }
     uint32_t inc = sum;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -1319,9 +1338,9 @@ __global__ void __launch_bounds__(FNT, 1) pf_step_kernel(const __grid_constant__
     }
     __threadfence();
     __syncthreads();
-    if (tid == 0) atomicExch(&cnt[PC_REL2], 1u);
+    if (tid == 0) pf_post(&cnt[PC_REL2], a.ep, 1u);
   } else {
-    pf_wait(&cnt[PC_REL2], flag_s);
+    pf_wait(&cnt[PC_REL2], a.ep, flag_s);
   }
   // ---- phase 3: words below b* -> A, in b* -> C
   const uint32_t bstar = __ldcg(&cnt[PC_BSTAR]);
@@ -1551,8 +1570,12 @@ int step_ensure(StepState& st, uint32_t n_inst, uint32_t max_active, cudaStream_
       (rc = salloc(st, &st.lb_gstatus, (size_t)st.n_tiles << STEP_RB_MAX)) ||
       (rc = salloc(st, &st.pf_A, PF_SCAP)) || (rc = salloc(st, &st.pf_C, N)) ||
       (rc = salloc(st, &st.gslot, N)) || (rc = salloc(st, &st.pf_theta, 2)) ||
-      (rc = salloc(st, &st.pf_H, PF_HCAP)) || (rc = salloc(st, &st.wkv, 1)))
+      (rc = salloc(st, &st.pf_H, PF_HCAP)) || (rc = salloc(st, &st.wkv, 1)) ||
+      (rc = salloc(st, &st.pf_nact, 2)))
     return rc;
+  cudaMemsetAsync(st.zbuf, 0, sizeof(uint32_t) * zwords, s);   // the prefix kernel expects clear counters
+  cudaMemsetAsync(st.pf_nact, 0, 2 * sizeof(uint32_t), s);
+  st.pf_epoch = 0;
   cudaMemsetAsync(st.wkv, 0, sizeof(uint32_t), s);
   cudaMemsetAsync(st.pf_theta, 0xFF, 2 * sizeof(unsigned long long), s);   // no anchor: every slot
   // one memset per step clears the queue counts, histograms and tile counters
@@ -1682,11 +1705,19 @@ int step_run_prefix(StepState& st, const augsched_config& cfg, int64_t cap,
     out->key = st.key;
     return cuda_check(cudaGetLastError(), "step_prefix");
   }
-  cudaMemsetAsync(st.zbuf, 0, sizeof(uint32_t) * st.zwords, s);
+  // no memset: the kernel leaves its counters cleared for the next call
+  // (a full step in between leaves its histograms behind: clear once)
+  if (st.pf_dirty) {
+    cudaMemsetAsync(st.zbuf, 0, sizeof(uint32_t) * st.zwords, s);
+    st.pf_dirty = false;
+  }
+  if (++st.pf_epoch >= (1u << 30)) st.pf_epoch = 1;
+  const uint32_t ep = st.pf_epoch;
   PfArgs pa;
   pa.S = S; pa.cfg = cfg; pa.cap = cap; pa.now = now; pa.N = (uint32_t)st.N; pa.spec = st.pf_spec ? 1 : 0;
   pa.k0 = st.k0; pa.A = st.pf_A; pa.C = st.pf_C; pa.theta = st.pf_theta; pa.H = st.pf_H; pa.ghist = st.ghist;
-  pa.cnt = st.pf_cnt; pa.n_active = st.n_active; pa.budget = st.budget;
+  pa.cnt = st.pf_cnt; pa.ep = ep; pa.n_active = st.pf_nact + (ep & 1u); pa.n_active_next = st.pf_nact + ((ep + 1u) & 1u);
+  pa.budget = st.budget;
   pa.order = st.order; pa.keyout = st.key; pa.grant = st.grant; pa.admitted = st.admitted; pa.gslot = st.gslot;
   void* args[] = {&pa};
   cudaError_t e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(&pf_step_kernel), st.pf_grid, FNT,
@@ -1694,7 +1725,7 @@ int step_run_prefix(StepState& st, const augsched_config& cfg, int64_t cap,
   if (e != cudaSuccess) return cuda_check(e, "step_prefix: cooperative launch");
   *launches += 1;
   out->budget = reinterpret_cast<const int64_t*>(st.budget);
-  out->n_active = st.n_active;
+  out->n_active = pa.n_active;
   out->admitted = st.admitted;
   out->order = st.order;
   out->grant = st.grant;
@@ -1708,6 +1739,7 @@ int step_run(StepState& st, const augsched_config& cfg, int64_t cap,
   Slots S = slots_of(st, d_ip);
   const uint32_t ni = st.n_inst;
   run_records(st, S, d_err, now, s, launches);
+  st.pf_dirty = true;
   cudaMemsetAsync(st.zbuf, 0, sizeof(uint32_t) * st.zwords, s);
   KeyArgs ka;
   ka.S = S; ka.cfg = cfg; ka.cap = cap; ka.now = now; ka.k0 = st.k0;

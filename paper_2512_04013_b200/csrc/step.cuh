@@ -77,6 +77,9 @@ struct StepState {
   unsigned long long* pf_theta = nullptr;   // prefix step: anchor word and slot (kept across steps)
   unsigned long long* pf_H = nullptr;       // prefix step: holder list (resolution candidates)
   uint32_t* wkv = nullptr;                  // sticky flag: KV held outside running / swapped / Preserve-paused
+  uint32_t* pf_nact = nullptr;              // prefix step: queue-size words, alternating by epoch
+  uint32_t pf_epoch = 0;                    // prefix step: calls so far (epoch tag of the kernel's flags)
+  bool pf_dirty = false;                    // a full step ran since: counters need one clear
   int pf_grid = 0;                // prefix step: co-resident CTAs of the cooperative kernel
   bool pf_spec = true;            // prefix step: speculative pass (off when any instance shuffles)
   uint32_t max_limit = 0;         // largest token limit any instance can get

@@ -188,6 +188,29 @@ def test_prefix_step_anchor_event_stream(seed, cap, ranking):
     s.close()
 
 
+def test_prefix_and_full_steps_interleaved():
+    """One single-instance handle (10,000 slots) alternating augsched_step
+    and augsched_step_prefix: the prefix kernel keeps its counters clear
+    across calls (epoch-tagged flags, no per-step memset) and the full step
+    in between leaves nothing behind; every step equals the oracle's."""
+    rng = np.random.default_rng(41)
+    MA = 10_000
+    cfg = dict(tracegen.PRESET_G0, g_total=1000 + 600, g_model=1000)
+    ip = tracegen.inst_params(1, base=tracegen.INST_G0, ranking=0, budget_mode=0, target_max=300, alpha=1.5)
+    st = oracle.Step(cfg, ip, MA)
+    s = aug.Scheduler(cfg, ip, 1, MA)
+    for t in range(16):
+        rec = random_events(rng, st.slots(0), t, p_new=0.9 if t == 0 else 0.05)
+        if rec is not None:
+            assert st.enqueue(0, rec) == 0
+            s.enqueue(0, rec)
+        o = st.step(t)
+        pre = t % 4 != 2
+        g = s.step_result(s.step(t, prefix=pre))
+        compare(g, o, 1, f"interleaved step {t} prefix={pre}", prefix=pre)
+    s.close()
+
+
 def test_prefix_step_cfg4_one_million_queue():
     """Config 4 through augsched_step_prefix: 6 consecutive steps over the
     1,000,000-request queue (the first through the histogram fallback, the
