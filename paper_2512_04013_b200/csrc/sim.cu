@@ -369,7 +369,6 @@ struct GrantRule {
 // instance cannot run (its trace exceeds the arena; reported in its record).
 __device__ bool inst_begin(const SimParams& p, SimShm& s, uint32_t inst) {
   const int tid = ITID;
-  const int lane = tid & 31, warp = tid >> 5;
   const size_t off = (size_t)inst * p.max_active;
   const Arena& a = p.ar;
   if (tid == 0) { s.coef = make_coef(p.cfg, p.ip[inst]); s.ip = p.ip[inst]; }
