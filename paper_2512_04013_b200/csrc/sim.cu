@@ -381,7 +381,6 @@ __device__ bool inst_begin(const SimParams& p, SimShm& s, uint32_t inst) {
   c.r0 = p.tr.req_off[c.trace];
   c.n = p.tr.req_off[c.trace + 1] - c.r0;
   if (tid == 0) { s.inst = inst; s.trace = c.trace; s.r0 = c.r0; s.n = c.n; }
-  const uint64_t T = p.cfg.t_fwd_ticks;
   const uint32_t n = c.n;
   InstHdr& H = p.hdr[inst];
   augsched_result& acc = p.acc[inst];
@@ -407,11 +406,6 @@ __device__ bool inst_begin(const SimParams& p, SimShm& s, uint32_t inst) {
   for (int f = tid; f < AUGSCHED_R_NFIELD; f += SIM_NT) { s.cnt[f] = acc.f[f]; s.c32[f] = 0; }
   ISYNC();
   if (tid == 0) s.cnt[AUGSCHED_R_NREQ] = n;
-  const int64_t cap = p.cap;
-  auto key_of = [&](double V, uint64_t t, uint32_t last, uint32_t e) -> uint32_t {
-    return rank_key(c.k, c.ip, V, t, last, e & 0xFFFF);
-  };
-
   if (tid == 0) prep_step(p, s, n);
   ISYNC();
   return true;
