@@ -715,10 +715,6 @@ __device__ __forceinline__ unsigned long long gtime() {
 #endif
 
 constexpr int PNT = 1024;
-#ifndef AUGSCHED_PF_SORT_E
-#define AUGSCHED_PF_SORT_E 4
-#endif
-constexpr int PF_SORT_E = AUGSCHED_PF_SORT_E;   // elements per sorting thread (the sort's thread count follows)
 
 // The admitted prefix of instance `inst` from `mt` candidate words in sbuf
 // (which hold its first `target` order entries): bitonic sort, admission
@@ -762,6 +758,79 @@ __device__ __forceinline__ unsigned long long bitonic1(unsigned long long v, uns
   return v;
 }
 
+// Bitonic sort of 2^LOGP words, E per thread over T = 2^LOGP / E threads
+// (index t + e * T), the network fully unrolled: distances >= T inside the
+// thread, below 32 by warp shuffles, in between through a double-buffered
+// shared exchange (one named barrier over the T threads per stage).
+template <int LOGP, int E>
+__device__ __forceinline__ void bitonicE(unsigned long long (&v)[E], unsigned long long* b0,
+                                         unsigned long long* b1) {
+  constexpr uint32_t P = 1u << LOGP, T = P / E;
+  static_assert(T >= 32 && T * E == P, "one warp at least");
+  const uint32_t t = threadIdx.x;
+  int xp = 0;
+#pragma unroll
+  for (int lk = 1; lk <= LOGP; ++lk) {
+#pragma unroll
+    for (int lj = lk - 1; lj >= 0; --lj) {
+      const uint32_t k = 1u << lk, j = 1u << lj;
+      if (j >= T) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const int e2 = e ^ (int)(j / T);
+          if (e2 > e) {
+            const bool up = ((t + (uint32_t)e * T) & k) == 0;
+            const unsigned long long x0 = v[e], x1 = v[e2];
+            const bool sw = (x0 > x1) == up;
+            v[e] = sw ? x1 : x0;
+            v[e2] = sw ? x0 : x1;
+          }
+        }
+      } else if (j < 32) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const unsigned long long pv = __shfl_xor_sync(FULL, v[e], j);
+          const uint32_t idx = t + (uint32_t)e * T;
+          const bool keep_min = ((idx & j) == 0) == ((idx & k) == 0);
+          v[e] = (keep_min == (pv < v[e])) ? pv : v[e];
+        }
+      } else {
+        unsigned long long* xb = xp ? b1 : b0;
+        xp ^= 1;
+#pragma unroll
+        for (int e = 0; e < E; ++e) xb[t + e * T] = v[e];
+        bar_named(T);
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const uint32_t idx = t + (uint32_t)e * T;
+          const unsigned long long pv = xb[idx ^ j];
+          const bool keep_min = ((idx & j) == 0) == ((idx & k) == 0);
+          v[e] = (keep_min == (pv < v[e])) ? pv : v[e];
+        }
+      }
+    }
+  }
+}
+
+// Sort sbuf[0, P2) (words at mt and beyond padded with ~0) with E = P2 / NT
+// words per thread; every thread of the block calls it.
+template <int NT, int LOGP>
+__device__ __forceinline__ void pf_sortE(unsigned long long* sbuf, unsigned long long* xch, uint32_t mt) {
+  constexpr int E = (1 << LOGP) / NT;
+  static_assert(E >= 2, "one word per thread has its own network");
+  unsigned long long v[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const uint32_t idx = threadIdx.x + e * NT;
+    v[e] = idx < mt ? sbuf[idx] : ~0ull;
+  }
+  bar_named(NT);
+  bitonicE<LOGP, E>(v, sbuf, xch);
+  bar_named(NT);
+#pragma unroll
+  for (int e = 0; e < E; ++e) sbuf[threadIdx.x + e * NT] = v[e];
+}
+
 template <int NT, int EM>
 __device__ void pf_finish(const Slots& S, const augsched_config& cfg, int64_t cap, uint64_t now, uint32_t inst,
                           size_t base, const unsigned long long* keys, unsigned long long* sbuf,
@@ -771,23 +840,12 @@ __device__ void pf_finish(const Slots& S, const augsched_config& cfg, int64_t ca
                           const unsigned long long* H = nullptr, uint32_t nH = 0) {
   const int tid = threadIdx.x;
   const uint32_t MA = S.MA;
-  // ---- bitonic sort of the prefix (padded to a power of two P2) by the
-  // first ST threads, ST = P2 / E (E elements per thread, at most EMAX; at
-  // least one warp): a bitonic network does P2 log^2 P2 / 4 compare-exchanges
-  // whatever the thread count, but every partner outside the thread is
-  // evaluated twice, so few threads with many elements each issue the fewest
-  // instructions.  Thread t holds indices t + e * ST: partner distances
-  // j < 32 exchange by warp shuffles, j >= ST inside the thread, and only
-  // 32 <= j < ST through shared memory (double-buffered, one named barrier
-  // over the ST threads per stage).
-  uint32_t P2 = 1;
+  // ---- bitonic sort of the prefix, padded to a power of two P2 <= EM * NT:
+  // one word per thread up to P2 = NT (<= 1,024), else E = P2 / NT words per
+  // thread; both networks fully unrolled per size.
+  uint32_t P2 = 32;
   while (P2 < mt) P2 <<= 1;
-  if (P2 < 32) P2 = 32;
-  constexpr int EMAX = EM < PF_SORT_E ? EM : PF_SORT_E;
-  const uint32_t ST = P2 / EMAX > 32 ? (P2 / EMAX < (uint32_t)NT ? P2 / EMAX : (uint32_t)NT) : 32u;
-  const uint32_t E = P2 / ST;
   if (P2 <= (uint32_t)NT && P2 <= 1024u) {
-    // one word per thread: the unrolled network
     if ((uint32_t)tid < P2) {
       unsigned long long v = (uint32_t)tid < mt ? sbuf[tid] : ~0ull;
       bar_named(P2);
@@ -802,63 +860,15 @@ __device__ void pf_finish(const Slots& S, const augsched_config& cfg, int64_t ca
       bar_named(P2);
       sbuf[tid] = v;
     }
-  } else if ((uint32_t)tid < ST) {
-    unsigned long long v[EMAX];
-#pragma unroll
-    for (int e = 0; e < EMAX; ++e) {
-      const uint32_t idx = tid + e * ST;
-      v[e] = (e < (int)E && idx < mt) ? sbuf[idx] : ~0ull;
-    }
-    asm volatile("bar.sync 1, %0;" ::"r"(ST) : "memory");
-    int xp = 0;
-    for (uint32_t k = 2; k <= P2; k <<= 1) {
-      for (uint32_t j = k >> 1; j > 0; j >>= 1) {
-        if (j < 32) {
-#pragma unroll
-          for (int e = 0; e < EMAX; ++e) {
-            if (e >= (int)E) break;
-            const unsigned long long pv = __shfl_xor_sync(FULL, v[e], j);
-            const uint32_t idx = tid + e * ST;
-            const bool keep_min = ((idx & j) == 0) == ((idx & k) == 0);
-            v[e] = keep_min ? (pv < v[e] ? pv : v[e]) : (pv > v[e] ? pv : v[e]);
-          }
-        } else if (j < ST) {
-          unsigned long long* xbuf = xp ? xch : sbuf;
-          xp ^= 1;
-#pragma unroll
-          for (int e = 0; e < EMAX; ++e)
-            if (e < (int)E) xbuf[tid + e * ST] = v[e];
-          asm volatile("bar.sync 1, %0;" ::"r"(ST) : "memory");
-#pragma unroll
-          for (int e = 0; e < EMAX; ++e) {
-            if (e >= (int)E) break;
-            const uint32_t idx = tid + e * ST;
-            const unsigned long long pv = xbuf[idx ^ j];
-            const bool keep_min = ((idx & j) == 0) == ((idx & k) == 0);
-            v[e] = keep_min ? (pv < v[e] ? pv : v[e]) : (pv > v[e] ? pv : v[e]);
-          }
-        } else {
-          // partner inside the thread: e ^ (j / ST), unrolled so v stays in registers
-#pragma unroll
-          for (int bsh = 0; (1 << bsh) < EMAX; ++bsh) {
-            if (j != (ST << bsh)) continue;
-#pragma unroll
-            for (int e = 0; e < EMAX; ++e) {
-              const int e2 = e ^ (1 << bsh);
-              if (e2 <= e || e2 >= (int)E) continue;
-              const uint32_t idx = tid + e * ST;
-              const bool up = (idx & k) == 0;
-              const unsigned long long x0 = v[e], x1 = v[e2];
-              if ((x0 > x1) == up) { v[e] = x1; v[e2] = x0; }
-            }
-          }
-        }
-      }
-    }
-    asm volatile("bar.sync 1, %0;" ::"r"(ST) : "memory");
-#pragma unroll
-    for (int e = 0; e < EMAX; ++e)
-      if (e < (int)E) sbuf[tid + e * ST] = v[e];
+  } else if (NT == 256) {
+    static_assert(NT != 256 || EM >= 4, "prefix of 1,024 words");
+    if (P2 == 512) pf_sortE<256, 9>(sbuf, xch, mt);
+    else pf_sortE<256, 10>(sbuf, xch, mt);
+  } else if (NT == 1024) {
+    static_assert(NT != 1024 || EM >= 8, "prefix of 8,192 words");
+    if (P2 == 2048) pf_sortE<1024, 11>(sbuf, xch, mt);
+    else if (P2 == 4096) pf_sortE<1024, 12>(sbuf, xch, mt);
+    else pf_sortE<1024, 13>(sbuf, xch, mt);
   }
   __syncthreads();
   PF_T(4, false);
