@@ -1425,7 +1425,8 @@ template <int NT, int EM>
 __global__ void __launch_bounds__(NT) pf_multi_kernel(Slots S, augsched_config cfg, int64_t cap, uint64_t now,
                                                        long long* budget, uint32_t* n_active, uint32_t* order,
                                                        uint32_t* keyout, uint32_t* grant, uint32_t* admitted,
-                                                       uint32_t* gslot, uint32_t sbuf_cap) {
+                                                       uint32_t* gslot, uint32_t sbuf_cap,
+                                                       unsigned long long* theta) {
   extern __shared__ __align__(16) unsigned long long pf_sm[];
   const uint32_t MA = S.MA;
   unsigned long long* kbuf = pf_sm;             // [MA] packed words of the instance
@@ -1434,8 +1435,9 @@ __global__ void __launch_bounds__(NT) pf_multi_kernel(Slots S, augsched_config c
   __shared__ SelShm sel;
   __shared__ unsigned long long wsum[NT / 32 + 1];
   __shared__ unsigned long long freed;
-  __shared__ uint32_t m_s;
+  __shared__ uint32_t m_s, c_s;
   __shared__ long long B_s;
+  __shared__ unsigned long long th_s;
   const int tid = threadIdx.x;
   const uint32_t inst = blockIdx.x;
   const size_t base = (size_t)inst * MA;
@@ -1445,6 +1447,7 @@ __global__ void __launch_bounds__(NT) pf_multi_kernel(Slots S, augsched_config c
     B_s = token_limit(cfg, k, ip, cap, ld_ll(&S.A[inst]), ld_ll(&S.P[inst]));
     budget[inst] = B_s;
     m_s = 0;
+    c_s = 0;
   }
   unsigned long long myq = 0;
   for (uint32_t x = tid; x < MA; x += NT) {
@@ -1459,18 +1462,58 @@ __global__ void __launch_bounds__(NT) pf_multi_kernel(Slots S, augsched_config c
   const long long B = B_s;
   const uint32_t target = pf_target(B, (uint32_t)nq);
   if (tid == 0) n_active[inst] = (uint32_t)nq;
+  // candidates kept beyond the prefix (the anchor's margin), within the buffer
+  const uint32_t margin = target / 8 > 32u ? target / 8 : 32u;
+  uint32_t want = target + margin < (uint32_t)nq ? target + margin : (uint32_t)nq;
+  want = want < sbuf_cap ? want : sbuf_cap;
   if (target > 0) {
-    wselect<NT>(sel, MA, target, 64, [&](uint32_t i, uint64_t& key, uint32_t& w) {
-      key = kbuf[i]; w = 1u; return (key >> PK_TIER) < 3; });
-    const unsigned long long tau = sel.r.found ? sel.r.k : ~0ull;
+    // anchored filter (as in the single-instance step): the words at or below
+    // the current word of the slot the previous step chose a margin beyond its
+    // prefix; exact whenever target <= their count <= sbuf_cap.  Otherwise
+    // (first step, random ranking, events that moved the anchor) a
+    // count-weighted radix select of the `want` smallest.
+    if (tid == 0) {
+      unsigned long long th = 0;   // no anchor: take the select
+      if (ip.ranking != AUGSCHED_RANK_RANDOM) {
+        th = theta[2 * inst];
+        const unsigned long long sg = theta[2 * inst + 1];
+        if (sg < MA && (kbuf[sg] >> PK_TIER) < 3) th = kbuf[sg];
+      }
+      th_s = th;
+    }
+    __syncthreads();
+    const unsigned long long th = th_s;
+    uint32_t c = 0;
+    for (uint32_t x = tid; x < MA; x += NT) {
+      const unsigned long long kx = kbuf[x];
+      c += (kx >> PK_TIER) < 3 && kx <= th;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(FULL, c, o);
+    if ((tid & 31) == 0 && c) atomicAdd(&c_s, c);
+    __syncthreads();
+    const uint32_t cnt = c_s;
+    unsigned long long tau = th;
+    if (cnt < target || cnt > sbuf_cap) {
+      wselect<NT>(sel, MA, want, 64, [&](uint32_t i, uint64_t& key, uint32_t& w) {
+        key = kbuf[i]; w = 1u; return (key >> PK_TIER) < 3; });
+      tau = sel.r.found ? sel.r.k : ~0ull;
+    }
     for (uint32_t x = tid; x < MA; x += NT) {
       const unsigned long long kx = kbuf[x];
       if ((kx >> PK_TIER) < 3 && kx <= tau) sbuf[atomicAdd(&m_s, 1u)] = kx;
     }
   }
   __syncthreads();
-  pf_finish<NT, EM>(S, cfg, cap, now, inst, base, kbuf, sbuf, xch, m_s, target, B, order, keyout, grant,
+  const uint32_t mt = m_s;
+  pf_finish<NT, EM>(S, cfg, cap, now, inst, base, kbuf, sbuf, xch, mt, target, B, order, keyout, grant,
                     admitted, gslot, sel, wsum, freed);
+  // next anchor: the want-th smallest word (sbuf is sorted by pf_finish)
+  if (tid == 0) {
+    const uint32_t K = want < mt ? want : mt;
+    theta[2 * inst] = K > 0 ? sbuf[K - 1] : ~0ull;
+    theta[2 * inst + 1] = K > 0 ? (sbuf[K - 1] & SLOT_MASK) : ~0ull;
+  }
 }
 
 }  // namespace
@@ -1579,7 +1622,7 @@ int step_ensure(StepState& st, uint32_t n_inst, uint32_t max_active, cudaStream_
       (rc = salloc(st, &st.lb_status, (size_t)st.n_tiles << STEP_RB_MAX)) ||
       (rc = salloc(st, &st.lb_gstatus, (size_t)st.n_tiles << STEP_RB_MAX)) ||
       (rc = salloc(st, &st.pf_A, PF_SCAP)) || (rc = salloc(st, &st.pf_C, N)) ||
-      (rc = salloc(st, &st.gslot, N)) || (rc = salloc(st, &st.pf_theta, 2)) ||
+      (rc = salloc(st, &st.gslot, N)) || (rc = salloc(st, &st.pf_theta, 2 * (size_t)n_inst)) ||
       (rc = salloc(st, &st.pf_H, PF_HCAP)) || (rc = salloc(st, &st.wkv, 1)) ||
       (rc = salloc(st, &st.pf_nact, 2)))
     return rc;
@@ -1587,7 +1630,7 @@ int step_ensure(StepState& st, uint32_t n_inst, uint32_t max_active, cudaStream_
   cudaMemsetAsync(st.pf_nact, 0, 2 * sizeof(uint32_t), s);
   st.pf_epoch = 0;
   cudaMemsetAsync(st.wkv, 0, sizeof(uint32_t), s);
-  cudaMemsetAsync(st.pf_theta, 0xFF, 2 * sizeof(unsigned long long), s);   // no anchor: every slot
+  cudaMemsetAsync(st.pf_theta, 0xFF, 2 * sizeof(unsigned long long) * (size_t)n_inst, s);   // no anchor: every slot
   // one memset per step clears the queue counts, histograms and tile counters
   st.zwords = zwords;
   st.n_active = st.zbuf;
@@ -1701,11 +1744,11 @@ int step_run_prefix(StepState& st, const augsched_config& cfg, int64_t cap,
 #endif
     if (scap <= AUGSCHED_PF_MULTI_SMALL)   // small limits: 256-thread CTAs, more instances resident per SM
       pf_multi_kernel<256, 4><<<st.n_inst, 256, msmem, s>>>(S, cfg, cap, now, st.budget, st.n_active, st.order,
-                                                             st.key, st.grant, st.admitted, st.gslot, scap);
+                                                             st.key, st.grant, st.admitted, st.gslot, scap, st.pf_theta);
     else
       pf_multi_kernel<PNT, PF_SCAP / PNT><<<st.n_inst, PNT, msmem, s>>>(S, cfg, cap, now, st.budget, st.n_active,
                                                                         st.order, st.key, st.grant, st.admitted,
-                                                                        st.gslot, scap);
+                                                                        st.gslot, scap, st.pf_theta);
     *launches += 1;
     out->budget = reinterpret_cast<const int64_t*>(st.budget);
     out->n_active = st.n_active;
