@@ -251,10 +251,17 @@ AUGSCHED_API int augsched_step(augsched_t* h, uint64_t now_iter, augsched_step_o
  * prefix: order/key/grant are valid for positions [0, admitted) of each
  * instance; later positions are not written.  Every queued request has
  * demand >= 1, so the admitted prefix lies within the first min(B, n)
- * entries of the order; a single-instance handle whose largest token limit
- * is <= 8192 finds them by a count-based selection (keys + one histogram
- * pass, a collect pass, one block that sorts and admits them) instead of a
- * full sort; any other handle runs augsched_step.  Asynchronous. */
+ * entries of the order, and they are found by selection instead of a full
+ * sort when the handle's largest token limit is <= 8192:
+ *   - one instance: one cooperative kernel (one launch per call): a
+ *     streaming pass keeps the words at or below the current word of an
+ *     anchor slot chosen by the previous call (exact whenever their count
+ *     lies in [min(B, n), 8192]; otherwise a histogram pass and a collect
+ *     pass), then one CTA sorts and admits them.  The kernel needs every
+ *     SM's share of the grid resident at once (cooperative launch);
+ *   - several instances whose slots fit in shared memory: one CTA per
+ *     instance, the same anchored filter per instance, else a radix select.
+ * Any other handle runs augsched_step.  Asynchronous. */
 AUGSCHED_API int augsched_step_prefix(augsched_t* h, uint64_t now_iter, augsched_step_out* out);
 
 /* Run every instance's simulation (Algorithm 1 + engine model + metrics) until
