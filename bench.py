@@ -206,17 +206,24 @@ def step_bench(args, dev, stream, peak, prefix=False, n_override=None):
     s.close()
     ms = float(np.median(cold))
     ach = 32.0 * n / (ms / 1e3) / 1e9
-    what = ("augsched_step_prefix: one cooperative kernel (streaming pass: Eq.26 key of every slot, words at "
-            "or below the previous step's anchor kept as candidates; one CTA sorts them and admits/resolves/"
-            "applies; histogram fallback when the anchor fails) + one memset"
+    what = ("augsched_step_prefix: one cooperative kernel, one launch (streaming pass: Eq.26 key of every "
+            "slot, words at or below the previous step's anchor kept as candidates; one CTA sorts them and "
+            "admits/resolves/applies; histogram fallback when the anchor fails)"
             if prefix else "augsched_step: keys + 4 LSD sort passes + admit/resolve/apply")
+    traffic = None
+    if prefix:   # ncu DRAM bytes per steady launch of the same command (profiles/step_prefix_traffic.json)
+        try:
+            tj = json.load(open(os.path.join(ROOT, "profiles", "step_prefix_traffic.json")))
+            traffic = tj["sizes"].get(str(n), {}).get("dram_bytes_per_launch_mean")
+        except (OSError, ValueError, KeyError):
+            traffic = None
     return {"workload": f"cfg4: one queue of {n} requests (512 running, 512 swapped, rest waiting "
                         "80% Stage I / 20% Stage II), " + ("admitted prefix" if prefix else "full stable order") +
                         " + admission per step",
             "value": n / (ms / 1e3), "unit": UNIT, "ms_per_step_cold_l2": ms,
             "ms_per_step_warm_l2": float(np.median(warm)), "launches_per_step": launches,
             "roofline": {"bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
-                         "frac": round(ach / peak, 4), "traffic": None,
+                         "frac": round(ach / peak, 4), "traffic": traffic,
                          "note": what + "; 32 B/decision, whole step, L2 flushed before each step"}}
 
 
