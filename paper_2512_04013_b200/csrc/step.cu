@@ -1251,8 +1251,10 @@ __global__ void __launch_bounds__(FNT, 1) pf_step_kernel(const __grid_constant__
             const uint32_t b = bc + __popc(cm[u] & lt);
             if (b < PF_SCAP) {
               a.A[b] = wv[u];
+#ifndef AUGSCHED_PF_NO_PREFETCH
               // the admission reads this slot's token state: start bringing it to L2
               prefetch_l2(&S.ctx[s]); prefetch_l2(&S.kv[s]); prefetch_l2(&S.cpu[s]); prefetch_l2(&S.pend[s]);
+#endif
             }
           }
           if ((hm[u] >> lane) & 1u) {
