@@ -26,7 +26,12 @@ PRESERVE, SWAP, DISCARD = 0, 1, 2
 
 
 def build(force: bool = False) -> str:
-    """Compile the oracle with g++ (no FMA contraction, R3)."""
+    """Compile the oracle with g++ (no FMA contraction, R3).  The environment
+    variable AUGSCHED_ORACLE_LIB names a prebuilt library to load instead
+    (tools/oracle_mutants.py uses it to run the pins against mutants)."""
+    alt = os.environ.get("AUGSCHED_ORACLE_LIB")
+    if alt:
+        return alt
     if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < os.path.getmtime(SRC):
         subprocess.check_call([
             "g++", "-O2", "-std=c++17", "-ffp-contract=off", "-fno-fast-math", "-fPIC",
