@@ -208,14 +208,26 @@ typedef struct augsched_record_soa {
 
 /* Outputs of one step: device pointers owned by the handle, valid until the
  * next call on it.  Per instance i the queue segment is
- * [i*max_active, i*max_active + n_active[i]) of order/grant/key.          */
+ * [i*max_active, i*max_active + n_active[i]) of order/grant/key.
+ *
+ * admitted[i] is the length of the admission prefix: the entries j of the
+ * order with P_{j-1} < B that Algorithm 1 adds to the batch (P:1225-1229,
+ * R17), counted BEFORE memory resolution (R20).  A tail eviction can cancel
+ * a grant inside the prefix, so grant[j] may be 0 for j < admitted[i]; the
+ * batch to run is {order[j] : j < admitted[i], grant[j] > 0}.  augsched_step
+ * writes grant[j] = 0 for every admitted[i] <= j < n_active[i].
+ * tier_off[3*i + k] is the position (within instance i's segment) where
+ * tier k (0 running, 1 swapped, 2 waiting, R16) starts; tier k
+ * ends where tier k+1 starts, tier 2 at n_active[i].                      */
 typedef struct augsched_step_out {
   const int64_t* budget;     /* [n_instances] token limit N_max of this step */
   const uint32_t* n_active;  /* [n_instances] |running u swapped u waiting| */
-  const uint32_t* admitted;  /* [n_instances] entries granted > 0 */
+  const uint32_t* admitted;  /* [n_instances] admission-prefix length (see above) */
   const uint32_t* order;     /* slot ids in scheduling order */
-  const uint32_t* grant;     /* tokens granted to order[j] this step */
+  const uint32_t* grant;     /* tokens granted to order[j] this step (0 if none or cancelled) */
   const uint32_t* key;       /* orderable u32 of the fp32 score of order[j] */
+  const uint32_t* tier_off;  /* [3 * n_instances] per-tier segment starts (augsched_step only;
+                                NULL from augsched_step_prefix) */
 } augsched_step_out;
 
 typedef struct augsched_handle augsched_t;
@@ -264,6 +276,16 @@ AUGSCHED_API int augsched_step(augsched_t* h, uint64_t now_iter, augsched_step_o
  * Any other handle runs augsched_step.  Asynchronous. */
 AUGSCHED_API int augsched_step_prefix(augsched_t* h, uint64_t now_iter, augsched_step_out* out);
 
+/* Export instance `instance`'s slot state to host memory (synchronizes the
+ * handle's stream): slots[6*x .. 6*x+5] = status (0 empty, 1 running,
+ * 2 swapped, 3 waiting, 4 paused), applied policy (AUGSCHED_PRESERVE/SWAP/
+ * DISCARD; 2 for an empty slot), ctx, kv, cpu, pend of slot x (the token
+ * state an IMPORT record carries); ledger[0..1] = A (KV of non-paused
+ * requests) and P (KV of Preserve-paused requests), Eq.27-28.  Either
+ * pointer may be NULL.  Records still pending are not applied.  Returns OK,
+ * E_INVALID or E_CUDA (a latched device fault is left for augsched_sync). */
+AUGSCHED_API int augsched_step_export(augsched_t* h, uint32_t instance, int32_t* slots, int64_t* ledger);
+
 /* Run every instance's simulation (Algorithm 1 + engine model + metrics) until
  * all its requests finished or its iteration counter reaches max_iters.
  * inst_trace_id[i] selects instance i's trace.  results: n_instances records.
@@ -282,7 +304,8 @@ AUGSCHED_API int augsched_simulate(augsched_t* h, const augsched_trace* traces, 
 AUGSCHED_API int augsched_generate(augsched_t* h, const augsched_gen_spec* spec, const augsched_gen_tables* tables,
                       augsched_trace* out, uint32_t req_cap, uint32_t seg_cap);
 
-/* Wait for the handle's stream; returns a latched device error (E_STATE) if any. */
+/* Wait for the handle's stream; returns a latched device error (E_STATE) if
+ * any, once: the latch is cleared when it is reported. */
 AUGSCHED_API int augsched_sync(augsched_t* h);
 
 /* Number of kernel launches issued by this handle since creation. */

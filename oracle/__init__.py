@@ -241,7 +241,7 @@ class Step:
         L.oracle_step_create.argtypes = [C.POINTER(OCfg), C.c_void_p, C.c_uint32, C.c_uint32]
         L.oracle_step_destroy.argtypes = [C.c_void_p]
         L.oracle_step_enqueue.argtypes = [C.c_void_p, C.c_uint32, C.c_uint32] + [C.c_void_p] * 12
-        L.oracle_step.argtypes = [C.c_void_p, C.c_uint64] + [C.c_void_p] * 6
+        L.oracle_step.argtypes = [C.c_void_p, C.c_uint64] + [C.c_void_p] * 7
         L.oracle_step_ledger.argtypes = [C.c_void_p, C.c_uint32, C.c_void_p, C.c_void_p]
         self.L = L
         self.cfg = make_cfg(cfg)
@@ -272,17 +272,17 @@ class Step:
         order = np.zeros(n * m, np.uint32)
         grant = np.zeros(n * m, np.uint32)
         keys = np.zeros(n * m, np.uint32)
+        toff = np.zeros(3 * n, np.uint32)
         rc = self.L.oracle_step(self.h, now, B.ctypes.data, na.ctypes.data, adm.ctypes.data,
-                                order.ctypes.data, grant.ctypes.data, keys.ctypes.data)
+                                order.ctypes.data, grant.ctypes.data, keys.ctypes.data, toff.ctypes.data)
         return dict(rc=rc, B=B, n_active=na, admitted=adm, order=order.reshape(n, m),
-                    grant=grant.reshape(n, m), keys=keys.reshape(n, m))
+                    grant=grant.reshape(n, m), keys=keys.reshape(n, m), tier_off=toff.reshape(n, 3))
 
     def slots(self, inst: int) -> np.ndarray:
         """[max_active, 6] int32: status, policy, ctx, kv, cpu, pend."""
-        self.L.oracle_step_slot.argtypes = [C.c_void_p, C.c_uint32, C.c_uint32, C.c_void_p]
+        self.L.oracle_step_slots_all.argtypes = [C.c_void_p, C.c_uint32, C.c_void_p]
         out = np.zeros((self.max_active, 6), np.int32)
-        for j in range(self.max_active):
-            self.L.oracle_step_slot(self.h, inst, j, out[j].ctypes.data)
+        self.L.oracle_step_slots_all(self.h, inst, out.ctypes.data)
         return out
 
     def ledger(self, inst: int):

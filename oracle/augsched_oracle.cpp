@@ -508,7 +508,7 @@ double intake_value(const Coef& k, const OInst& ip, bool stage2, int pol, uint64
 }
 
 int step_one(OStep& S, uint32_t i, uint64_t now, int64_t* B_out, uint32_t* n_out,
-             uint32_t* adm_out, uint32_t* order, uint32_t* grant, uint32_t* keys) {
+             uint32_t* adm_out, uint32_t* order, uint32_t* grant, uint32_t* keys, uint32_t* tier_off) {
   SInst& I = S.inst[i];
   const OInst& ip = S.ip[i];
   const OCfg& cfg = S.cfg;
@@ -566,6 +566,9 @@ int step_one(OStep& S, uint32_t i, uint64_t now, int64_t* B_out, uint32_t* n_out
     } else {
       int st = (r.flags >> 4) & 7, pol = (r.flags >> 8) & 3;
       bool st2 = (r.flags >> 12) & 1;
+      // reading B9: a last-scheduled time in the future is a state violation
+      // (Eq.26's wait now - last is a time that has passed, R14/R15)
+      if ((uint64_t)r.last > now) { err = -4; continue; }
       s.V = intake_value(k, ip, st2, pol, r.la, r.lb, r.lc, (double)r.ta, (r.flags & 1) != 0,
                          A_snap);
       s.status = st; s.pol = pol; s.last = r.last;
@@ -648,6 +651,12 @@ int step_one(OStep& S, uint32_t i, uint64_t now, int64_t* B_out, uint32_t* n_out
   *B_out = B;
   *n_out = (uint32_t)ord.size();
   *adm_out = n_prefix;
+  // tier segment starts of the order (running => swapped => waiting)
+  for (int t = 0; t < 3; ++t) {
+    uint32_t c = 0;
+    for (const Ent& e : ord) c += e.tier < t;
+    tier_off[t] = c;
+  }
   return err;
 }
 
@@ -751,13 +760,13 @@ int oracle_step_enqueue(void* h, uint32_t inst, uint32_t n, const uint32_t* kind
   return 0;
 }
 int oracle_step(void* h, uint64_t now, int64_t* B, uint32_t* n_active, uint32_t* admitted,
-                uint32_t* order, uint32_t* grant, uint32_t* keys) {
+                uint32_t* order, uint32_t* grant, uint32_t* keys, uint32_t* tier_off) {
   OStep* S = (OStep*)h;
   int err = 0;
   for (uint32_t i = 0; i < S->n_inst; ++i) {
     size_t off = (size_t)i * S->max_active;
     int e = step_one(*S, i, now, &B[i], &n_active[i], &admitted[i], order + off, grant + off,
-                     keys + off);
+                     keys + off, tier_off + 3 * (size_t)i);
     if (e) err = e;
   }
   return err;
@@ -767,6 +776,10 @@ void oracle_step_slot(void* h, uint32_t inst, uint32_t id, int32_t* out6) {
   const SSlot& s = ((OStep*)h)->inst[inst].s[id];
   out6[0] = s.status; out6[1] = s.pol; out6[2] = (int32_t)s.ctx; out6[3] = (int32_t)s.kv;
   out6[4] = (int32_t)s.cpu; out6[5] = (int32_t)s.pend;
+}
+void oracle_step_slots_all(void* h, uint32_t inst, int32_t* out) {   // [max_active][6]
+  OStep* S = (OStep*)h;
+  for (uint32_t id = 0; id < S->max_active; ++id) oracle_step_slot(h, inst, id, out + 6 * (size_t)id);
 }
 void oracle_step_ledger(void* h, uint32_t inst, int64_t* A, int64_t* P) {
   OStep* S = (OStep*)h;

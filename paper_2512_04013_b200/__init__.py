@@ -30,7 +30,7 @@ NBIN = 160
 RESULT_DTYPE = np.dtype([("f", np.uint64, (len(RESULT_FIELDS),)), ("hist_ttft", np.uint32, (NBIN,)),
                          ("hist_norm", np.uint32, (NBIN,))])
 EXPORTS = ["augsched_create", "augsched_enqueue", "augsched_step", "augsched_step_prefix", "augsched_simulate",
-           "augsched_generate",
+           "augsched_generate", "augsched_step_export",
            "augsched_sync", "augsched_launch_count", "augsched_destroy", "augsched_last_error"]
 
 
@@ -74,7 +74,8 @@ class GenSpec(C.Structure):
 
 
 class StepOut(C.Structure):
-    _fields_ = [(n, C.c_void_p) for n in ("budget", "n_active", "admitted", "order", "grant", "key")]
+    _fields_ = [(n, C.c_void_p) for n in ("budget", "n_active", "admitted", "order", "grant", "key",
+                                          "tier_off")]
 
 
 _lib = None
@@ -96,6 +97,8 @@ def lib():
         L.augsched_generate.argtypes = [vp, C.POINTER(GenSpec), C.POINTER(GenTables), C.POINTER(Trace), u32, u32]
         L.augsched_generate.restype = C.c_int
         L.augsched_sync.argtypes = [vp]
+        L.augsched_step_export.argtypes = [vp, u32, vp, vp]
+        L.augsched_step_export.restype = C.c_int
         L.augsched_launch_count.argtypes = [vp]
         L.augsched_launch_count.restype = u64
         L.augsched_destroy.argtypes = [vp]
@@ -300,7 +303,7 @@ class Scheduler:
         _check(self.L.augsched_sync(self.h))
 
     # ---- simulate ------------------------------------------------------------
-    def simulate(self, traces, inst_trace_id, max_iters: int = 2**62, out=None, resume=False):
+    def simulate(self, traces, inst_trace_id, max_iters: int = 2**32, out=None, resume=False):
         """Device path: traces is a DeviceTraces, inst_trace_id a device int32
         tensor; returns (and fills) a device uint8 tensor of result records.
         Asynchronous on the handle's stream."""
@@ -314,7 +317,7 @@ class Scheduler:
                                         int(max_iters), C.c_void_p(out.data_ptr()), flags))
         return out
 
-    def simulate_host(self, traces, inst_trace_id, max_iters: int = 2**62, resume=False):
+    def simulate_host(self, traces, inst_trace_id, max_iters: int = 2**32, resume=False):
         """End-to-end path: host trace arrays in, host result records out (the
         library stages the copies; the call synchronizes)."""
         ts, keep = host_trace_struct(traces)
@@ -345,16 +348,32 @@ class Scheduler:
         _check(f(self.h, int(now), C.byref(out)))
         return out
 
+    def slots(self, instance: int) -> np.ndarray:
+        """[max_active, 6] int32 slot state (augsched_step_export): status,
+        policy, ctx, kv, cpu, pend -- the layout of oracle.Step.slots()."""
+        out = np.zeros((self.max_active, 6), np.int32)
+        _check(self.L.augsched_step_export(self.h, instance, C.c_void_p(out.ctypes.data), None))
+        return out
+
+    def ledger(self, instance: int):
+        """(A, P) of an instance (augsched_step_export)."""
+        ap = np.zeros(2, np.int64)
+        _check(self.L.augsched_step_export(self.h, instance, None, C.c_void_p(ap.ctypes.data)))
+        return int(ap[0]), int(ap[1])
+
     def step_result(self, out: StepOut) -> dict:
         """Copy one step's outputs to host numpy (synchronizes)."""
         n, m = self.n_instances, self.max_active
         self.sync()
         g = lambda ptr, cnt, dt: device_view(ptr, cnt, dt).cpu().numpy().copy()
-        return dict(B=g(out.budget, n, "<i8"), n_active=g(out.n_active, n, "<u4"),
-                    admitted=g(out.admitted, n, "<u4"),
-                    order=g(out.order, n * m, "<u4").reshape(n, m),
-                    grant=g(out.grant, n * m, "<u4").reshape(n, m),
-                    keys=g(out.key, n * m, "<u4").reshape(n, m))
+        r = dict(B=g(out.budget, n, "<i8"), n_active=g(out.n_active, n, "<u4"),
+                 admitted=g(out.admitted, n, "<u4"),
+                 order=g(out.order, n * m, "<u4").reshape(n, m),
+                 grant=g(out.grant, n * m, "<u4").reshape(n, m),
+                 keys=g(out.key, n * m, "<u4").reshape(n, m))
+        if out.tier_off:
+            r["tier_off"] = g(out.tier_off, 3 * n, "<u4").reshape(n, 3)
+        return r
 
 
 class _CAI:

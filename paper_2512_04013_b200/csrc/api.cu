@@ -267,6 +267,7 @@ int augsched_sync(augsched_t* h) {
   CUDA_TRY(cudaStreamSynchronize(h->stream));
   uint32_t err = 0;
   CUDA_TRY(cudaMemcpy(&err, h->d_err, sizeof(err), cudaMemcpyDeviceToHost));
+  if (err) CUDA_TRY(cudaMemset(h->d_err, 0, sizeof(err)));   // reported once
   if (err & 1u) return fail(AUGSCHED_E_STATE, "a record violated the request state machine");
   if (err & 2u) return fail(AUGSCHED_E_CAPACITY, "a trace is longer than max_active_per_instance");
   if (err & 4u) return fail(AUGSCHED_E_INVALID, "a request has n_seg outside [1, 255]");
@@ -279,6 +280,8 @@ int augsched_simulate(augsched_t* h, const augsched_trace* traces, const uint32_
     return fail(AUGSCHED_E_INVALID, "simulate: NULL argument");
   if (flags & ~(AUGSCHED_HOST_TRACES | AUGSCHED_HOST_RESULTS | AUGSCHED_RESUME))
     return fail(AUGSCHED_E_INVALID, "simulate: unknown flags 0x%x", flags);
+  if (max_iters > (1ull << 32))   // last-scheduled iterations are stored as u32 (R14)
+    return fail(AUGSCHED_E_INVALID, "simulate: max_iters %llu > 2^32", (unsigned long long)max_iters);
   CUDA_TRY(cudaSetDevice(h->device));
   int rc = ensure_sim(h);
   if (rc) return rc;
@@ -378,11 +381,25 @@ int augsched_enqueue(augsched_t* h, uint32_t instance, const augsched_record_soa
   return step_enqueue(h->st, instance, recs, n, recs_on_device, h->stream, h->d_err, &h->launches);
 }
 
+// Iteration indices are stored as u32 last-scheduled times (R14), so `now`
+// must be < 2^32, and time must not run backwards (Eq.26's wait now - last
+// is unsigned).
+static int check_now(augsched_t* h, uint64_t now, const char* who) {
+  if (now >= (1ull << 32)) return fail(AUGSCHED_E_INVALID, "%s: now_iter %llu >= 2^32", who, (unsigned long long)now);
+  if (h->st.have_now && now < h->st.last_now)
+    return fail(AUGSCHED_E_INVALID, "%s: now_iter %llu < previous %llu", who, (unsigned long long)now,
+                (unsigned long long)h->st.last_now);
+  h->st.have_now = true;
+  h->st.last_now = now;
+  return AUGSCHED_OK;
+}
+
 int augsched_step_prefix(augsched_t* h, uint64_t now_iter, augsched_step_out* out) {
   if (!h || !out) return fail(AUGSCHED_E_INVALID, "step_prefix: NULL argument");
   CUDA_TRY(cudaSetDevice(h->device));
   int rc = step_ensure(h->st, h->n_inst, h->max_active, h->stream, h->cfg, h->d_ip, &h->launches);
   if (rc) return rc;
+  if ((rc = check_now(h, now_iter, "step_prefix"))) return rc;
   return step_run_prefix(h->st, h->cfg, h->cap, h->d_ip, h->d_err, now_iter, out, h->stream, &h->launches);
 }
 
@@ -391,7 +408,46 @@ int augsched_step(augsched_t* h, uint64_t now_iter, augsched_step_out* out) {
   CUDA_TRY(cudaSetDevice(h->device));
   int rc = step_ensure(h->st, h->n_inst, h->max_active, h->stream, h->cfg, h->d_ip, &h->launches);
   if (rc) return rc;
+  if ((rc = check_now(h, now_iter, "step"))) return rc;
   return step_run(h->st, h->cfg, h->cap, h->d_ip, h->d_err, now_iter, out, h->stream, &h->launches);
+}
+
+int augsched_step_export(augsched_t* h, uint32_t instance, int32_t* slots, int64_t* ledger) {
+  if (!h) return fail(AUGSCHED_E_INVALID, "step_export: NULL handle");
+  if (instance >= h->n_inst) return fail(AUGSCHED_E_INVALID, "step_export: bad instance %u", instance);
+  CUDA_TRY(cudaSetDevice(h->device));
+  int rc = step_ensure(h->st, h->n_inst, h->max_active, h->stream, h->cfg, h->d_ip, &h->launches);
+  if (rc) return rc;
+  const uint32_t MA = h->max_active;
+  const size_t off = (size_t)instance * MA;
+  if (slots) {
+    std::vector<uint32_t> st(MA);
+    std::vector<int32_t> ctx(MA), kv(MA), cpu(MA), pend(MA);
+    CUDA_TRY(cudaMemcpyAsync(st.data(), h->st.st + off, 4 * (size_t)MA, cudaMemcpyDeviceToHost, h->stream));
+    CUDA_TRY(cudaMemcpyAsync(ctx.data(), h->st.ctx + off, 4 * (size_t)MA, cudaMemcpyDeviceToHost, h->stream));
+    CUDA_TRY(cudaMemcpyAsync(kv.data(), h->st.kv + off, 4 * (size_t)MA, cudaMemcpyDeviceToHost, h->stream));
+    CUDA_TRY(cudaMemcpyAsync(cpu.data(), h->st.cpu + off, 4 * (size_t)MA, cudaMemcpyDeviceToHost, h->stream));
+    CUDA_TRY(cudaMemcpyAsync(pend.data(), h->st.pend + off, 4 * (size_t)MA, cudaMemcpyDeviceToHost, h->stream));
+    CUDA_TRY(cudaStreamSynchronize(h->stream));
+    for (uint32_t x = 0; x < MA; ++x) {
+      const uint32_t sv = st[x] & 15;
+      slots[6 * (size_t)x + 0] = (int32_t)sv;
+      slots[6 * (size_t)x + 1] = sv == ST_NONE ? AUGSCHED_DISCARD : (int32_t)((st[x] >> 4) & 3);
+      slots[6 * (size_t)x + 2] = ctx[x];
+      slots[6 * (size_t)x + 3] = kv[x];
+      slots[6 * (size_t)x + 4] = cpu[x];
+      slots[6 * (size_t)x + 5] = pend[x];
+    }
+  }
+  if (ledger) {
+    long long ap[2];
+    CUDA_TRY(cudaMemcpyAsync(&ap[0], h->st.A + instance, sizeof(long long), cudaMemcpyDeviceToHost, h->stream));
+    CUDA_TRY(cudaMemcpyAsync(&ap[1], h->st.P + instance, sizeof(long long), cudaMemcpyDeviceToHost, h->stream));
+    CUDA_TRY(cudaStreamSynchronize(h->stream));
+    ledger[0] = ap[0];
+    ledger[1] = ap[1];
+  }
+  return AUGSCHED_OK;   // a latched device fault is left for augsched_sync
 }
 
 }  // extern "C"

@@ -35,9 +35,19 @@ __global__ void coef_kernel(augsched_config cfg, const augsched_instance_params*
   if (i < n) coef[i] = make_coef(cfg, ip[i]);
 }
 
-// convert per-instance ids to global slot indices and validate kinds/ids
+// Claim key of record j of a batch (see StepState::claimA): a later batch
+// has a smaller key; within a batch the lower index wins, and in the
+// RETURN/NEW/IMPORT phase a RETURN wins over a NEW/IMPORT (the oracle applies
+// returns first, B6).
+__device__ __forceinline__ unsigned long long claim_key(uint32_t batch, uint32_t prio, uint32_t j) {
+  return ((unsigned long long)(0xFFFFFFFFu - batch) << 32) | ((unsigned long long)prio << 31) | j;
+}
+
+// convert per-instance ids to global slot indices, validate kinds/ids, and
+// claim the record's slot for its phase of the coming batch (records j0 + j)
 __global__ void rec_fix_kernel(const uint32_t* kind, uint32_t* id, uint32_t n, uint32_t inst,
-                               uint32_t MA, uint32_t* err) {
+                               uint32_t MA, uint32_t* err, unsigned long long* claimA,
+                               unsigned long long* claimB, uint32_t batch, uint32_t j0) {
   const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= n) return;
   const uint32_t k = kind[j], x = id[j];
@@ -46,7 +56,10 @@ __global__ void rec_fix_kernel(const uint32_t* kind, uint32_t* id, uint32_t n, u
     id[j] = 0xffffffffu;
     return;
   }
-  id[j] = inst * MA + x;
+  const uint32_t g = inst * MA + x;
+  id[j] = g;
+  if (k == AUGSCHED_K_CALL || k == AUGSCHED_K_FINISH) atomicMin(&claimA[g], claim_key(batch, 0u, j0 + j));
+  else atomicMin(&claimB[g], claim_key(batch, k != AUGSCHED_K_RETURN, j0 + j));
 }
 
 struct Rec {
@@ -64,6 +77,9 @@ struct Slots {
   const augsched_instance_params* ip;
   uint32_t MA;
   uint32_t* wkv;   // sticky: an IMPORT created a KV holder outside running / swapped / Preserve-paused
+  const unsigned long long *claimA, *claimB;   // winning record per slot and phase (duplicates: E_STATE)
+  uint32_t batch;
+  uint32_t* gdirty;   // per instance: grant[] positions [0, gdirty) may be nonzero (the full step clears)
 };
 
 __device__ __forceinline__ void ledger_add(long long* x, long long d) {
@@ -77,6 +93,9 @@ __global__ void rec_phaseA(Rec r, uint32_t n, Slots S, uint32_t* err) {
   if (j >= n) return;
   const uint32_t k = r.kind[j], g = r.id[j];
   if (g == 0xffffffffu || (k != AUGSCHED_K_CALL && k != AUGSCHED_K_FINISH)) return;
+  // a second CALL/FINISH for the same slot in one batch is a state violation
+  // (the oracle applies the first and rejects the rest)
+  if (S.claimA[g] != claim_key(S.batch, 0u, j)) { flag_err(err, 1u); return; }
   const uint32_t inst = g / S.MA;
   const uint32_t st = S.st[g] & 15;
   if (k == AUGSCHED_K_FINISH) {
@@ -108,6 +127,7 @@ __global__ void rec_phaseBC(Rec r, uint32_t n, Slots S, uint64_t now, uint32_t* 
   if (j >= n) return;
   const uint32_t k = r.kind[j], g = r.id[j];
   if (g == 0xffffffffu || k == AUGSCHED_K_CALL || k == AUGSCHED_K_FINISH) return;
+  if (S.claimB[g] != claim_key(S.batch, k != AUGSCHED_K_RETURN, j)) { flag_err(err, 1u); return; }
   const uint32_t inst = g / S.MA;
   const Coef& c = S.coef[inst];
   const uint32_t pm = S.ip[inst].policy_mode;
@@ -135,11 +155,12 @@ __global__ void rec_phaseBC(Rec r, uint32_t n, Slots S, uint64_t now, uint32_t* 
     S.last[g] = (uint32_t)now;
     return;
   }
-  // IMPORT
+  // IMPORT (a last-scheduled time in the future is a state violation:
+  // Eq.26's wait now - last would wrap)
   const uint32_t f = r.flags[j];
   const uint32_t ns = (f >> 4) & 7, pol = (f >> 8) & 3;
   const bool st2 = (f >> 12) & 1;
-  if (ns < ST_RUN || ns > ST_PAUSED || pol > 2) { flag_err(err, 1u); return; }
+  if (ns < ST_RUN || ns > ST_PAUSED || pol > 2 || (uint64_t)r.last[j] > now) { flag_err(err, 1u); return; }
   S.V[g] = st2 ? intake_stage2(c, pm, (int)pol, r.la[j], r.lb[j], r.lc[j], (double)r.ta[j], flag1, Asnap)
                : intake_stage1(c, pm, r.la[j], r.lb[j], (double)r.ta[j], flag1, Asnap);
   S.st[g] = ns | (pol << 4);
@@ -159,7 +180,7 @@ struct KeyArgs {
   uint64_t now;
   unsigned long long* k0;
   uint32_t* ghist;
-  uint32_t* n_active;
+  uint32_t* tcnt;      // [4 * n_inst] queued slots per (instance, tier), zero at entry
   long long* budget;
   int npass;
   PassDesc passes[STEP_MAX_PASS];
@@ -181,7 +202,7 @@ __device__ __forceinline__ uint32_t digit_of(unsigned long long x, const PassDes
 // get tier 3 and sort behind their instance's queue.  Also the token limit of
 // each instance (a3), its queue size and the digit histograms of every sort
 // pass (warp-aggregated shared atomics).
-constexpr int KCNT = 1024;   // per-block instance-count table of the keys kernel
+constexpr int KCNT = 1024;   // per-block (instance, tier) count table of the keys kernel (4 words per instance)
 
 #ifndef AUGSCHED_KEYS_KU
 #define AUGSCHED_KEYS_KU 4
@@ -220,8 +241,8 @@ __global__ void __launch_bounds__(KNT) keys_kernel(KeyArgs a) {
   const uint32_t c0 = blockIdx.x * chunk;
   const uint32_t c1 = c0 + chunk < a.N ? c0 + chunk : a.N;
   const uint32_t i0 = c0 / MA;
-  const bool local_cnt = c1 > c0 && (c1 - 1) / MA - i0 < (uint32_t)KCNT;
-  uint32_t myq = 0;   // queued slots seen by this thread (single-instance handles)
+  const bool local_cnt = c1 > c0 && (c1 - 1) / MA - i0 < (uint32_t)KCNT / 4;
+  uint32_t myq[3] = {0u, 0u, 0u};   // queued slots per tier seen by this thread (single-instance handles)
   if (single) {
     // one instance: its constants in registers, the three scoring words of
     // KU slots loaded together
@@ -247,7 +268,7 @@ __global__ void __launch_bounds__(KNT) keys_kernel(KeyArgs a) {
                                      ((unsigned long long)key << PK_KEY) | s;
         if (s < c1) {
           a.k0[s] = x;
-          myq += tier < 3;
+          if (tier < 3) ++myq[tier];
         }
         for (int p = 0; p < a.npass; ++p)
           hist_add(h + a.passes[p].hoff, s < c1 ? (int)digit_of(x, a.passes[p], MA) : -1);
@@ -278,15 +299,15 @@ __global__ void __launch_bounds__(KNT) keys_kernel(KeyArgs a) {
       const unsigned long long x = ((unsigned long long)tier << PK_TIER) |
                                    ((unsigned long long)key << PK_KEY) | s;
       if (valid) a.k0[s] = x;
-      // queued count per instance
+      // queued count per (instance, tier)
       const bool q = valid && tier < 3;
       {
         const unsigned qm = __ballot_sync(FULL, q);
         if (qm) {
-          const unsigned peers = __match_any_sync(FULL, q ? (int)inst : -1) & qm;
+          const unsigned peers = __match_any_sync(FULL, q ? (int)(inst * 4 + tier) : -1) & qm;
           if (q && lane == __ffs(peers) - 1) {
-            if (local_cnt) atomicAdd(&qcnt[inst - i0], (unsigned)__popc(peers));
-            else atomicAdd(&a.n_active[inst], (unsigned)__popc(peers));
+            if (local_cnt) atomicAdd(&qcnt[(inst - i0) * 4 + tier], (unsigned)__popc(peers));
+            else atomicAdd(&a.tcnt[inst * 4 + tier], (unsigned)__popc(peers));
           }
         }
       }
@@ -298,15 +319,19 @@ __global__ void __launch_bounds__(KNT) keys_kernel(KeyArgs a) {
   }
   if (single) {
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) myq += __shfl_xor_sync(FULL, myq, o);
-    if (lane == 0) atomicAdd(&qcnt[0], myq);
+    for (int t = 0; t < 3; ++t) {
+      uint32_t q = myq[t];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) q += __shfl_xor_sync(FULL, q, o);
+      if (lane == 0 && q) atomicAdd(&qcnt[t], q);
+    }
   }
   __syncthreads();
   for (int b = tid; b < hw; b += KNT)
     if (h[b]) atomicAdd(&a.ghist[b], h[b]);
   if (local_cnt)
-    for (uint32_t b = tid; b <= (c1 - 1) / MA - i0; b += KNT)
-      if (qcnt[b]) atomicAdd(&a.n_active[i0 + b], qcnt[b]);
+    for (uint32_t b = tid; b < 4 * ((c1 - 1) / MA - i0 + 1); b += KNT)
+      if (qcnt[b]) atomicAdd(&a.tcnt[4 * i0 + b], qcnt[b]);
 }
 
 // ------------------------------------------------------------------ sort pass
@@ -534,8 +559,12 @@ constexpr int ANW = ANT / 32;
 //       fit the free KV memory (R20)
 //   S9  last = now and the granted batch's token accounting (decode adds one
 //       token; the engine reports segment ends with CALL / FINISH records)
+//   out  n_active and the per-tier segment starts (from the keys kernel's
+//        per-tier counts); grant[j] = 0 for j >= the admitted prefix (the
+//        previous step's grants beyond it are cleared)
 __global__ void __launch_bounds__(ANT) admit_kernel(Slots S, augsched_config cfg, int64_t cap, uint64_t now,
-                                                    const long long* budget, const uint32_t* n_active,
+                                                    const long long* budget, const uint32_t* tcnt,
+                                                    uint32_t* n_active, uint32_t* tier_off,
                                                     const uint32_t* order, uint32_t* grant,
                                                     uint32_t* admitted) {
   __shared__ unsigned long long wsum[ANW + 1];
@@ -546,7 +575,9 @@ __global__ void __launch_bounds__(ANT) admit_kernel(Slots S, augsched_config cfg
   const uint32_t MA = S.MA;
   const size_t base = (size_t)i * MA;
   const long long B = budget[i];
-  const uint32_t n = n_active[i];
+  const uint32_t c0 = tcnt[4 * i], c1 = tcnt[4 * i + 1], c2 = tcnt[4 * i + 2];
+  const uint32_t n = c0 + c1 + c2;
+  const uint32_t prev_adm = S.gdirty[i];   // earlier steps' grants live in [0, prev_adm)
   // ---- a6 admission
   unsigned long long Prun = 0, gsum = 0;
   uint32_t adm = 0;
@@ -646,10 +677,17 @@ __global__ void __launch_bounds__(ANT) admit_kernel(Slots S, augsched_config cfg
     S.last[g] = (uint32_t)now;
     S.st[g] = ST_RUN | (S.st[g] & 0x30u);
   }
+  // grants beyond the prefix: zero (the previous step wrote [0, prev_adm))
+  for (uint32_t j = adm + tid; j < prev_adm && j < MA; j += ANT) grant[base + j] = 0;
   unsigned long long tot;
   block_incl_scan_u64<ANT>(dA, wsum, &tot);
   if (tid == 0) {
     admitted[i] = adm;
+    S.gdirty[i] = adm;
+    n_active[i] = n;
+    tier_off[3 * i] = 0;
+    tier_off[3 * i + 1] = c0;
+    tier_off[3 * i + 2] = c0 + c1;
     const long long a = ld_ll(&S.A[i]) + (long long)tot;
     S.A[i] = a;
     S.Aevt[i] = a;
@@ -1017,6 +1055,7 @@ __device__ void pf_finish(const Slots& S, const augsched_config& cfg, int64_t ca
   block_incl_scan_u64<NT>(dA, wsum, &tot);
   if (tid == 0) {
     admitted[inst] = adm;
+    if (S.gdirty[inst] < adm) S.gdirty[inst] = adm;
     const long long a = ld_ll(&S.A[inst]) + (long long)tot;
     S.A[inst] = a;
     S.Aevt[inst] = a;
@@ -1578,7 +1617,7 @@ int grow_records(StepState& st, uint32_t need, cudaStream_t s) {
 
 Slots slots_of(StepState& st, const augsched_instance_params* d_ip) {
   return Slots{st.st, st.V, st.last, st.ctx, st.kv, st.cpu, st.pend, st.A, st.P, st.Aevt, st.Asnap,
-               st.coef, d_ip, st.max_active, st.wkv};
+               st.coef, d_ip, st.max_active, st.wkv, st.claimA, st.claimB, st.rec_batch, st.gdirty};
 }
 
 }  // namespace
@@ -1609,7 +1648,7 @@ int step_ensure(StepState& st, uint32_t n_inst, uint32_t max_active, cudaStream_
   add(0, PK_KEY + 24, 10);
   for (uint32_t x = n_inst - 1, b = 0; x > 0; x >>= 8, ++b) add(2, (int)(8 * b), 8);
   if (hoff > STEP_HIST_WORDS) return set_error(AUGSCHED_E_CAPACITY, "step: too many sort passes");
-  const size_t zwords = (size_t)n_inst + STEP_HIST_WORDS + STEP_MAX_PASS + PF_NCNT;
+  const size_t zwords = 4 * (size_t)n_inst + STEP_HIST_WORDS + STEP_MAX_PASS + PF_NCNT;
   int rc;
   if ((rc = salloc(st, &st.st, N)) || (rc = salloc(st, &st.V, N)) || (rc = salloc(st, &st.last, N)) ||
       (rc = salloc(st, &st.ctx, N)) || (rc = salloc(st, &st.kv, N)) || (rc = salloc(st, &st.cpu, N)) ||
@@ -1626,30 +1665,45 @@ int step_ensure(StepState& st, uint32_t n_inst, uint32_t max_active, cudaStream_
       (rc = salloc(st, &st.pf_A, PF_SCAP)) || (rc = salloc(st, &st.pf_C, N)) ||
       (rc = salloc(st, &st.gslot, N)) || (rc = salloc(st, &st.pf_theta, 2 * (size_t)n_inst)) ||
       (rc = salloc(st, &st.pf_H, PF_HCAP)) || (rc = salloc(st, &st.wkv, 1)) ||
-      (rc = salloc(st, &st.pf_nact, 2)))
+      (rc = salloc(st, &st.pf_nact, 2)) || (rc = salloc(st, &st.n_active, n_inst)) ||
+      (rc = salloc(st, &st.tier_off, 3 * (size_t)n_inst)) || (rc = salloc(st, &st.claimA, N)) ||
+      (rc = salloc(st, &st.claimB, N)) || (rc = salloc(st, &st.gdirty, n_inst)))
     return rc;
-  cudaMemsetAsync(st.zbuf, 0, sizeof(uint32_t) * zwords, s);   // the prefix kernel expects clear counters
-  cudaMemsetAsync(st.pf_nact, 0, 2 * sizeof(uint32_t), s);
-  st.pf_epoch = 0;
-  cudaMemsetAsync(st.wkv, 0, sizeof(uint32_t), s);
-  cudaMemsetAsync(st.pf_theta, 0xFF, 2 * sizeof(unsigned long long) * (size_t)n_inst, s);   // no anchor: every slot
-  // one memset per step clears the queue counts, histograms and tile counters
+  // one memset per full step clears the tier counts, histograms and tile counters
   st.zwords = zwords;
-  st.n_active = st.zbuf;
-  st.ghist = st.zbuf + n_inst;
+  st.tcnt = st.zbuf;
+  st.ghist = st.zbuf + 4 * (size_t)n_inst;
   st.tile_ctr = st.ghist + STEP_HIST_WORDS;
   st.pf_cnt = st.tile_ctr + STEP_MAX_PASS;
-  cudaMemsetAsync(st.gslot, 0, sizeof(uint32_t) * N, s);
-  cudaMemsetAsync(st.st, 0, sizeof(uint32_t) * N, s);
-  cudaMemsetAsync(st.ctx, 0, sizeof(int32_t) * N, s);
-  cudaMemsetAsync(st.kv, 0, sizeof(int32_t) * N, s);
-  cudaMemsetAsync(st.cpu, 0, sizeof(int32_t) * N, s);
-  cudaMemsetAsync(st.pend, 0, sizeof(int32_t) * N, s);
-  cudaMemsetAsync(st.A, 0, sizeof(long long) * n_inst, s);
-  cudaMemsetAsync(st.P, 0, sizeof(long long) * n_inst, s);
-  cudaMemsetAsync(st.Aevt, 0, sizeof(long long) * n_inst, s);
-  cudaMemsetAsync(st.lb_status, 0, sizeof(unsigned long long) * ((size_t)st.n_tiles << STEP_RB_MAX), s);
-  cudaMemsetAsync(st.lb_gstatus, 0, sizeof(unsigned long long) * ((size_t)st.n_tiles << STEP_RB_MAX), s);
+  st.pf_epoch = 0;
+  st.rec_batch = 0;
+  struct Z { void* p; int v; size_t n; };
+  const Z zs[] = {
+      {st.zbuf, 0, sizeof(uint32_t) * zwords},            // the prefix kernel expects clear counters
+      {st.pf_nact, 0, 2 * sizeof(uint32_t)},
+      {st.wkv, 0, sizeof(uint32_t)},
+      {st.pf_theta, 0xFF, 2 * sizeof(unsigned long long) * (size_t)n_inst},   // no anchor: every slot
+      {st.claimA, 0xFF, sizeof(unsigned long long) * N},  // no claim: larger than every key
+      {st.claimB, 0xFF, sizeof(unsigned long long) * N},
+      {st.gslot, 0, sizeof(uint32_t) * N},
+      {st.st, 0, sizeof(uint32_t) * N},
+      {st.ctx, 0, sizeof(int32_t) * N},
+      {st.kv, 0, sizeof(int32_t) * N},
+      {st.cpu, 0, sizeof(int32_t) * N},
+      {st.pend, 0, sizeof(int32_t) * N},
+      {st.grant, 0, sizeof(uint32_t) * N},                // grant[j] = 0 beyond the admitted prefix
+      {st.admitted, 0, sizeof(uint32_t) * n_inst},
+      {st.gdirty, 0, sizeof(uint32_t) * n_inst},
+      {st.n_active, 0, sizeof(uint32_t) * n_inst},
+      {st.tier_off, 0, 3 * sizeof(uint32_t) * n_inst},
+      {st.A, 0, sizeof(long long) * n_inst},
+      {st.P, 0, sizeof(long long) * n_inst},
+      {st.Aevt, 0, sizeof(long long) * n_inst},
+      {st.lb_status, 0, sizeof(unsigned long long) * ((size_t)st.n_tiles << STEP_RB_MAX)},
+      {st.lb_gstatus, 0, sizeof(unsigned long long) * ((size_t)st.n_tiles << STEP_RB_MAX)},
+  };
+  for (const Z& z : zs)
+    if ((rc = cuda_check(cudaMemsetAsync(z.p, z.v, z.n, s), "step_ensure: clear"))) return rc;
   st.G = 1;
   while ((uint64_t)st.G * st.G < st.n_tiles) ++st.G;   // ~sqrt(tiles) tiles per look-back group
   coef_kernel<<<(n_inst + 255) / 256, 256, 0, s>>>(cfg, d_ip, st.coef, n_inst);
@@ -1697,7 +1751,8 @@ int step_enqueue(StepState& st, uint32_t inst, const augsched_record_soa* r, uin
   cudaError_t e = cudaMemcpyAsync(st.r_ta + st.r_n, r->ta, sizeof(float) * n, kind, s);
   if (e != cudaSuccess) return cuda_check(e, "enqueue copy");
   rec_fix_kernel<<<(n + 255) / 256, 256, 0, s>>>(st.r_kind + st.r_n, st.r_id + st.r_n, n, inst,
-                                                 st.max_active, d_err);
+                                                 st.max_active, d_err, st.claimA, st.claimB,
+                                                 st.rec_batch + 1, st.r_n);
   *launches += 1;
   st.r_n += n;
   if (!on_dev) {
@@ -1711,9 +1766,10 @@ int step_enqueue(StepState& st, uint32_t inst, const augsched_record_soa* r, uin
 
 namespace {
 // Engine events of the last forward, snapshot, returns / arrivals / imports.
-void run_records(StepState& st, const Slots& S, uint32_t* d_err, uint64_t now, cudaStream_t s,
+void run_records(StepState& st, Slots S, uint32_t* d_err, uint64_t now, cudaStream_t s,
                  uint64_t* launches) {
   if (!st.r_n) return;
+  S.batch = ++st.rec_batch;   // the batch the pending records claimed their slots for
   const uint32_t ni = st.n_inst;
   Rec r{st.r_kind, st.r_id, st.r_la, st.r_lb, st.r_lc, st.r_flags, st.r_last, st.r_ctx, st.r_kv,
         st.r_cpu, st.r_pend, st.r_ta};
@@ -1758,12 +1814,14 @@ int step_run_prefix(StepState& st, const augsched_config& cfg, int64_t cap,
     out->order = st.order;
     out->grant = st.grant;
     out->key = st.key;
+    out->tier_off = nullptr;
     return cuda_check(cudaGetLastError(), "step_prefix");
   }
   // no memset: the kernel leaves its counters cleared for the next call
   // (a full step in between leaves its histograms behind: clear once)
   if (st.pf_dirty) {
-    cudaMemsetAsync(st.zbuf, 0, sizeof(uint32_t) * st.zwords, s);
+    const int rc = cuda_check(cudaMemsetAsync(st.zbuf, 0, sizeof(uint32_t) * st.zwords, s), "step_prefix: clear");
+    if (rc) return rc;
     st.pf_dirty = false;
   }
   if (++st.pf_epoch >= (1u << 30)) st.pf_epoch = 1;
@@ -1785,6 +1843,7 @@ int step_run_prefix(StepState& st, const augsched_config& cfg, int64_t cap,
   out->order = st.order;
   out->grant = st.grant;
   out->key = st.key;
+  out->tier_off = nullptr;
   return cuda_check(cudaGetLastError(), "step_prefix");
 }
 
@@ -1795,10 +1854,11 @@ int step_run(StepState& st, const augsched_config& cfg, int64_t cap,
   const uint32_t ni = st.n_inst;
   run_records(st, S, d_err, now, s, launches);
   st.pf_dirty = true;
-  cudaMemsetAsync(st.zbuf, 0, sizeof(uint32_t) * st.zwords, s);
+  int rc = cuda_check(cudaMemsetAsync(st.zbuf, 0, sizeof(uint32_t) * st.zwords, s), "step: clear");
+  if (rc) return rc;
   KeyArgs ka;
   ka.S = S; ka.cfg = cfg; ka.cap = cap; ka.now = now; ka.k0 = st.k0;
-  ka.ghist = st.ghist; ka.n_active = st.n_active; ka.budget = st.budget; ka.npass = st.npass;
+  ka.ghist = st.ghist; ka.tcnt = st.tcnt; ka.budget = st.budget; ka.npass = st.npass;
   for (int p = 0; p < st.npass; ++p) ka.passes[p] = st.passes[p];
   ka.N = (uint32_t)st.N;
   const size_t kblocks = (st.N + KNT * KU - 1) / (KNT * KU);
@@ -1819,8 +1879,8 @@ int step_run(StepState& st, const augsched_config& cfg, int64_t cap,
     *launches += 1;
     unsigned long long* t = kin; kin = kout; kout = t;
   }
-  admit_kernel<<<ni, ANT, 0, s>>>(S, cfg, cap, now, st.budget, st.n_active, st.order, st.grant,
-                                  st.admitted);
+  admit_kernel<<<ni, ANT, 0, s>>>(S, cfg, cap, now, st.budget, st.tcnt, st.n_active, st.tier_off, st.order,
+                                  st.grant, st.admitted);
   *launches += 1;
   out->budget = reinterpret_cast<const int64_t*>(st.budget);
   out->n_active = st.n_active;
@@ -1828,6 +1888,7 @@ int step_run(StepState& st, const augsched_config& cfg, int64_t cap,
   out->order = st.order;
   out->grant = st.grant;
   out->key = st.key;
+  out->tier_off = st.tier_off;
   return cuda_check(cudaGetLastError(), "step");
 }
 

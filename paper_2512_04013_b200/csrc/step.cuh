@@ -55,10 +55,20 @@ struct StepState {
            *r_cpu = nullptr, *r_pend = nullptr;
   float* r_ta = nullptr;
   uint32_t r_cap = 0, r_n = 0;
+  uint64_t last_now = 0;         // last `now` passed to a step (time must not run backwards)
+  bool have_now = false;
+  // duplicate-record detection: per slot, the winning record of the batch in
+  // each record phase (CALL/FINISH; RETURN/NEW/IMPORT), key
+  // (~batch << 32) | prio << 31 | index, atomicMin
+  unsigned long long *claimA = nullptr, *claimB = nullptr;
+  uint32_t rec_batch = 0;        // batches processed so far
   // outputs
   long long* budget = nullptr;
   uint32_t *n_active = nullptr, *admitted = nullptr, *order = nullptr, *grant = nullptr,
            *key = nullptr, *flag = nullptr;
+  uint32_t* tcnt = nullptr;      // [4 * n_inst] per-tier queue counts of the full step (zeroed each step)
+  uint32_t* tier_off = nullptr;  // [3 * n_inst] per-tier segment starts (full step output)
+  uint32_t* gdirty = nullptr;    // [n_inst] grant[] positions [0, gdirty) may hold grants of earlier steps
   // sort scratch
   unsigned long long *k0 = nullptr, *k1 = nullptr;   // packed tier:2 | key:32 | slot:30
   unsigned long long* lb_status = nullptr;           // [tiles][1 << STEP_RB_MAX] tile aggregates

@@ -15,7 +15,7 @@ if not torch.cuda.is_available():
 import paper_2512_04013_b200 as aug  # noqa: E402
 
 
-def gpu_run(cfg, ip, tr, tid, max_iters=2**62, windows=None):
+def gpu_run(cfg, ip, tr, tid, max_iters=2**32, windows=None):
     n = len(tid)
     ma = int(max(tr.trace_len(i) for i in range(tr.n_traces)))
     s = aug.Scheduler(cfg, ip, n, max(ma, 1))
@@ -113,7 +113,7 @@ def test_resume_windows_equal_full_run():
     ip = tracegen.inst_params(4, alpha=[0.0, 4.6e7, 0.0, 4.6e7])
     tid = [0, 0, 1, 1]
     full, _ = gpu_run(tracegen.PRESET_7B, ip, tr, tid)
-    win, _ = gpu_run(tracegen.PRESET_7B, ip, tr, tid, windows=[500, 1234, 5000, 2**62])
+    win, _ = gpu_run(tracegen.PRESET_7B, ip, tr, tid, windows=[500, 1234, 5000, 2**32])
     assert full.tobytes() == win.tobytes()
     cut, _ = gpu_run(tracegen.PRESET_7B, ip, tr, tid, max_iters=3000)
     o = oracle.simulate(tracegen.PRESET_7B, ip, tr, tid, max_iters=3000)
@@ -232,4 +232,16 @@ def test_n_seg_above_255_is_rejected():
     with pytest.raises(aug.AugschedError) as e:
         s.simulate_host(tr, [0])
     assert e.value.code == aug.E_INVALID
+    s.close()
+
+
+def test_max_iters_above_2_32_is_rejected():
+    """Last-scheduled iterations are stored as u32 (R14): max_iters > 2^32
+    is rejected instead of silently wrapping."""
+    tr = tracegen.from_requests([[R(0, 5, [(2,)])]])
+    s = aug.Scheduler(tracegen.PRESET_G0, tracegen.inst_params(1, base=tracegen.INST_G0), 1, 4)
+    with pytest.raises(aug.AugschedError) as e:
+        s.simulate_host(tr, [0], max_iters=2**32 + 1)
+    assert e.value.code == aug.E_INVALID
+    s.simulate_host(tr, [0], max_iters=2**32)
     s.close()

@@ -30,7 +30,18 @@ def compare(g, o, n_inst, label, prefix=False):
         assert np.array_equal(g["keys"][i, :n], o["keys"][i, :n]), f"{label}: keys inst {i}"
         assert np.array_equal(g["grant"][i, :a], o["grant"][i, :a]), f"{label}: grant inst {i}"
         if not prefix:
-            assert not o["grant"][i, a:n].any()
+            # the full step writes zero grants beyond the admitted prefix
+            assert not g["grant"][i, a:n].any(), f"{label}: stale grant beyond the prefix, inst {i}"
+            assert np.array_equal(g["tier_off"][i], o["tier_off"][i]), f"{label}: tier offsets inst {i}"
+
+
+def compare_slots(s, st, n_inst, label):
+    """GPU slot state (augsched_step_export) and ledger equal the oracle's."""
+    for i in range(n_inst):
+        gs, os_ = s.slots(i), st.slots(i)
+        assert np.array_equal(gs, os_), f"{label}: slot state inst {i}: rows " \
+            f"{np.nonzero((gs != os_).any(1))[0][:8]}"
+        assert s.ledger(i) == st.ledger(i), f"{label}: ledger inst {i}"
 
 
 def test_G3_gpu():
@@ -99,6 +110,7 @@ def test_random_event_stream(seed, cap):
         assert o["rc"] == 0
         g = s.step_result(s.step(t))
         compare(g, o, n_inst, f"seed {seed} step {t}")
+        compare_slots(s, st, n_inst, f"seed {seed} step {t}")
     s.close()
 
 
@@ -156,6 +168,7 @@ def test_prefix_step_event_stream(seed, cap, ranking):
         assert o["rc"] == 0
         g = s.step_result(s.step(t, prefix=True))
         compare(g, o, 1, f"prefix seed {seed} step {t}", prefix=True)
+        compare_slots(s, st, 1, f"prefix seed {seed} step {t}")
     s.close()
 
 
@@ -280,4 +293,143 @@ def test_prefix_step_multi_instance_event_stream(seed, cap):
         assert o["rc"] == 0
         g = s.step_result(s.step(t, prefix=True))
         compare(g, o, n_inst, f"multi prefix seed {seed} step {t}", prefix=True)
+        compare_slots(s, st, n_inst, f"multi prefix seed {seed} step {t}")
+    s.close()
+
+
+# ------------------------------------------------------------------ round-2 boundary checks
+def _g0(cap=10**6):
+    return dict(tracegen.PRESET_G0, g_total=1000 + cap, g_model=1000)
+
+
+def _imp(rows):
+    n = len(rows)
+    col = lambda k, d=0: [r.get(k, d) for r in rows]
+    return oracle.records(n, kind=col("kind", oracle.K_IMPORT), id=col("id"), la=col("la", 1), lb=col("lb", 1),
+                          flags=[(r.get("st", 3) << 4) | (r.get("pol", 2) << 8) for r in rows],
+                          last=col("last"), ctx=col("ctx"), kv=col("kv"), cpu=col("cpu"), pend=col("pend"))
+
+
+@pytest.mark.parametrize("prefix", [False, True])
+def test_r2_golden_pins_on_gpu(prefix):
+    """The hand-worked step-mode goldens P3 (demotion order) and P4
+    (eviction of a slot mid swap-in; admitted = prefix length with a
+    cancelled grant inside it) of tests/golden/r2_pins.json, on the GPU."""
+    import json
+    import os
+    G = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "r2_pins.json")))
+    g3 = G["P3_demotion_order_step"]
+    s = aug.Scheduler(_g0(61), tracegen.inst_params(1, base=tracegen.INST_G0, l_static=100), 1, 5)
+    s.enqueue(0, _imp([dict(id=0, st=4, pol=0, ctx=15, kv=15), dict(id=1, st=4, pol=0, ctx=5, kv=5),
+                       dict(id=2, st=4, pol=0, ctx=15, kv=15), dict(id=3, st=1, ctx=10, kv=10, la=1, lb=1),
+                       dict(id=4, st=3, pend=25, la=25, lb=1)]))
+    g = s.step_result(s.step(10, prefix=prefix))
+    assert int(g["admitted"][0]) == g3["admitted"] and int(g["n_active"][0]) == g3["n_active"]
+    assert g["order"][0][:2].tolist() == g3["order"] and g["grant"][0][:2].tolist() == g3["grant"]
+    assert s.slots(0).tolist() == g3["slots_after"]
+    assert s.ledger(0) == (g3["ledger_after"]["A"], g3["ledger_after"]["P"])
+    s.close()
+    g4 = G["P4_evict_mid_swapin_step"]
+    s = aug.Scheduler(_g0(55), tracegen.inst_params(1, base=tracegen.INST_G0, l_static=100), 1, 2)
+    s.enqueue(0, _imp([dict(id=0, st=1, ctx=10, kv=10, la=1, lb=1),
+                       dict(id=1, st=1, ctx=100, kv=40, cpu=60, la=2, lb=2)]))
+    for now, key in ((10, "step1"), (11, "step2")):
+        g = s.step_result(s.step(now, prefix=prefix))
+        w = g4[key]
+        assert int(g["admitted"][0]) == w["admitted"]
+        assert g["order"][0].tolist() == w["order"] and g["grant"][0].tolist() == w["grant"]
+        assert s.slots(0).tolist() == w["slots_after"]
+        assert s.ledger(0) == (w["ledger_after"]["A"], w["ledger_after"]["P"])
+    s.close()
+
+
+def test_stale_grants_cleared_by_full_step():
+    """a full step after a step with a longer admitted prefix
+    writes zeros (not the old grants) at the positions beyond its own prefix."""
+    cfg = _g0()
+    ip = tracegen.inst_params(1, base=tracegen.INST_G0, l_static=100)
+    for pre0 in (True, False):
+        st = oracle.Step(cfg, ip, 16)
+        s = aug.Scheduler(cfg, ip, 1, 16)
+        rec = _imp([dict(id=j, st=3, pend=5, la=5, lb=1) for j in range(8)])
+        st.enqueue(0, rec)
+        s.enqueue(0, rec)
+        o = st.step(0)
+        g = s.step_result(s.step(0, prefix=pre0))
+        compare(g, o, 1, "stale t0", prefix=pre0)
+        assert int(g["admitted"][0]) == 8
+        rec = oracle.records(12, kind=[oracle.K_FINISH] * 6 + [oracle.K_NEW] * 6, id=list(range(6)) + list(range(8, 14)),
+                             la=[0] * 6 + [200] * 6, lb=[0] * 6 + [1] * 6)
+        st.enqueue(0, rec)
+        s.enqueue(0, rec)
+        o = st.step(1)
+        g = s.step_result(s.step(1))
+        assert int(o["admitted"][0]) == 3 and int(o["n_active"][0]) == 8
+        compare(g, o, 1, "stale t1")
+        s.close()
+
+
+def test_duplicate_slot_records_are_state_violations():
+    """two records for one slot in the same record phase (CALL +
+    FINISH, two FINISHes, two NEWs, RETURN + NEW) are state violations: the
+    first in the oracle's processing order applies, the others are rejected
+    with E_STATE, and every slot's state equals the oracle's."""
+    cfg = _g0()
+    ip = tracegen.inst_params(1, base=tracegen.INST_G0, l_static=1000)
+    st = oracle.Step(cfg, ip, 8)
+    s = aug.Scheduler(cfg, ip, 1, 8)
+    init = _imp([dict(id=0, st=1, ctx=10, kv=10), dict(id=1, st=1, ctx=12, kv=12),
+                 dict(id=2, st=4, pol=2, ctx=20), dict(id=3, st=3, pend=4, la=4)])
+    st.enqueue(0, init)
+    s.enqueue(0, init)
+    st.step(0)
+    s.step_result(s.step(0))
+    K = oracle
+    dup = oracle.records(7, kind=[K.K_CALL, K.K_FINISH, K.K_FINISH, K.K_FINISH, K.K_NEW, K.K_NEW, K.K_RETURN],
+                         id=[0, 0, 1, 1, 5, 5, 2], la=[0, 0, 0, 0, 7, 9, 3], lb=[0, 0, 0, 0, 2, 2, 1],
+                         ta=[0.0, 0, 0, 0, 0, 0, 0])
+    # RETURN + NEW on slot 2 (paused): the return applies, the NEW is rejected
+    dup2 = oracle.records(1, kind=[K.K_NEW], id=[2], la=[5], lb=[1])
+    for r in (dup, dup2):
+        st.enqueue(0, r)
+        s.enqueue(0, r)
+    o = st.step(1)
+    assert o["rc"] == -4
+    s.step(1)
+    with pytest.raises(aug.AugschedError) as e:
+        s.sync()
+    assert e.value.code == aug.E_STATE
+    assert np.array_equal(s.slots(0), st.slots(0))
+    assert s.ledger(0) == st.ledger(0)
+    s.close()
+
+
+def test_import_last_in_the_future_is_rejected():
+    cfg = _g0()
+    ip = tracegen.inst_params(1, base=tracegen.INST_G0)
+    st = oracle.Step(cfg, ip, 4)
+    s = aug.Scheduler(cfg, ip, 1, 4)
+    rec = _imp([dict(id=0, st=3, pend=5, last=7), dict(id=1, st=3, pend=5, last=3)])
+    st.enqueue(0, rec)
+    s.enqueue(0, rec)
+    assert st.step(5)["rc"] == -4
+    s.step(5)
+    with pytest.raises(aug.AugschedError) as e:
+        s.sync()
+    assert e.value.code == aug.E_STATE
+    assert np.array_equal(s.slots(0), st.slots(0))
+    s.close()
+
+
+def test_now_must_fit_u32_and_not_run_backwards():
+    s = aug.Scheduler(_g0(), tracegen.inst_params(1, base=tracegen.INST_G0), 1, 4)
+    with pytest.raises(aug.AugschedError) as e:
+        s.step(2**32)
+    assert e.value.code == aug.E_INVALID
+    s.step(10)
+    with pytest.raises(aug.AugschedError) as e:
+        s.step(9, prefix=True)
+    assert e.value.code == aug.E_INVALID
+    s.step(10)        # equal is fine
+    s.sync()
     s.close()
