@@ -355,6 +355,18 @@ struct SortArgs {
 // Lanes of the warp holding the same RB-bit digit as this lane (d < 0: the
 // lane holds no item and is in no other lane's set).  RB + 1 ballots; the
 // __match_any_sync variant is kept for comparison (AUGSCHED_SORT_BALLOT=0).
+// All 32 lanes hold an item: RB ballots.
+template <int RB>
+__device__ __forceinline__ unsigned digit_peers_full(uint32_t d) {
+  unsigned m = FULL;
+#pragma unroll
+  for (int b = 0; b < RB; ++b) {
+    const unsigned v = __ballot_sync(FULL, (d >> b) & 1u);
+    m &= ((d >> b) & 1u) ? v : ~v;
+  }
+  return m;
+}
+
 template <int RB>
 __device__ __forceinline__ unsigned digit_peers(int d) {
 #if AUGSCHED_SORT_BALLOT
@@ -869,21 +881,26 @@ __device__ __forceinline__ void pf_sortE(unsigned long long* sbuf, unsigned long
   for (int e = 0; e < E; ++e) sbuf[threadIdx.x + e * NT] = v[e];
 }
 
-template <int NT, int EM>
+// SORTED: sbuf already holds the instance's whole order (the full-order
+// batched step); `keys` then holds the same sorted words and nkeys = their
+// count (otherwise keys are slot-indexed and nkeys = MA).
+template <int NT, int EM, bool SORTED = false>
 __device__ void pf_finish(const Slots& S, const augsched_config& cfg, int64_t cap, uint64_t now, uint32_t inst,
                           size_t base, const unsigned long long* keys, unsigned long long* sbuf,
                           unsigned long long* xch, uint32_t mt, uint32_t target, long long B, uint32_t* order,
                           uint32_t* keyout, uint32_t* grant, uint32_t* admitted, uint32_t* gslot, SelShm& sel,
                           unsigned long long* wsum, unsigned long long& freed,
-                          const unsigned long long* H = nullptr, uint32_t nH = 0) {
+                          const unsigned long long* H = nullptr, uint32_t nH = 0, uint32_t nkeys = 0xFFFFFFFFu) {
   const int tid = threadIdx.x;
   const uint32_t MA = S.MA;
+  if (nkeys == 0xFFFFFFFFu) nkeys = MA;
   // ---- bitonic sort of the prefix, padded to a power of two P2 <= EM * NT:
   // one word per thread up to P2 = NT (<= 1,024), else E = P2 / NT words per
   // thread; both networks fully unrolled per size.
   uint32_t P2 = 32;
   while (P2 < mt) P2 <<= 1;
-  if (P2 <= (uint32_t)NT && P2 <= 1024u) {
+  if (SORTED) {
+  } else if (P2 <= (uint32_t)NT && P2 <= 1024u) {
     if ((uint32_t)tid < P2) {
       unsigned long long v = (uint32_t)tid < mt ? sbuf[tid] : ~0ull;
       bar_named(P2);
@@ -914,13 +931,24 @@ __device__ void pf_finish(const Slots& S, const augsched_config& cfg, int64_t ca
   // ---- a6 admission over the prefix (P_{j-1} < B, partial last, R17)
   unsigned long long Prun = 0, gsum = 0;
   uint32_t adm = 0;
+  // token state of the next round's entries is loaded before this round's
+  // scan (one round of lookahead hides the gather latency)
+  int32_t nx_ctx = 0, nx_kv = 0, nx_cpu = 0, nx_pend = 0;
+  uint32_t nx_slot = 0;
+  if ((uint32_t)tid < m) {
+    nx_slot = (uint32_t)sbuf[tid] & SLOT_MASK;
+    const size_t g = base + nx_slot;
+    nx_ctx = S.ctx[g]; nx_kv = S.kv[g]; nx_cpu = S.cpu[g]; nx_pend = S.pend[g];
+  }
   for (uint32_t j0 = 0; j0 < m && (long long)Prun < B; j0 += NT) {
     const uint32_t j = j0 + tid;
     unsigned long long d = 0;
-    uint32_t slot = 0;
-    if (j < m) {
-      slot = (uint32_t)sbuf[j] & SLOT_MASK;
-      d = slot_demand(S, (uint32_t)(base + slot), cfg.s_in);
+    const uint32_t slot = nx_slot;
+    if (j < m) d = demand_of(nx_ctx, nx_kv, nx_cpu, nx_pend, cfg.s_in);
+    if (j + NT < m) {
+      nx_slot = (uint32_t)sbuf[j + NT] & SLOT_MASK;
+      const size_t g = base + nx_slot;
+      nx_ctx = S.ctx[g]; nx_kv = S.kv[g]; nx_cpu = S.cpu[g]; nx_pend = S.pend[g];
     }
     unsigned long long tot;
     const unsigned long long inc = block_incl_scan_u64<NT>(d, wsum, &tot);
@@ -1005,7 +1033,7 @@ __device__ void pf_finish(const Slots& S, const augsched_config& cfg, int64_t ca
         key = ~kx;
         return w > 0;
       };
-      const uint32_t ne = H ? nH + adm : MA;
+      const uint32_t ne = H ? nH + adm : nkeys;
       wselect<NT>(sel, ne, (uint64_t)((long long)need - fr), 64, gete);
       const bool f1 = sel.r.found != 0;
       const uint64_t k1 = sel.r.k;
@@ -1557,6 +1585,184 @@ __global__ void __launch_bounds__(NT) pf_multi_kernel(Slots S, augsched_config c
   }
 }
 
+
+// Full-order step of a multi-instance handle (the batched scheduler): one CTA
+// per instance sorts all of the instance's packed words in shared memory --
+// a stable LSD radix sort of the 34-bit (tier, key) field above the slot
+// (digits of 9, 9, 8 and 8 bits), each warp ranking a contiguous run of
+// E x 32 words with ballot-built digit-peer masks and warp-private digit
+// counters, one block scan of the (digit, warp) counters per pass -- then
+// admission / resolution / grant accounting (pf_finish over the sorted
+// words), and writes the whole order, keys, zero grants beyond the prefix,
+// the queue size and the per-tier segment starts.  Words of slots that are
+// not queued carry tier 3 and sort behind the queue.  No device-wide pass:
+// HBM traffic is the 16 B/slot read of the scoring state plus the 12 B/slot
+// order/key/grant write.
+
+#ifndef AUGSCHED_FM_MATCH
+#define AUGSCHED_FM_MATCH 0   // 1: __match_any_sync digit peers instead of bit ballots
+#endif
+#ifndef AUGSCHED_FM_MINB
+#define AUGSCHED_FM_MINB 4     // resident CTAs per SM the register budget targets (256 threads, E = 8; 5 spills: slower)
+#endif
+template <int NT, int E>
+__global__ void __launch_bounds__(NT, (NT == 256 && E == 8) ? AUGSCHED_FM_MINB : 1) full_multi_kernel(Slots S, augsched_config cfg, int64_t cap, uint64_t now,
+                                                        long long* budget, uint32_t* n_active, uint32_t* tier_off,
+                                                        uint32_t* order, uint32_t* keyout, uint32_t* grant,
+                                                        uint32_t* admitted, uint32_t* gslot) {
+  constexpr int NW = NT / 32;
+  constexpr int NBMAX = 512;
+  constexpr uint32_t MP = (uint32_t)NT * E;      // padded slot count (>= MA)
+  extern __shared__ __align__(16) unsigned long long fm_sm[];
+  unsigned long long* buf0 = fm_sm;               // [MP]
+  unsigned long long* buf1 = fm_sm + MP;          // [MP]
+  // 16-bit digit counters, warp-major [NW][NBMAX] (counts and offsets < 2^16)
+  uint16_t* wcnt = reinterpret_cast<uint16_t*>(fm_sm + 2 * (size_t)MP);
+  // the rare resolution's selection state reuses the counters' space (the
+  // region is sized for the larger of the two, full_multi_smem)
+  SelShm& sel = *reinterpret_cast<SelShm*>(wcnt);
+  __shared__ unsigned long long wsum[NW + 1];
+  __shared__ unsigned long long freed;
+  __shared__ uint32_t tc_s[3], tsum[NT / 32];
+  __shared__ long long B_s;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const unsigned lt = (1u << lane) - 1;
+  const uint32_t inst = blockIdx.x;
+  const uint32_t MA = S.MA;
+  const size_t base = (size_t)inst * MA;
+  const Coef k = S.coef[inst];
+  const augsched_instance_params ip = S.ip[inst];
+  if (tid == 0) {
+    B_s = token_limit(cfg, k, ip, cap, ld_ll(&S.A[inst]), ld_ll(&S.P[inst]));
+    budget[inst] = B_s;
+    tc_s[0] = tc_s[1] = tc_s[2] = 0;
+  }
+  // ---- words of every slot (a4), per-tier counts
+  uint32_t tcount[3] = {0u, 0u, 0u};
+  {
+    // the E slots of this thread loaded together (independent loads in flight)
+    uint32_t stv[E], lst[E];
+    double V[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const uint32_t x = tid + e * NT;
+      stv[e] = 0u; lst[e] = 0u; V[e] = 0.0;
+      if (x < MA) { stv[e] = S.st[base + x]; V[e] = S.V[base + x]; lst[e] = S.last[base + x]; }
+    }
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const uint32_t x = tid + e * NT;
+      unsigned long long w = ~0ull;
+      if (x < MA) {
+        w = slot_word(k, ip, stv[e], V[e], lst[e], now, x);
+        const uint32_t t = (uint32_t)(w >> PK_TIER);
+        if (t < 3) ++tcount[t];
+      }
+      buf0[x] = w;
+    }
+  }
+#pragma unroll
+  for (int t = 0; t < 3; ++t) {
+    uint32_t c = tcount[t];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(FULL, c, o);
+    if (lane == 0 && c) atomicAdd(&tc_s[t], c);
+  }
+  // ---- LSD radix sort of bits [30, 64) (tier:2 | key:32), stable.
+  // Counters are warp-major (wcnt[w * NBMAX + d]: the leaders of one warp hit
+  // distinct banks unless their digits agree mod 32); thread t owns digits
+  // [t * DPT, t * DPT + DPT) for the scan in (digit, warp) order.
+  unsigned long long* src = buf0;
+  unsigned long long* dst = buf1;
+#pragma unroll 1
+  for (int p = 0; p < 4; ++p) {
+    const int shift = PK_KEY + (p == 0 ? 0 : p == 1 ? 9 : p == 2 ? 18 : 26), bits = p < 2 ? 9 : 8;
+    const int NB = 1 << bits;
+    for (int i = tid; i < NBMAX * NW; i += NT) wcnt[i] = 0;
+    __syncthreads();
+    unsigned long long xv[E];
+    uint32_t rk[E];
+    int dg[E];
+    const uint32_t seg = (uint32_t)warp * 32 * E;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      xv[e] = src[seg + e * 32 + lane];
+      dg[e] = (int)((xv[e] >> shift) & (unsigned long long)(NB - 1));
+    }
+    uint16_t* wc = wcnt + warp * NBMAX;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      unsigned peers;
+#if AUGSCHED_FM_MATCH
+      peers = __match_any_sync(FULL, dg[e]);
+#else
+      if (bits == 9) peers = digit_peers_full<9>((uint32_t)dg[e]);
+      else peers = digit_peers_full<8>((uint32_t)dg[e]);
+#endif
+      rk[e] = wc[dg[e]] + __popc(peers & lt);
+      __syncwarp();
+      if (lane == __ffs(peers) - 1) wc[dg[e]] = (uint16_t)(wc[dg[e]] + __popc(peers));
+      __syncwarp();
+    }
+    __syncthreads();
+    {
+      const int DPT = NB / NT > 0 ? NB / NT : 1;   // 2 or 1 (NT = 256), 1 (NT = 512)
+      const int d0 = tid * DPT;
+      uint32_t sum = 0;
+      if (d0 < NB)
+        for (int j = 0; j < DPT; ++j)
+#pragma unroll
+          for (int w = 0; w < NW; ++w) sum += wcnt[w * NBMAX + d0 + j];
+      uint32_t inc = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(FULL, inc, o);
+        if (lane >= o) inc += y;
+      }
+      if (lane == 31) tsum[warp] = inc;
+      __syncthreads();
+      uint32_t run = inc - sum;
+      for (int w = 0; w < warp; ++w) run += tsum[w];
+      if (d0 < NB)
+        for (int j = 0; j < DPT; ++j)
+#pragma unroll
+          for (int w = 0; w < NW; ++w) {
+            const uint32_t c = wcnt[w * NBMAX + d0 + j];
+            wcnt[w * NBMAX + d0 + j] = (uint16_t)run;
+            run += c;
+          }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < E; ++e) dst[wc[dg[e]] + rk[e]] = xv[e];
+    __syncthreads();
+    unsigned long long* t = src; src = dst; dst = t;
+  }
+  // ---- admission (R17), resolution (R20), grant accounting over the order
+  const uint32_t c0 = tc_s[0], c1 = tc_s[1], c2 = tc_s[2];
+  const uint32_t n = c0 + c1 + c2;
+  const long long B = B_s;
+  const uint32_t target = pf_target(B, n);
+  const uint32_t prev = S.gdirty[inst];
+  pf_finish<NT, 8, true>(S, cfg, cap, now, inst, base, src, src, dst, n, target, B, order, keyout, grant,
+                         admitted, gslot, sel, wsum, freed, nullptr, 0, n);
+  __syncthreads();
+  // ---- the rest of the order; zero grants beyond the prefix (R16)
+  const uint32_t adm = admitted[inst];   // written by thread 0 at the end of pf_finish
+  for (uint32_t j = adm + tid; j < n; j += NT) {
+    const unsigned long long w = src[j];
+    order[base + j] = (uint32_t)w & SLOT_MASK;
+    keyout[base + j] = (uint32_t)(w >> PK_KEY);
+  }
+  for (uint32_t j = adm + tid; j < prev && j < MA; j += NT) grant[base + j] = 0;
+  if (tid == 0) {
+    S.gdirty[inst] = adm;
+    n_active[inst] = n;
+    tier_off[3 * inst] = 0;
+    tier_off[3 * inst + 1] = c0;
+    tier_off[3 * inst + 2] = c0 + c1;
+  }
+}
 }  // namespace
 
 // ====================================================================== host
@@ -1623,6 +1829,10 @@ Slots slots_of(StepState& st, const augsched_instance_params* d_ip) {
 }  // namespace
 
 static size_t pf_smem_bytes() { return sizeof(unsigned long long) * 2 * PF_SCAP; }
+static size_t full_multi_smem(int NT, int E) {
+  const size_t cnt = sizeof(uint16_t) * 512 * (NT / 32);
+  return sizeof(unsigned long long) * 2 * (size_t)NT * E + (cnt > sizeof(SelShm) ? cnt : sizeof(SelShm));
+}
 
 int step_ensure(StepState& st, uint32_t n_inst, uint32_t max_active, cudaStream_t s,
                 const augsched_config& cfg, const augsched_instance_params* d_ip, uint64_t* launches) {
@@ -1847,12 +2057,47 @@ int step_run_prefix(StepState& st, const augsched_config& cfg, int64_t cap,
   return cuda_check(cudaGetLastError(), "step_prefix");
 }
 
+template <int NT, int E>
+static void launch_full_multi(const StepState& st, const Slots& S, const augsched_config& cfg, int64_t cap,
+                              uint64_t now, cudaStream_t s) {
+  const size_t smem = full_multi_smem(NT, E);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(full_multi_kernel<NT, E>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  full_multi_kernel<NT, E><<<st.n_inst, NT, smem, s>>>(S, cfg, cap, now, st.budget, st.n_active, st.tier_off,
+                                                        st.order, st.key, st.grant, st.admitted, st.gslot);
+}
+
 int step_run(StepState& st, const augsched_config& cfg, int64_t cap,
              const augsched_instance_params* d_ip, uint32_t* d_err, uint64_t now,
              augsched_step_out* out, cudaStream_t s, uint64_t* launches) {
   Slots S = slots_of(st, d_ip);
   const uint32_t ni = st.n_inst;
   run_records(st, S, d_err, now, s, launches);
+#ifndef AUGSCHED_NO_FULL_MULTI
+  // several instances whose slots fit in one CTA's shared memory: one CTA
+  // per instance sorts and admits (no device-wide pass)
+  if (ni > 1 && st.max_active <= 8192) {
+    const uint32_t MA = st.max_active;
+    if (MA <= 256) launch_full_multi<256, 1>(st, S, cfg, cap, now, s);
+    else if (MA <= 512) launch_full_multi<256, 2>(st, S, cfg, cap, now, s);
+    else if (MA <= 1024) launch_full_multi<256, 4>(st, S, cfg, cap, now, s);
+    else if (MA <= 2048) launch_full_multi<256, 8>(st, S, cfg, cap, now, s);
+    else if (MA <= 4096) launch_full_multi<256, 16>(st, S, cfg, cap, now, s);
+    else launch_full_multi<512, 16>(st, S, cfg, cap, now, s);
+    *launches += 1;
+    out->budget = reinterpret_cast<const int64_t*>(st.budget);
+    out->n_active = st.n_active;
+    out->admitted = st.admitted;
+    out->order = st.order;
+    out->grant = st.grant;
+    out->key = st.key;
+    out->tier_off = st.tier_off;
+    return cuda_check(cudaGetLastError(), "step (batched)");
+  }
+#endif
   st.pf_dirty = true;
   int rc = cuda_check(cudaMemsetAsync(st.zbuf, 0, sizeof(uint32_t) * st.zwords, s), "step: clear");
   if (rc) return rc;

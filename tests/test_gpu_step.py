@@ -433,3 +433,30 @@ def test_now_must_fit_u32_and_not_run_backwards():
     s.step(10)        # equal is fine
     s.sync()
     s.close()
+
+
+@pytest.mark.parametrize("n_inst,MA,cap", [(3, 100, 10**6), (2, 3000, 900), (2, 5000, 10**6), (5, 1500, 600)])
+def test_batched_full_order_shapes(n_inst, MA, cap):
+    """The batched full-order kernel (one CTA per instance, shared-memory LSD
+    sort) at slot counts that are not powers of two and at its 512-thread
+    size (MA > 4,096): 12 steps of random events, every output and the slot
+    state equal the oracle's."""
+    rng = np.random.default_rng(MA + n_inst)
+    cfg = dict(tracegen.PRESET_G0, g_total=1000 + cap, g_model=1000)
+    ip = tracegen.inst_params(n_inst, base=tracegen.INST_G0, ranking=[0, 1, 0, 2, 0][:n_inst],
+                              budget_mode=0, target_max=[300, 200, 120, 90, 400][:n_inst],
+                              alpha=[1.5, 0.0, 3.0, 0.0, 0.2][:n_inst], rank_seed=7)
+    st = oracle.Step(cfg, ip, MA)
+    s = aug.Scheduler(cfg, ip, n_inst, MA)
+    for t in range(12):
+        for i in range(n_inst):
+            rec = random_events(rng, st.slots(i), t, p_new=0.7 if t == 0 else 0.1)
+            if rec is not None:
+                assert st.enqueue(i, rec) == 0
+                s.enqueue(i, rec)
+        o = st.step(t)
+        assert o["rc"] == 0
+        g = s.step_result(s.step(t))
+        compare(g, o, n_inst, f"batched MA={MA} step {t}")
+        compare_slots(s, st, n_inst, f"batched MA={MA} step {t}")
+    s.close()
