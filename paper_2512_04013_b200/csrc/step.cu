@@ -1,5 +1,6 @@
 // augsched_step kernels (see step.cuh).  sm_100a, compiled with -fmad=false.
 #include <cuda_runtime.h>
+#include <cooperative_groups.h>
 #include <cstdio>
 #include "step.cuh"
 #include "select.cuh"
@@ -1763,6 +1764,318 @@ __global__ void __launch_bounds__(NT, (NT == 256 && E == 8) ? AUGSCHED_FM_MINB :
     tier_off[3 * inst + 2] = c0 + c1;
   }
 }
+
+// ====================================================================== full step, one instance
+// augsched_step on a single-instance handle: ONE cooperative kernel (one
+// 1,024-thread CTA per SM, a contiguous chunk of slots per CTA) runs the
+// keys, a stable LSD radix sort of the 34-bit (tier, key) field in four
+// passes (9, 9, 8, 8 bits) and the admission, with grid barriers between
+// the phases instead of kernel boundaries and no decoupled look-back:
+//   K    packed word of every slot of the chunk (Eq.26 key; tier 3 = not
+//        queued) -> kA, and the chunk's digit histogram of pass 0
+//   per pass p: publish the chunk histogram H[p][cta][digit]; barrier; each
+//        CTA sums the published histograms (all CTAs: digit totals; CTAs
+//        before it: its own base per digit); then ranks its chunk stably in
+//        sub-tiles of 8,192 words (ballot digit peers, warp-private 16-bit
+//        counters, a scan over (digit, warp)) and scatters; barrier; the
+//        histogram of the next pass over its chunk of the output
+//   last pass writes order (slot) and key of every position and the packed
+//        words of the first PF_SCAP positions; the tier counts come from
+//        its digit totals (the digit's top two bits are the tier)
+//   F    CTA 0: admission (R17), resolution (R20), grant accounting over the
+//        first min(B, n) words (pf_finish), grants beyond the prefix zeroed.
+constexpr int CNT = 1024;          // threads per CTA
+constexpr int CEPT = 8;            // words per thread per sub-tile
+constexpr int CNW = CNT / 32;
+constexpr int CNB = 512;           // widest digit (9 bits)
+constexpr uint32_t CSUB = CNT * CEPT;
+
+struct CoopArgs {
+  Slots S;
+  augsched_config cfg;
+  int64_t cap;
+  uint64_t now;
+  uint32_t N;
+  uint32_t max_limit;                // largest token limit (bounds the admitted prefix)
+  unsigned long long *kA, *kB;       // [N] packed words (ping-pong)
+  unsigned long long* kpre;          // [PF_SCAP] words of the first positions of the order
+  uint32_t* hist;                    // [4][G][CNB] per-CTA digit histograms
+  uint32_t* tot;                     // [4][CNB] digit totals
+  unsigned long long* bar;           // grid-barrier counter (monotone across calls)
+  unsigned long long bar_base;       // its value at this call's start
+  long long* budget;
+  uint32_t *n_active, *tier_off, *order, *keyout, *grant, *admitted, *gslot;
+};
+
+#ifdef AUGSCHED_COOP_TIMING
+__device__ unsigned long long g_coop_arr[16];   // latest arrival per barrier (ns)
+#endif
+#ifndef AUGSCHED_COOP_CG
+#define AUGSCHED_COOP_CG 1   // grid barrier: cooperative_groups grid sync (0: own counter + nanosleep spin)
+#endif
+__device__ __forceinline__ void coop_barrier(const CoopArgs& a, uint32_t& k) {
+  ++k;
+#ifdef AUGSCHED_COOP_TIMING
+  if (threadIdx.x == 0) atomicMax(&g_coop_arr[k], gtime());
+#endif
+#if AUGSCHED_COOP_CG
+  cooperative_groups::this_grid().sync();
+#else
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(a.bar, 1ull);
+    const unsigned long long target = a.bar_base + (unsigned long long)k * gridDim.x;
+    while (*(volatile unsigned long long*)a.bar < target) __nanosleep(20);
+    __threadfence();
+  }
+  __syncthreads();
+#endif
+}
+
+#ifdef AUGSCHED_COOP_TIMING
+#define CT(i) do { if (blockIdx.x == 0 && threadIdx.x == 0) ct[i] = gtime(); } while (0)
+#else
+#define CT(i) do {} while (0)
+#endif
+
+__device__ __forceinline__ int coop_shift(int p) { return PK_KEY + (p == 0 ? 0 : p == 1 ? 9 : p == 2 ? 18 : 26); }
+__device__ __forceinline__ int coop_bits(int p) { return p < 2 ? 9 : 8; }
+
+__global__ void __launch_bounds__(CNT, 1) full_coop_kernel(const __grid_constant__ CoopArgs a) {
+  extern __shared__ __align__(16) unsigned long long fc_sm[];
+  unsigned long long* sbuf = fc_sm;                                            // [PF_SCAP] (phase F)
+  uint16_t* wcnt = reinterpret_cast<uint16_t*>(fc_sm + PF_SCAP);              // [CNW][CNB]
+  __shared__ uint32_t h[CNB];          // chunk histogram of the next pass
+  __shared__ uint32_t base_s[CNB];     // running position of each digit for this CTA
+  __shared__ uint32_t tot_s[CNB];      // digit totals (all CTAs)
+  __shared__ uint32_t wsc[CNW + 1];
+  __shared__ SelShm sel;
+  __shared__ unsigned long long wsum[CNW + 1];
+  __shared__ unsigned long long freed;
+  __shared__ long long B_s;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const unsigned lt = (1u << lane) - 1;
+  const uint32_t G = gridDim.x, c = blockIdx.x, N = a.N;
+  const Slots& S = a.S;
+  const uint32_t chunk = ((N + G - 1) / G + 31) & ~31u;
+  const uint32_t c0 = c * chunk < N ? c * chunk : N;
+  const uint32_t c1 = c0 + chunk < N ? c0 + chunk : N;
+  uint32_t nbar = 0;
+#ifdef AUGSCHED_COOP_TIMING
+  unsigned long long ct[32];
+#endif
+  CT(0);
+  // A chunk that fits one sub-tile stays in registers between the phases
+  // (xr, element i = c0 + warp * 256 + e * 32 + lane, the ranking order):
+  // the words are not written by K, and each pass's input is read once.
+  const bool reg = c1 - c0 <= CSUB;
+  unsigned long long xr[CEPT];
+  // ---- K: words of the chunk + histogram of pass 0
+  {
+    const Coef k = S.coef[0];
+    const augsched_instance_params ip = S.ip[0];
+    for (int b = tid; b < CNB; b += CNT) h[b] = 0;
+    __syncthreads();
+    for (uint32_t b0 = c0; b0 < c1; b0 += CSUB) {   // block-uniform trip count
+      uint32_t stv[CEPT], lst[CEPT];
+      double V[CEPT];
+      const uint32_t seg = b0 + (uint32_t)warp * 32 * CEPT;
+#pragma unroll
+      for (int u = 0; u < CEPT; ++u) {
+        const uint32_t x = seg + u * 32 + lane;
+        stv[u] = 0u; lst[u] = 0u; V[u] = 0.0;
+        if (x < c1) { stv[u] = S.st[x]; V[u] = S.V[x]; lst[u] = S.last[x]; }
+      }
+#pragma unroll
+      for (int u = 0; u < CEPT; ++u) {
+        const uint32_t x = seg + u * 32 + lane;
+        const unsigned long long w = slot_word(k, ip, stv[u], V[u], lst[u], a.now, x);
+        xr[u] = w;
+        if (x < c1 && !reg) a.kA[x] = w;
+        hist_add(h, x < c1 ? (int)((w >> coop_shift(0)) & (CNB - 1)) : -1);
+      }
+    }
+    if (c == 0 && tid == 0) {
+      B_s = token_limit(a.cfg, k, ip, a.cap, ld_ll(&S.A[0]), ld_ll(&S.P[0]));
+      a.budget[0] = B_s;
+    }
+  }
+  unsigned long long* src = a.kA;
+  unsigned long long* dst = a.kB;
+#pragma unroll 1
+  for (int p = 0; p < 4; ++p) {
+    const int shift = coop_shift(p), bits = coop_bits(p), NB = 1 << bits;
+    const bool last = p == 3;
+    // publish the chunk histogram of this pass
+    __syncthreads();
+    uint32_t* Hp = a.hist + (size_t)p * G * CNB;
+    for (int b = tid; b < NB; b += CNT) Hp[(size_t)c * CNB + b] = h[b];
+    CT(1 + 6 * p);
+    coop_barrier(a, nbar);
+    CT(2 + 6 * p);
+    // column scan: CTA c owns digits [c * DPC, c * DPC + DPC) and scans
+    // each over the G CTAs (thread tid: digit j = tid / 256, CTA tid % 256),
+    // writing the exclusive prefixes back in place and the digit total
+    {
+      const int DPC = (NB + (int)G - 1) / (int)G;        // <= 4 (G >= 128)
+      const int j = tid >> 8, cc = tid & 255;
+      const int d = (int)c * DPC + j;
+      const bool own = j < DPC && d < NB && cc < (int)G;
+      const uint32_t v = own ? __ldcg(&Hp[(size_t)cc * CNB + d]) : 0u;
+      uint32_t inc = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(FULL, inc, o);
+        if (lane >= o) inc += y;
+      }
+      if (lane == 31) wsc[warp] = inc;
+      __syncthreads();
+      uint32_t run = inc - v;
+      for (int w = j * 8; w < warp; ++w) run += wsc[w];   // the 8 warps of digit group j
+      if (own) Hp[(size_t)cc * CNB + d] = run;
+      if (j < DPC && d < NB && cc == 255) a.tot[p * CNB + d] = run + v;
+    }
+    coop_barrier(a, nbar);
+    // this CTA's base per digit: exclusive scan of the totals over digits
+    // plus its own column prefix
+    {
+      const uint32_t v = tid < NB ? __ldcg(&a.tot[p * CNB + tid]) : 0u;
+      const uint32_t pre = tid < NB ? __ldcg(&Hp[(size_t)c * CNB + tid]) : 0u;
+      uint32_t inc = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(FULL, inc, o);
+        if (lane >= o) inc += y;
+      }
+      __syncthreads();   // wsc reuse
+      if (lane == 31) wsc[warp] = inc;
+      __syncthreads();
+      uint32_t run = inc - v;
+      for (int w = 0; w < warp; ++w) run += wsc[w];
+      if (tid < NB) { base_s[tid] = run + pre; tot_s[tid] = v; }
+      __syncthreads();
+    }
+    CT(3 + 6 * p);
+    if (last && c == 0 && tid == 0) {
+      // tier counts: the last digit's top two bits are the tier
+      uint32_t tc[4] = {0u, 0u, 0u, 0u};
+      for (int d = 0; d < NB; ++d) tc[d >> 6] += tot_s[d];
+      const uint32_t n = tc[0] + tc[1] + tc[2];
+      a.n_active[0] = n;
+      a.tier_off[0] = 0;
+      a.tier_off[1] = tc[0];
+      a.tier_off[2] = tc[0] + tc[1];
+    }
+    // rank and scatter the chunk, sub-tile by sub-tile
+    for (uint32_t s0 = c0; s0 < c1; s0 += CSUB) {
+      for (int i = tid; i < CNW * CNB; i += CNT) wcnt[i] = 0;
+      __syncthreads();
+      unsigned long long xv[CEPT];
+      uint32_t rk[CEPT];
+      int dg[CEPT];
+      const uint32_t seg = s0 + (uint32_t)warp * 32 * CEPT;
+#pragma unroll
+      for (int e = 0; e < CEPT; ++e) {
+        const uint32_t i = seg + e * 32 + lane;
+        xv[e] = i >= c1 ? 0ull : reg ? xr[e] : __ldcg(&src[i]);
+        dg[e] = i < c1 ? (int)((xv[e] >> shift) & (unsigned long long)(NB - 1)) : -1;
+      }
+      uint16_t* wc = wcnt + warp * CNB;
+#pragma unroll
+      for (int e = 0; e < CEPT; ++e) {
+        unsigned peers;
+        if (bits == 9) peers = digit_peers<9>(dg[e]);
+        else peers = digit_peers<8>(dg[e]);
+        if (dg[e] >= 0) rk[e] = wc[dg[e]] + __popc(peers & lt);
+        __syncwarp();
+        if (dg[e] >= 0 && lane == __ffs(peers) - 1) wc[dg[e]] = (uint16_t)(wc[dg[e]] + __popc(peers));
+        __syncwarp();
+      }
+      __syncthreads();
+      // per digit: exclusive offsets over the warps, advance the running base
+      for (int d = tid; d < NB; d += CNT) {
+        uint32_t run = base_s[d];
+#pragma unroll 8
+        for (int w = 0; w < CNW; ++w) {
+          const uint32_t v = wcnt[w * CNB + d];
+          wcnt[w * CNB + d] = (uint16_t)(run - base_s[d]);
+          run += v;
+        }
+        tot_s[d] = run;   // the base for the next sub-tile (tot_s is free after the scan)
+      }
+      __syncthreads();
+#pragma unroll
+      for (int e = 0; e < CEPT; ++e) {
+        if (dg[e] < 0) continue;
+        const uint32_t pos = base_s[dg[e]] + wc[dg[e]] + rk[e];
+        if (last) {
+          const uint32_t x = (uint32_t)xv[e] & SLOT_MASK;
+          a.order[pos] = x;
+          a.keyout[pos] = (uint32_t)(xv[e] >> PK_KEY);
+          if (pos < PF_SCAP) a.kpre[pos] = xv[e];
+          if (pos < a.max_limit) {   // the admission (phase F) reads these slots' token state
+            prefetch_l2(&S.ctx[x]); prefetch_l2(&S.kv[x]); prefetch_l2(&S.cpu[x]); prefetch_l2(&S.pend[x]);
+          }
+        } else {
+          dst[pos] = xv[e];
+        }
+      }
+      __syncthreads();
+      for (int d = tid; d < NB; d += CNT) base_s[d] = tot_s[d];
+      __syncthreads();
+    }
+    CT(4 + 6 * p);
+    coop_barrier(a, nbar);
+    CT(5 + 6 * p);
+    if (!last) {
+      // histogram of the next pass over this CTA's chunk of the output
+      const int ns = coop_shift(p + 1);
+      const int nm = (1 << coop_bits(p + 1)) - 1;
+      for (int b = tid; b < CNB; b += CNT) h[b] = 0;
+      __syncthreads();
+      for (uint32_t i0 = c0; i0 < c1; i0 += CSUB) {
+        const uint32_t seg = i0 + (uint32_t)warp * 32 * CEPT;
+#pragma unroll
+        for (int u = 0; u < CEPT; ++u) {
+          const uint32_t i = seg + u * 32 + lane;
+          xr[u] = i < c1 ? __ldcg(&dst[i]) : 0ull;
+        }
+#pragma unroll
+        for (int u = 0; u < CEPT; ++u) {
+          const uint32_t i = seg + u * 32 + lane;
+          hist_add(h, i < c1 ? (int)((xr[u] >> ns) & (unsigned long long)nm) : -1);
+        }
+      }
+      unsigned long long* t = src; src = dst; dst = t;
+    }
+    CT(6 + 6 * p);
+  }
+  if (c != 0) return;
+  // ---- F: admission over the first min(B, n) positions
+  const uint32_t n = __ldcg(&a.n_active[0]);
+  const long long B = B_s;
+  const uint32_t target = pf_target(B, n);
+  for (uint32_t i = tid; i < target; i += CNT) sbuf[i] = __ldcg(&a.kpre[i]);
+  const uint32_t prev = S.gdirty[0];
+  __syncthreads();
+  pf_finish<CNT, PF_SCAP / CNT, true>(S, a.cfg, a.cap, a.now, 0, 0, nullptr, sbuf, nullptr, target, target, B,
+                                      a.order, a.keyout, a.grant, a.admitted, a.gslot, sel, wsum, freed);
+  __syncthreads();
+  const uint32_t adm = a.admitted[0];
+  for (uint32_t j = adm + tid; j < prev && j < N; j += CNT) a.grant[j] = 0;
+  if (tid == 0) S.gdirty[0] = adm;
+#ifdef AUGSCHED_COOP_TIMING
+  CT(25);
+  if (tid == 0) {
+    printf("coop_t ns:");
+    for (int i = 1; i <= 25; ++i) printf(" %llu", ct[i] - ct[0]);
+    printf("\ncoop_arr ns:");
+    for (int i = 1; i <= 12; ++i) { printf(" %llu", g_coop_arr[i] - ct[0]); g_coop_arr[i] = 0; }
+    printf("\n");
+  }
+#endif
+}
 }  // namespace
 
 // ====================================================================== host
@@ -1829,6 +2142,9 @@ Slots slots_of(StepState& st, const augsched_instance_params* d_ip) {
 }  // namespace
 
 static size_t pf_smem_bytes() { return sizeof(unsigned long long) * 2 * PF_SCAP; }
+static size_t coop_smem_bytes() {
+  return sizeof(unsigned long long) * PF_SCAP + sizeof(uint16_t) * CNW * CNB;
+}
 static size_t full_multi_smem(int NT, int E) {
   const size_t cnt = sizeof(uint16_t) * 512 * (NT / 32);
   return sizeof(unsigned long long) * 2 * (size_t)NT * E + (cnt > sizeof(SelShm) ? cnt : sizeof(SelShm));
@@ -1877,7 +2193,8 @@ int step_ensure(StepState& st, uint32_t n_inst, uint32_t max_active, cudaStream_
       (rc = salloc(st, &st.pf_H, PF_HCAP)) || (rc = salloc(st, &st.wkv, 1)) ||
       (rc = salloc(st, &st.pf_nact, 2)) || (rc = salloc(st, &st.n_active, n_inst)) ||
       (rc = salloc(st, &st.tier_off, 3 * (size_t)n_inst)) || (rc = salloc(st, &st.claimA, N)) ||
-      (rc = salloc(st, &st.claimB, N)) || (rc = salloc(st, &st.gdirty, n_inst)))
+      (rc = salloc(st, &st.claimB, N)) || (rc = salloc(st, &st.gdirty, n_inst)) ||
+      (rc = salloc(st, &st.coop_bar, 1)))
     return rc;
   // one memset per full step clears the tier counts, histograms and tile counters
   st.zwords = zwords;
@@ -1904,6 +2221,7 @@ int step_ensure(StepState& st, uint32_t n_inst, uint32_t max_active, cudaStream_
       {st.grant, 0, sizeof(uint32_t) * N},                // grant[j] = 0 beyond the admitted prefix
       {st.admitted, 0, sizeof(uint32_t) * n_inst},
       {st.gdirty, 0, sizeof(uint32_t) * n_inst},
+      {st.coop_bar, 0, sizeof(unsigned long long)},
       {st.n_active, 0, sizeof(uint32_t) * n_inst},
       {st.tier_off, 0, 3 * sizeof(uint32_t) * n_inst},
       {st.A, 0, sizeof(long long) * n_inst},
@@ -1928,6 +2246,15 @@ int step_ensure(StepState& st, uint32_t n_inst, uint32_t max_active, cudaStream_
     st.pf_grid = st.sms * (occ > 0 ? occ : 1);
   }
   cudaFuncSetAttribute(pf_multi_kernel<256, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PF_MULTI_SMEM);
+  if (n_inst == 1) {
+    cudaFuncSetAttribute(full_coop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)coop_smem_bytes());
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, full_coop_kernel, CNT, coop_smem_bytes());
+    st.coop_grid = occ >= 1 ? st.sms : 0;   // one CTA per SM
+    st.coop_bar_base = 0;
+    if (st.sms < 128 || st.sms > 256) st.coop_grid = 0;   // column scan: <= 4 digits per CTA, one CTA per thread of a 256-thread group
+    if (st.coop_grid > 0 && (rc = salloc(st, &st.coop_hist, 4 * ((size_t)st.coop_grid + 1) * CNB))) return rc;
+  }
   cudaFuncSetAttribute(pf_multi_kernel<PNT, PF_SCAP / PNT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)PF_MULTI_SMEM);
   st.epoch = 0;
@@ -2076,6 +2403,33 @@ int step_run(StepState& st, const augsched_config& cfg, int64_t cap,
   Slots S = slots_of(st, d_ip);
   const uint32_t ni = st.n_inst;
   run_records(st, S, d_err, now, s, launches);
+#ifndef AUGSCHED_NO_FULL_COOP
+  // one instance: one cooperative kernel (keys, four sort passes with grid
+  // barriers, admission by CTA 0)
+  if (ni == 1 && st.max_limit <= PF_SCAP && st.coop_grid > 0) {
+    CoopArgs ca;
+    ca.S = S; ca.cfg = cfg; ca.cap = cap; ca.now = now; ca.N = (uint32_t)st.N; ca.max_limit = st.max_limit;
+    ca.kA = st.k0; ca.kB = st.k1; ca.kpre = st.pf_A; ca.hist = st.coop_hist; ca.bar = st.coop_bar;
+    ca.tot = st.coop_hist + 4 * (size_t)st.coop_grid * CNB;
+    ca.bar_base = st.coop_bar_base;
+    ca.budget = st.budget; ca.n_active = st.n_active; ca.tier_off = st.tier_off; ca.order = st.order;
+    ca.keyout = st.key; ca.grant = st.grant; ca.admitted = st.admitted; ca.gslot = st.gslot;
+    void* args[] = {&ca};
+    cudaError_t e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(&full_coop_kernel), st.coop_grid,
+                                                CNT, args, coop_smem_bytes(), s);
+    if (e != cudaSuccess) return cuda_check(e, "step: cooperative launch");
+    st.coop_bar_base += 12ull * (unsigned long long)st.coop_grid;   // twelve grid barriers per call
+    *launches += 1;
+    out->budget = reinterpret_cast<const int64_t*>(st.budget);
+    out->n_active = st.n_active;
+    out->admitted = st.admitted;
+    out->order = st.order;
+    out->grant = st.grant;
+    out->key = st.key;
+    out->tier_off = st.tier_off;
+    return cuda_check(cudaGetLastError(), "step (cooperative)");
+  }
+#endif
 #ifndef AUGSCHED_NO_FULL_MULTI
   // several instances whose slots fit in one CTA's shared memory: one CTA
   // per instance sorts and admits (no device-wide pass)

@@ -91,6 +91,10 @@ struct StepState {
   uint32_t pf_epoch = 0;                    // prefix step: calls so far (epoch tag of the kernel's flags)
   bool pf_dirty = false;                    // a full step ran since: counters need one clear
   int pf_grid = 0;                // prefix step: co-resident CTAs of the cooperative kernel
+  int coop_grid = 0;              // full step, one instance: CTAs of the cooperative kernel (0: not used)
+  unsigned long long* coop_bar = nullptr;   // its grid-barrier counter (monotone)
+  unsigned long long coop_bar_base = 0;     // the counter's value at the next call's start
+  uint32_t* coop_hist = nullptr;            // [4][coop_grid][512] per-CTA digit histograms
   bool pf_spec = true;            // prefix step: speculative pass (off when any instance shuffles)
   uint32_t max_limit = 0;         // largest token limit any instance can get
   size_t zwords = 0;

@@ -131,3 +131,27 @@ def test_cfg5_through_iteration_37500():
     assert_equal_records(g[sample], o, "cfg5 @37,500")
     d = [oracle.as_dict(x) for x in o]
     assert max(x["final_t"] for x in d) >= 25 * W - 1 or all(x["completed"] == x["n_requests"] for x in d)
+
+
+@pytest.mark.parametrize("n", [1_000_000, 4_194_304])
+def test_full_step_single_queue_parity(n):
+    """augsched_step (the full order, one cooperative kernel) on one queue at
+    the bench's sizes: 1M (each CTA's chunk fits one sub-tile: kept in
+    registers) and 4M (several sub-tiles per CTA), three steps; order, keys,
+    grants, tier offsets and the slot state equal the oracle's."""
+    rec = tracegen.cfg4_records(n)
+    cfg, ip = tracegen.PRESET_CFG4, tracegen.inst_params(1)
+    st = oracle.Step(cfg, ip, n)
+    assert st.enqueue(0, rec) == 0
+    s = aug.Scheduler(cfg, ip, 1, n)
+    s.enqueue(0, rec)
+    del rec
+    t0 = 65536
+    for k in range(3):
+        o = st.step(t0 + k)
+        assert o["rc"] == 0
+        g = s.step_result(s.step(t0 + k))
+        check_step(g, o, 1, f"full {n} step {k}", False)
+    assert np.array_equal(s.slots(0), st.slots(0)), f"full {n}: slot state"
+    s.close()
+    st.close()
