@@ -291,7 +291,12 @@ AUGSCHED_API int augsched_step_export(augsched_t* h, uint32_t instance, int32_t*
  * inst_trace_id[i] selects instance i's trace.  results: n_instances records.
  * flags: AUGSCHED_HOST_TRACES / AUGSCHED_HOST_RESULTS / AUGSCHED_RESUME.
  * Without HOST_RESULTS the call is asynchronous and results must be a
- * device buffer.  E_CAPACITY if a trace is longer than the handle allows. */
+ * device buffer.  E_CAPACITY if a trace is longer than the handle allows.
+ * The per-request checks (n_seg in [1, 255], segment lists inside the
+ * segment arrays) run on the device before the simulation: a violation
+ * latches E_INVALID, returned by the synchronizing call (this one with
+ * HOST_RESULTS, else augsched_sync), and no instance is simulated.
+ * max_iters <= 2^32 (E_INVALID otherwise). */
 AUGSCHED_API int augsched_simulate(augsched_t* h, const augsched_trace* traces, const uint32_t* inst_trace_id,
                       uint64_t max_iters, augsched_result* results, uint32_t flags);
 

@@ -25,6 +25,17 @@ using namespace augsched;
 
 namespace {
 
+__global__ void validate_requests_kernel(const uint32_t* seg_off, const uint32_t* n_seg, uint32_t n_req,
+                                         uint32_t n_seg_total, uint32_t* err, uint32_t* work) {
+  const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n_req) return;
+  const uint32_t ns = n_seg[r];
+  if (ns < 1 || ns > 255 || (uint64_t)seg_off[r] + ns > n_seg_total) {
+    atomicOr(err, 4u);
+    atomicMax(work, 0x80000000u);   // the simulate kernel finds no instance to run
+  }
+}
+
 thread_local char g_err[512] = "";
 
 int fail(int code, const char* fmt, ...) {
@@ -300,11 +311,7 @@ int augsched_simulate(augsched_t* h, const augsched_trace* traces, const uint32_
         return fail(AUGSCHED_E_CAPACITY, "instance %u: trace %u has %u requests > max_active %u",
                     i, k, traces->req_off[k + 1] - traces->req_off[k], h->max_active);
     }
-    for (uint32_t r = 0; r < nr; ++r)   // segment lists inside the arrays, meta holds 8 bits
-      if (traces->n_seg[r] < 1 || traces->n_seg[r] > 255 ||
-          (uint64_t)traces->seg_off[r] + traces->n_seg[r] > ns)
-        return fail(AUGSCHED_E_INVALID, "request %u: n_seg %u / seg_off %u out of range", r,
-                    traces->n_seg[r], traces->seg_off[r]);
+    // the per-request segment checks run on the device (validate_requests_kernel)
     const size_t b_req_off = sizeof(uint32_t) * (nt + 1), b64 = sizeof(uint64_t) * nr,
                  b32r = sizeof(uint32_t) * nr, b32s = sizeof(uint32_t) * ns,
                  btid = sizeof(uint32_t) * h->n_inst;
@@ -344,6 +351,13 @@ int augsched_simulate(augsched_t* h, const augsched_trace* traces, const uint32_
     CUDA_TRY(cudaMemsetAsync(h->d_acc, 0, sizeof(augsched_result) * h->n_inst, h->stream));
   }
   CUDA_TRY(cudaMemsetAsync(h->d_work, 0, sizeof(uint32_t), h->stream));
+  if (traces->n_req) {
+    // segment lists inside the arrays, n_seg in [1, 255] (meta holds 8 bits);
+    // a violation latches E_INVALID and leaves the simulation no work
+    validate_requests_kernel<<<(traces->n_req + 255) / 256, 256, 0, h->stream>>>(
+        tr.seg_off, tr.n_seg, traces->n_req, traces->n_seg_total, h->d_err, h->d_work);
+    h->launches += 1;
+  }
   SimParams p{};
   p.cfg = h->cfg;
   p.cap = h->cap;

@@ -112,8 +112,8 @@ def test_cfg5_through_iteration_37500():
     import argparse
     import bench
     from test_gpu_simulate import assert_equal_records
-    args = argparse.Namespace(workload="cfg5", instances=65536)
-    tr, ip, tid, ma, _ = bench.workload(args, 0)
+    args = argparse.Namespace(workload="cfg5", instances=65536, scaling="strong")
+    tr, ip, tid, ma, _, _ = bench.workload(args, 0, 1)
     n = len(tid)
     s = aug.Scheduler(tracegen.PRESET_7B, ip, n, ma)
     dt = aug.DeviceTraces(tr)

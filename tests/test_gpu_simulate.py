@@ -179,8 +179,8 @@ def test_cfg5_bench_launch_sampled_parity():
     for the same number of iterations and compared record by record."""
     import bench
     import argparse
-    args = argparse.Namespace(workload="cfg5", instances=65536)
-    tr, ip, tid, ma, _ = bench.workload(args, 0)
+    args = argparse.Namespace(workload="cfg5", instances=65536, scaling="strong")
+    tr, ip, tid, ma, _, _ = bench.workload(args, 0, 1)
     n = len(tid)
     s = aug.Scheduler(tracegen.PRESET_7B, ip, n, ma)
     dt = aug.DeviceTraces(tr)

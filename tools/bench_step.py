@@ -20,7 +20,7 @@ ap.add_argument("--multi", action="store_true", help="the batched step (4,096 in
 a = ap.parse_args()
 torch.cuda.set_device(0)
 stream = torch.cuda.current_stream()
-peak = bench.hbm_peak() if hasattr(bench, "hbm_peak") else 6539.2
+peak = bench.hbm_peak()[0]
 out = {}
 if a.multi:
     print(json.dumps(bench.step_multi_bench(a, 0, stream, peak), indent=1))
