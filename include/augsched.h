@@ -165,7 +165,9 @@ enum {
   AUGSCHED_R_DEMOTIONS, AUGSCHED_R_CALLS_PRESERVE, AUGSCHED_R_CALLS_SWAP,
   AUGSCHED_R_CALLS_DISCARD, AUGSCHED_R_RETURNS, AUGSCHED_R_TOKENS, AUGSCHED_R_FINAL_T,
   AUGSCHED_R_MAKESPAN, AUGSCHED_R_SUM_TTFT, AUGSCHED_R_SUM_E2E, AUGSCHED_R_SUM_GEN,
-  AUGSCHED_R_ADMITTED, AUGSCHED_R_ERR, AUGSCHED_R_MAXQ, AUGSCHED_R_RSV22, AUGSCHED_R_RSV23,
+  AUGSCHED_R_ADMITTED, AUGSCHED_R_ERR, AUGSCHED_R_MAXQ,
+  AUGSCHED_R_INCOMPLETE,  /* requests not finished when the run stopped (R28) */
+  AUGSCHED_R_RSV23,
   AUGSCHED_R_NFIELD
 };
 #define AUGSCHED_NBIN 160   /* integer log-linear bins: v<16 -> v; else 16+4(e-4)+2 mantissa bits */

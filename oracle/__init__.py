@@ -19,7 +19,7 @@ FIELDS = [
     "n_requests", "arrived", "completed", "slo_ok", "slo_ok_5x", "busy_steps", "decisions",
     "evictions", "demotions", "calls_preserve", "calls_swap", "calls_discard", "returns",
     "tokens_granted", "final_t", "makespan_iter", "sum_ttft_ticks", "sum_e2e_ticks",
-    "sum_gen_tokens", "admitted", "err", "max_queue", "rsv22", "rsv23",
+    "sum_gen_tokens", "admitted", "err", "max_queue", "incomplete", "rsv23",
 ]
 NBIN = 160
 PRESERVE, SWAP, DISCARD = 0, 1, 2

@@ -235,7 +235,7 @@ struct Req {
 enum Field {
   F_NREQ, F_ARRIVED, F_COMPLETED, F_SLO_OK, F_SLO_OK5, F_BUSY, F_DECISIONS, F_EVICT,
   F_DEMOTE, F_CALL_P, F_CALL_S, F_CALL_D, F_RETURNS, F_TOKENS, F_FINAL_T, F_MAKESPAN,
-  F_SUM_TTFT, F_SUM_E2E, F_SUM_GEN, F_ADMITTED, F_ERR, F_MAXQ, F_R22, F_R23
+  F_SUM_TTFT, F_SUM_E2E, F_SUM_GEN, F_ADMITTED, F_ERR, F_MAXQ, F_INCOMPLETE, F_R23
 };
 
 int64_t demand_of(const Req& r, int64_t s_in) {  // a6 demand (R17, R18)
@@ -458,6 +458,10 @@ void simulate_one(const OCfg& cfg, const OInst& ip, const OTrace& tr, uint32_t t
     t += 1;                                            // S12
   }
   F[F_FINAL_T] = t;
+  // R28 / S:481: requests still unfinished when the run stopped (a W1/W3 run
+  // stops at the horizon, max_iters = H / T) are excluded from attainment
+  // and counted here
+  F[F_INCOMPLETE] = n - n_fin;
 }
 
 

@@ -929,6 +929,7 @@ __device__ void inst_end(const SimParams& p, SimShm& s) {
     H.t = s.t; H.A = s.A; H.P = s.P; H.min_ret = s.min_ret; H.next_arr = s.next_arr;
     H.n_r = s.n_r; H.n_w = s.n_w; H.n_pz = s.n_pz; H.n_fin = s.n_fin; H.w2 = s.w2;
     s.cnt[AUGSCHED_R_FINAL_T] = s.t;
+    s.cnt[AUGSCHED_R_INCOMPLETE] = s.n - s.n_fin;   // R28
   }
   ISYNC();
   augsched_result& out = p.out[inst];

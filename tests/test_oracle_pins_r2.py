@@ -249,3 +249,24 @@ def test_P10_slo_5x_ttft_term():
 def test_P11_last_scheduled_time_set_on_grant():
     g, rec, ft, fin = _run("P11_last_on_grant_sim", 1_000_000, 10, alpha=1000.0)
     assert list(ft) == g["first_token_iter"] and list(fin) == g["finish_iter"]
+
+
+def test_R28_incomplete_counter():
+    """R28 / S:481: a run stopped at the horizon counts the requests still
+    unfinished.  G4's request (prefill at t0, tokens at t1..t5,
+    finish at iteration 6): a run with max_iters 5 stops before its last
+    decode (1 incomplete), max_iters 6 lets it finish (0)."""
+    tr = tracegen.from_requests([[req(0, 10, [(5,)])]])
+    for mi, inc in ((5, 1), (6, 0), (1, 1)):
+        rec, ft, fin = oracle.simulate_detail(cfg0(), inst0(15), tr, max_iters=mi)
+        assert rec["incomplete"] == inc and rec["completed"] == 1 - inc
+
+
+def test_R28_completed_plus_incomplete_is_n():
+    tr = tracegen.gen_traces(3, 150, [2.0, 4.0, 8.0], seed=5)
+    for mi in (300, 2000, 2**40):
+        res = oracle.simulate(tracegen.PRESET_7B, tracegen.inst_params(3), tr, np.arange(3, dtype=np.uint32),
+                              max_iters=mi)
+        for x in res:
+            d = oracle.as_dict(x)
+            assert d["completed"] + d["incomplete"] == d["n_requests"]

@@ -6,8 +6,10 @@ by side in one augsched_simulate call per CV:
   infercept FCFS + adaptive policy + static 500
   maxbatch  FCFS + adaptive policy + dynamic limit   ("w/ MaxBatch")
   augserve  two-stage values + adaptive policy + dynamic limit
-Reports goodput (SLO-meeting completions per second over the 30-minute
-window, R25) per (CV, rate, system).  Usage: python tools/cv_sweep.py [traces_per_rate]"""
+Every run stops at the 30-minute horizon (R28: max_iters = H / T^fwd);
+requests unfinished then are excluded from attainment and counted as
+incomplete.  Reports goodput (SLO-meeting completions per second
+over the window, R25) and the incomplete share per (CV, rate, system).  Usage: python tools/cv_sweep.py [traces_per_rate]"""
 import json
 import os
 import sys
@@ -52,14 +54,19 @@ def main():
         probe.close()
         s = aug.Scheduler(tracegen.PRESET_7B, ip, n_inst, ma)
         t0 = time.time()
-        res = aug.results_to_numpy(s.simulate(gt, torch.from_numpy(tid).cuda()))
+        max_iters = H // tracegen.PRESET_7B["t_fwd_ticks"]          # stop at the horizon (R28)
+        res = aug.results_to_numpy(s.simulate(gt, torch.from_numpy(tid).cuda(), max_iters))
         s.sync()
         dt = time.time() - t0
         s.close()
-        slo = res["f"][:, aug.RESULT_FIELDS.index("slo_ok")].astype(np.float64).reshape(n_traces, len(names))
+        F = lambda k: res["f"][:, aug.RESULT_FIELDS.index(k)].astype(np.float64).reshape(n_traces, len(names))
+        slo, inc, nreq = F("slo_ok"), F("incomplete"), F("n_requests")
         for ri, r in enumerate(RATES):
-            g = slo[ri * per_rate:(ri + 1) * per_rate].mean(axis=0) / 1800.0
+            rs = slice(ri * per_rate, (ri + 1) * per_rate)
+            g = slo[rs].mean(axis=0) / 1800.0
             out["goodput_req_s"][f"cv{cv}_rate{r}"] = {nm: round(float(x), 4) for nm, x in zip(names, g)}
+            out.setdefault("incomplete_share", {})[f"cv{cv}_rate{r}"] = {
+                nm: round(float(x), 4) for nm, x in zip(names, inc[rs].sum(axis=0) / nreq[rs].sum(axis=0))}
         print(f"cv {cv}: {n_inst} instances simulated in {dt:.1f} s", flush=True)
     print(json.dumps(out))
 
