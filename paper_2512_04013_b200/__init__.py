@@ -85,9 +85,12 @@ def lib():
     """Load libaugsched.so (raises if it has not been built)."""
     global _lib
     if _lib is None:
-        if not os.path.exists(LIB_PATH):
-            raise RuntimeError(f"libaugsched.so not built at {LIB_PATH}; run __graft_entry__.build()")
-        L = C.CDLL(LIB_PATH)
+        # AUGSCHED_LIB: another build of this library (the AUGSCHED_DEBUG
+        # variant, _build.build_debug); there is no fallback of any kind
+        path = os.environ.get("AUGSCHED_LIB", LIB_PATH)
+        if not os.path.exists(path):
+            raise RuntimeError(f"libaugsched.so not built at {path}; run __graft_entry__.build()")
+        L = C.CDLL(path)
         vp, u32, u64 = C.c_void_p, C.c_uint32, C.c_uint64
         L.augsched_create.argtypes = [C.POINTER(Config), vp, u32, u32, C.c_int, vp, C.POINTER(vp)]
         L.augsched_enqueue.argtypes = [vp, u32, C.POINTER(RecordSoA), u32, C.c_int]

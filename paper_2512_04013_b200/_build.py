@@ -35,19 +35,35 @@ def stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not stale():
+def build(force: bool = False, verbose: bool = False, out: str | None = None, extra_flags=()) -> str:
+    """Compile libaugsched.so (or, with `out`, a variant such as the
+    AUGSCHED_DEBUG build at DEBUG_LIB)."""
+    dst = out or LIB
+    if not force and out is None and not stale():
         return LIB
+    if out is not None and not force and os.path.exists(dst) and os.path.getmtime(dst) >= os.path.getmtime(LIB) \
+            and not stale():
+        return dst
     extra = os.environ.get("AUGSCHED_NVCC_EXTRA", "").split()  # tuning experiments only
-    cmd = [_nvcc(), *NVCC_FLAGS, *extra, "-shared", "-I", os.path.join(ROOT, "include"),
-           *[os.path.join(CSRC, s) for s in SOURCES], "-o", LIB + ".tmp"]
+    cmd = [_nvcc(), *NVCC_FLAGS, *extra, *extra_flags, "-shared", "-I", os.path.join(ROOT, "include"),
+           *[os.path.join(CSRC, s) for s in SOURCES], "-o", dst + ".tmp"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError("nvcc failed:\n" + r.stdout + r.stderr)
     if verbose:
         print(r.stderr)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(dst + ".tmp", dst)
+    return dst
+
+
+DEBUG_LIB = os.path.join(PKG, "libaugsched_debug.so")
+
+
+def build_debug(force: bool = False) -> str:
+    """The AUGSCHED_DEBUG build: device checks of the SURVEY §8(c).4
+    invariants (sum of grants <= B, ledger A + P <= cap, the limit inside
+    its clamp) latch E_STATE.  Loaded by setting AUGSCHED_LIB to its path."""
+    return build(force=force, out=DEBUG_LIB, extra_flags=("-DAUGSCHED_DEBUG",))
 
 
 if __name__ == "__main__":

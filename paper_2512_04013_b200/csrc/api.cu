@@ -282,6 +282,7 @@ int augsched_sync(augsched_t* h) {
   if (err & 1u) return fail(AUGSCHED_E_STATE, "a record violated the request state machine");
   if (err & 2u) return fail(AUGSCHED_E_CAPACITY, "a trace is longer than max_active_per_instance");
   if (err & 4u) return fail(AUGSCHED_E_INVALID, "a request has n_seg outside [1, 255]");
+  if (err & 8u) return fail(AUGSCHED_E_STATE, "an invariant of SURVEY 8(c).4 failed (AUGSCHED_DEBUG build)");
   return AUGSCHED_OK;
 }
 

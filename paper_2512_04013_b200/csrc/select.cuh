@@ -95,7 +95,7 @@ __device__ void wselect(SelBinsT<RB>& sb, SelRes& s, uint32_t n, uint64_t D, int
         if (lane == __ffs(peers) - 1) {
           atomicAdd(&wbin[dig], (unsigned long long)sum);
           atomicAdd(&cbin[dig], (unsigned)__popc(peers));
-          wkey[dig] = key;
+          atomicExch(&wkey[dig], (unsigned long long)key);   // a witness: read only when the bin holds one item
         }
       }
     }

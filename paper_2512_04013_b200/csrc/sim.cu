@@ -86,12 +86,17 @@ __device__ __forceinline__ void ISYNC() {
 #define AUGSCHED_SIM_PSYNC 24
 #endif
 constexpr int SIM_PHASES = SIM_WPC > 1 ? __builtin_popcount(AUGSCHED_SIM_PSYNC) : 0;
+// Every phase fence is this one barrier instruction (not inlined), so warps
+// that reach a fence from different places of the step -- a warp that
+// skips the rest of its step passes its remaining fences in phase_rest --
+// still meet at the same bar.sync.
+__device__ __noinline__ void cta_fence() { __syncthreads(); }
 template <int I>
 __device__ __forceinline__ void phase_bar(int& nb) {
-  if (SIM_WPC > 1 && ((AUGSCHED_SIM_PSYNC >> I) & 1)) { __syncthreads(); ++nb; }
+  if (SIM_WPC > 1 && ((AUGSCHED_SIM_PSYNC >> I) & 1)) { cta_fence(); ++nb; }
 }
 __device__ __forceinline__ void phase_rest(int& nb) {
-  if (SIM_PHASES) for (; nb < SIM_PHASES; ++nb) __syncthreads();
+  if (SIM_PHASES) for (; nb < SIM_PHASES; ++nb) cta_fence();
 }
 __device__ __forceinline__ int isync_count(bool x) {
   if (SIM_WPC > 1) { __syncwarp(); return __popc(__ballot_sync(FULL, x)); }
@@ -240,6 +245,7 @@ __device__ void compact_list(SimShm& s, const List& l, int L, unsigned int& n_re
   ISYNC();
   const uint32_t nh = s.nholes[L];
   if (nh == 0) return;
+  ISYNC();   // every lane has read nholes before thread 0 clears it
   if (nh <= HOLE_CAP) {
     if (tid == 0) {
       const uint32_t n = n_ref, n_new = n - nh;
@@ -467,6 +473,7 @@ __device__ bool inst_step(const SimParams& p, SimShm& s) {
       if (cnt < SIM_NT) break;
     }
     // ---- idle jump (not counted) or S4 token limit ---------------------------
+    ISYNC();   // every lane has read t / tT / run before thread 0 may move them
     if (tid == 0) {
       s.idle = 0;
       if (s.n_r + s.n_w == 0) {
@@ -893,6 +900,10 @@ __device__ bool inst_step(const SimParams& p, SimShm& s) {
       accP += __shfl_xor_sync(FULL, accP, o);
       accW2 += __shfl_xor_sync(FULL, accW2, o);
     }
+#ifdef AUGSCHED_DEBUG
+    // §8(c).4: the step's grants fit the limit (R17: sum g <= B)
+    if (lane == 0 && (long long)my_tok > (B > 0 ? B : 0)) err_set(p, 8u);
+#endif
     if (lane == 0) {
       if (my_tok) cinc(s, AUGSCHED_R_TOKENS, my_tok);
       if (my_adm) cinc(s, AUGSCHED_R_ADMITTED, my_adm);
@@ -906,6 +917,15 @@ __device__ bool inst_step(const SimParams& p, SimShm& s) {
   compact_list(s, c.W, 1, s.n_w);
   if (tid == 0) {
     if (s.A < 0 || s.P < 0 || s.A + s.P > cap) s.cnt[AUGSCHED_R_ERR] |= 1;
+#ifdef AUGSCHED_DEBUG
+    // §8(c).4: ledger inside the capacity; a dynamic limit inside its clamp
+    if (s.A < 0 || s.P < 0 || s.A + s.P > cap) err_set(p, 8u);
+    if (s.ip.budget_mode == AUGSCHED_BUDGET_DYNAMIC) {
+      const long long lo = (long long)floor(p.cfg.beta_low * (double)s.ip.target_max);
+      const long long hi = (long long)floor(p.cfg.beta_high * (double)s.ip.target_max);
+      if (B < lo || B > hi) err_set(p, 8u);
+    }
+#endif
     s.t = t + 1;                                       // S12
     prep_step(p, s, n);
   }

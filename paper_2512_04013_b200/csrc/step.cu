@@ -81,7 +81,20 @@ struct Slots {
   const unsigned long long *claimA, *claimB;   // winning record per slot and phase (duplicates: E_STATE)
   uint32_t batch;
   uint32_t* gdirty;   // per instance: grant[] positions [0, gdirty) may be nonzero (the full step clears)
+  uint32_t* err;      // device error word (AUGSCHED_DEBUG invariant checks: bit 8)
 };
+
+#ifdef AUGSCHED_DEBUG
+// §8(c).4 after a step's accounting: sum of grants <= B, ledger non-negative
+// (A + P <= cap is the simulator's invariant: step-mode IMPORTs may start a
+// handle above its capacity)
+__device__ __forceinline__ void debug_check_step(const Slots& S, uint32_t inst, unsigned long long gsum,
+                                                 long long B, int64_t cap) {
+  (void)cap;
+  const long long A = *(volatile long long*)&S.A[inst], P = *(volatile long long*)&S.P[inst];
+  if ((long long)gsum > (B > 0 ? B : 0) || A < 0 || P < 0) atomicOr(S.err, 8u);
+}
+#endif
 
 __device__ __forceinline__ void ledger_add(long long* x, long long d) {
   atomicAdd(reinterpret_cast<unsigned long long*>(x), (unsigned long long)d);
@@ -704,6 +717,9 @@ __global__ void __launch_bounds__(ANT) admit_kernel(Slots S, augsched_config cfg
     const long long a = ld_ll(&S.A[i]) + (long long)tot;
     S.A[i] = a;
     S.Aevt[i] = a;
+#ifdef AUGSCHED_DEBUG
+    debug_check_step(S, i, tot, B, cap);
+#endif
   }
 }
 
@@ -1088,6 +1104,9 @@ __device__ void pf_finish(const Slots& S, const augsched_config& cfg, int64_t ca
     const long long a = ld_ll(&S.A[inst]) + (long long)tot;
     S.A[inst] = a;
     S.Aevt[inst] = a;
+#ifdef AUGSCHED_DEBUG
+    debug_check_step(S, inst, tot, B, cap);
+#endif
   }
 }
 
@@ -1144,7 +1163,9 @@ __device__ __forceinline__ bool pf_arrive_last(uint32_t* ctr, uint32_t G, uint32
     if (flag) __threadfence();
   }
   __syncthreads();
-  return flag != 0;
+  const bool last = flag != 0;
+  __syncthreads();   // every thread has read `flag` before thread 0 may reuse it
+  return last;
 }
 
 // Epoch-tagged flag word: (epoch << 2) | value.  Wait until this call's
@@ -1160,7 +1181,9 @@ __device__ __forceinline__ uint32_t pf_wait(const uint32_t* w, uint32_t ep, uint
     flag = v & 3u;
   }
   __syncthreads();
-  return flag;
+  const uint32_t r = flag;
+  __syncthreads();   // every thread has read `flag` before thread 0 may reuse it
+  return r;
 }
 
 
@@ -1638,6 +1661,7 @@ __global__ void __launch_bounds__(NT, (NT == 256 && E == 8) ? AUGSCHED_FM_MINB :
     budget[inst] = B_s;
     tc_s[0] = tc_s[1] = tc_s[2] = 0;
   }
+  __syncthreads();   // the tier counters are clear before any warp adds to them
   // ---- words of every slot (a4), per-tier counts
   uint32_t tcount[3] = {0u, 0u, 0u};
   {
@@ -2134,9 +2158,9 @@ int grow_records(StepState& st, uint32_t need, cudaStream_t s) {
   return AUGSCHED_OK;
 }
 
-Slots slots_of(StepState& st, const augsched_instance_params* d_ip) {
+Slots slots_of(StepState& st, const augsched_instance_params* d_ip, uint32_t* d_err) {
   return Slots{st.st, st.V, st.last, st.ctx, st.kv, st.cpu, st.pend, st.A, st.P, st.Aevt, st.Asnap,
-               st.coef, d_ip, st.max_active, st.wkv, st.claimA, st.claimB, st.rec_batch, st.gdirty};
+               st.coef, d_ip, st.max_active, st.wkv, st.claimA, st.claimB, st.rec_batch, st.gdirty, d_err};
 }
 
 }  // namespace
@@ -2331,7 +2355,7 @@ int step_run_prefix(StepState& st, const augsched_config& cfg, int64_t cap,
   const size_t msmem = sizeof(unsigned long long) * ((size_t)st.max_active + 2 * (size_t)scap);
   if (st.max_limit > PF_SCAP || (st.n_inst > 1 && msmem > PF_MULTI_SMEM))
     return step_run(st, cfg, cap, d_ip, d_err, now, out, s, launches);
-  Slots S = slots_of(st, d_ip);
+  Slots S = slots_of(st, d_ip, d_err);
   run_records(st, S, d_err, now, s, launches);
   if (st.n_inst > 1) {
 #ifndef AUGSCHED_PF_MULTI_SMALL
@@ -2400,7 +2424,7 @@ static void launch_full_multi(const StepState& st, const Slots& S, const augsche
 int step_run(StepState& st, const augsched_config& cfg, int64_t cap,
              const augsched_instance_params* d_ip, uint32_t* d_err, uint64_t now,
              augsched_step_out* out, cudaStream_t s, uint64_t* launches) {
-  Slots S = slots_of(st, d_ip);
+  Slots S = slots_of(st, d_ip, d_err);
   const uint32_t ni = st.n_inst;
   run_records(st, S, d_err, now, s, launches);
 #ifndef AUGSCHED_NO_FULL_COOP
