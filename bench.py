@@ -226,7 +226,7 @@ def _records(n, **kw):
     return _REC_CACHE[key]
 
 
-def step_bench(args, dev, stream, peak, prefix=False, n_override=None):
+def step_bench(args, dev, stream, peak, prefix=False, n_override=None, ranking=0):
     """Config 4: one scheduling step over one queue of n requests (default
     1,000,000), K consecutive steps, each timed with CUDA events after an L2
     flush.  prefix=False: augsched_step (full stable order; one cooperative
@@ -236,7 +236,8 @@ def step_bench(args, dev, stream, peak, prefix=False, n_override=None):
     import paper_2512_04013_b200 as aug
     n = n_override or args.step_n
     rec = _records(n)
-    s = aug.Scheduler(tracegen.PRESET_CFG4, tracegen.inst_params(1), 1, n, device=dev, stream=stream)
+    s = aug.Scheduler(tracegen.PRESET_CFG4, tracegen.inst_params(1, ranking=ranking), 1, n, device=dev,
+                      stream=stream)
     s.enqueue(0, rec)
     flush = torch.empty(512 * 2**20, dtype=torch.uint8, device=f"cuda:{dev}")
     t = 65536
@@ -262,10 +263,13 @@ def step_bench(args, dev, stream, peak, prefix=False, n_override=None):
     ach = 32.0 * n / (ms / 1e3) / 1e9
     what = ("augsched_step_prefix: one cooperative kernel (streaming pass against the previous step's anchor, "
             "one CTA sorts and admits the candidates)" if prefix else
+            "augsched_step, time-invariant keys (ranking 3, reading B12): one cooperative kernel merges the "
+            "slots changed since the last step into the previous order, then admits" if ranking == 3 else
             "augsched_step: one cooperative kernel (keys, 4 stable LSD passes with grid barriers, admission)")
     traffic = None
     try:   # ncu DRAM bytes per steady launch of the same command (profiles/step_*_traffic.json)
         tj = json.load(open(os.path.join(ROOT, "profiles", "step_prefix_traffic.json" if prefix
+                                         else "step_ti_traffic.json" if ranking == 3
                                          else "step_full_traffic.json")))
         traffic = tj["sizes"].get(str(n), {}).get("dram_bytes_per_launch_mean")
     except (OSError, ValueError, KeyError):
@@ -539,11 +543,12 @@ def run_gpu(args):
     if rank == 0 and not args.no_step:
         line["step_1m"] = step_bench(args, dev, stream, peak)
         line["step_1m_prefix"] = step_bench(args, dev, stream, peak, prefix=True)
+        line["step_1m_ti"] = step_bench(args, dev, stream, peak, ranking=3)
         # size sweeps: queues beyond L2 show the HBM-bound regime
-        for key, pre in (("step_1m", False), ("step_1m_prefix", True)):
+        for key, pre, rk in (("step_1m", False, 0), ("step_1m_prefix", True, 0), ("step_1m_ti", False, 3)):
             sweep = {}
             for n_sw in (4_194_304, 16_000_000):
-                r_sw = step_bench(args, dev, stream, peak, prefix=pre, n_override=n_sw)
+                r_sw = step_bench(args, dev, stream, peak, prefix=pre, n_override=n_sw, ranking=rk)
                 sweep[str(n_sw)] = {"value": r_sw["value"], "ms_per_step_cold_l2": r_sw["ms_per_step_cold_l2"],
                                     "roofline_frac": r_sw["roofline"]["frac"],
                                     "achieved_gbs": r_sw["roofline"]["achieved"],

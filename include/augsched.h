@@ -73,6 +73,12 @@ extern "C" {
 #define AUGSCHED_RANK_RANDOM 2        /* random scheduling of P:266-273: a fresh shuffle every
                                          iteration, key = hi32(mix(mix(rank_seed<<32 | id) ^ t))
                                          with mix = the SplitMix64 output function (reading B8) */
+#define AUGSCHED_RANK_AUGSERVE_TI 3   /* time-invariant form of Eq.26 (reading B12):
+                                         key = orderable_u32(fp32(V + alpha*(last*T))); between two events
+                                         it ranks like V - alpha*(now-last)*T in exact arithmetic, and a
+                                         waiting request's key never changes, so augsched_step on a
+                                         single-instance handle keeps the order incrementally (merge of the
+                                         changed entries into the previous order) */
 #define AUGSCHED_BUDGET_DYNAMIC 0     /* Eq.27-32 + clamp */
 #define AUGSCHED_BUDGET_STATIC 1      /* fixed l_static tokens */
 #define AUGSCHED_POLICY_ARGMIN 0      /* Eq.7-8 */

@@ -44,7 +44,7 @@ struct OInst {                // per-instance sweep parameters
   double alpha;               // anti-starvation coefficient (Eq.26)
   uint64_t slo_ttft_ticks;    // TTFT SLO
   uint32_t slo_norm_num, slo_norm_den;  // normalized latency < num/den * T
-  uint32_t ranking;           // 0 AugServe value order, 1 FCFS, 2 random
+  uint32_t ranking;           // 0 AugServe value order, 1 FCFS, 2 random, 3 time-invariant (B12)
   uint32_t budget_mode;       // 0 dynamic (Eq.27-32), 1 static
   uint32_t policy_mode;       // 0 argmin (Eq.7-8), 1 Preserve, 2 Swap, 3 Discard
   uint32_t rank_seed;         // seed of random scheduling (ranking 2)
@@ -183,10 +183,24 @@ uint32_t random_key(uint32_t seed, uint32_t id, uint64_t t) {
   return (uint32_t)(splitmix64_mix(a ^ t) >> 32);
 }
 
-// The order key of a queued request: Eq.26 value order, FCFS or random.
+// Reading B12: the time-invariant form of Eq.26.  Between two
+// events V - alpha*(now - last)*T and V + alpha*last*T differ by the same
+// alpha*now*T for every request, so they rank alike in exact arithmetic;
+// this form is rounded once to fp32 like R3.
+uint32_t ti_key(double V, double alpha, double Ts, uint64_t last) {
+  double s = V + (alpha * ((double)last * Ts));
+  float f = (float)s;
+  uint32_t u;
+  std::memcpy(&u, &f, 4);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
+// The order key of a queued request: Eq.26 value order, FCFS, random or the
+// time-invariant value order.
 uint32_t order_key(const OInst& ip, double V, double Ts, uint64_t now, uint64_t last, uint32_t id) {
   if (ip.ranking == 1) return 0u;                        // FCFS (R33)
   if (ip.ranking == 2) return random_key(ip.rank_seed, id, now);
+  if (ip.ranking == 3) return ti_key(V, ip.alpha, Ts, last);
   return sched_key(V, ip.alpha, Ts, now, last);
 }
 

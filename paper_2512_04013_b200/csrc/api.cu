@@ -114,7 +114,7 @@ int validate_params(const augsched_instance_params& p, uint32_t i) {
   if (!(p.alpha >= 0.0) || !std::isfinite(p.alpha))
     return fail(AUGSCHED_E_INVALID, "instance %u: alpha must be finite and >= 0", i);
   if (p.slo_norm_den < 1) return fail(AUGSCHED_E_INVALID, "instance %u: slo_norm_den must be >= 1", i);
-  if (p.ranking > 2 || p.budget_mode > 1 || p.policy_mode > 3)
+  if (p.ranking > 3 || p.budget_mode > 1 || p.policy_mode > 3)
     return fail(AUGSCHED_E_INVALID, "instance %u: bad ranking/budget_mode/policy_mode", i);
   if (p.l_static > (1u << 26)) return fail(AUGSCHED_E_INVALID, "instance %u: l_static too large", i);
   return AUGSCHED_OK;
@@ -181,7 +181,7 @@ int augsched_create(const augsched_config* cfg, const augsched_instance_params* 
   if (rc) return rc;
   std::vector<augsched_instance_params> ip(n_instances);
   uint32_t max_limit = 0;
-  bool any_random = false;
+  bool any_random = false, all_ti = true;
   for (uint32_t i = 0; i < n_instances; ++i) {
     ip[i] = per_inst ? per_inst[i] : cfg->defaults;
     if ((rc = validate_params(ip[i], i))) return rc;
@@ -190,6 +190,7 @@ int augsched_create(const augsched_config* cfg, const augsched_instance_params* 
     const uint32_t lim = ip[i].budget_mode == AUGSCHED_BUDGET_STATIC ? ip[i].l_static : (uint32_t)hi;
     max_limit = lim > max_limit ? lim : max_limit;
     any_random = any_random || ip[i].ranking == AUGSCHED_RANK_RANDOM;
+    all_ti = all_ti && ip[i].ranking == AUGSCHED_RANK_AUGSERVE_TI;
   }
   int ndev = 0;
   CUDA_TRY(cudaGetDeviceCount(&ndev));
@@ -202,6 +203,7 @@ int augsched_create(const augsched_config* cfg, const augsched_instance_params* 
   h->max_active = max_active_per_instance;
   h->st.max_limit = max_limit;
   h->st.pf_spec = !any_random;   // a fresh shuffle every iteration leaves no anchor
+  h->st.ti = all_ti && n_instances == 1;   // incremental full order (reading B12, f1)
   h->device = device;
   h->stream = reinterpret_cast<cudaStream_t>(cuda_stream);
   h->cap = (int64_t)((cfg->g_total - (cfg->g_model + cfg->g_runtime + cfg->g_safety)) /

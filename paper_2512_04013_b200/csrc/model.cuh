@@ -134,11 +134,20 @@ __device__ __forceinline__ uint32_t random_key(uint32_t seed, uint32_t id, uint6
   return (uint32_t)(mix64(mix64(((uint64_t)seed << 32) | id) ^ t) >> 32);
 }
 
+// Reading B12: the time-invariant form V + alpha*(last*T) of
+// Eq.26's score, one RN to fp32 and the same order-preserving map.
+__device__ __forceinline__ uint32_t ti_key(const Coef& k, double V, uint64_t last) {
+  const double s = dadd(V, dmul(k.alpha, dmul(u2d(last), k.Ts)));
+  const uint32_t u = __float_as_uint(__double2float_rn(s));
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
 // Score key of a queued request under the instance's ranking mode.
 __device__ __forceinline__ uint32_t rank_key(const Coef& k, const augsched_instance_params& ip, double V,
                                              uint64_t now, uint64_t last, uint32_t id) {
   if (ip.ranking == AUGSCHED_RANK_FCFS) return 0u;
   if (ip.ranking == AUGSCHED_RANK_RANDOM) return random_key(ip.rank_seed, id, now);
+  if (ip.ranking == AUGSCHED_RANK_AUGSERVE_TI) return ti_key(k, V, last);
   return sched_key(k, V, now, last);
 }
 

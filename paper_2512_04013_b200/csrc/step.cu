@@ -82,7 +82,22 @@ struct Slots {
   uint32_t batch;
   uint32_t* gdirty;   // per instance: grant[] positions [0, gdirty) may be nonzero (the full step clears)
   uint32_t* err;      // device error word (AUGSCHED_DEBUG invariant checks: bit 8)
+  // time-invariant keys (ranking 3, one instance): slots whose packed word
+  // changes are listed per step epoch (records of epoch e and the grants /
+  // evictions of step e-1 are marked e); null otherwise
+  uint32_t *dmark, *dlist, *dcnt;
+  uint32_t ti_ep;
 };
+
+constexpr uint32_t TI_DCAP = 8192;   // changed slots one incremental step merges (else a full sort)
+
+__device__ __forceinline__ void mark_dirty(const Slots& S, uint32_t g, uint32_t ep) {
+  if (!S.dmark) return;
+  if (atomicExch(&S.dmark[g], ep) != ep) {
+    const uint32_t q = atomicAdd(&S.dcnt[ep & 1], 1u);
+    if (q < TI_DCAP) S.dlist[(ep & 1) * TI_DCAP + q] = g;
+  }
+}
 
 #ifdef AUGSCHED_DEBUG
 // §8(c).4 after a step's accounting: sum of grants <= B, ledger non-negative
@@ -110,6 +125,7 @@ __global__ void rec_phaseA(Rec r, uint32_t n, Slots S, uint32_t* err) {
   // a second CALL/FINISH for the same slot in one batch is a state violation
   // (the oracle applies the first and rejects the rest)
   if (S.claimA[g] != claim_key(S.batch, 0u, j)) { flag_err(err, 1u); return; }
+  mark_dirty(S, g, S.ti_ep);
   const uint32_t inst = g / S.MA;
   const uint32_t st = S.st[g] & 15;
   if (k == AUGSCHED_K_FINISH) {
@@ -142,6 +158,7 @@ __global__ void rec_phaseBC(Rec r, uint32_t n, Slots S, uint64_t now, uint32_t* 
   const uint32_t k = r.kind[j], g = r.id[j];
   if (g == 0xffffffffu || k == AUGSCHED_K_CALL || k == AUGSCHED_K_FINISH) return;
   if (S.claimB[g] != claim_key(S.batch, k != AUGSCHED_K_RETURN, j)) { flag_err(err, 1u); return; }
+  mark_dirty(S, g, S.ti_ep);
   const uint32_t inst = g / S.MA;
   const Coef& c = S.coef[inst];
   const uint32_t pm = S.ip[inst].policy_mode;
@@ -1065,6 +1082,7 @@ __device__ void pf_finish(const Slots& S, const augsched_config& cfg, int64_t ca
           S.kv[base + x] = 0;
           S.cpu[base + x] = 0;
           S.st[base + x] = ST_WAIT | (S.st[base + x] & 0x30u);
+          mark_dirty(S, (uint32_t)(base + x), S.ti_ep + 1);   // its word changes (tier)
           if (gslot[base + x]) gslot[base + x] = 0xFFFFFFFFu;   // grant cancelled
         }
       }
@@ -1095,6 +1113,7 @@ __device__ void pf_finish(const Slots& S, const augsched_config& cfg, int64_t ca
     S.ctx[g_slot] = ctx; S.kv[g_slot] = kv; S.cpu[g_slot] = cpu; S.pend[g_slot] = pend;
     S.last[g_slot] = (uint32_t)now;
     S.st[g_slot] = ST_RUN | (S.st[g_slot] & 0x30u);
+    mark_dirty(S, (uint32_t)g_slot, S.ti_ep + 1);   // last and tier change
   }
   unsigned long long tot;
   block_incl_scan_u64<NT>(dA, wsum, &tot);
@@ -1829,6 +1848,15 @@ struct CoopArgs {
   unsigned long long bar_base;       // its value at this call's start
   long long* budget;
   uint32_t *n_active, *tier_off, *order, *keyout, *grant, *admitted, *gslot;
+  // time-invariant keys (reading B12): the previous order's words and the
+  // output of this one; ti_try: merge the changed slots into tiw_in
+  int ti, ti_try;
+  const unsigned long long* tiw_in;
+  unsigned long long *tiw_out, *ubuf;
+  const uint32_t* ti_n_in;
+  uint32_t* ti_n_out;
+  uint32_t* ti_misc;
+  uint32_t* gcnt;                    // [TI_DCAP + 1] unchanged words per D rank (kept zero between steps)
 };
 
 #ifdef AUGSCHED_COOP_TIMING
@@ -1866,6 +1894,355 @@ __device__ __forceinline__ void coop_barrier(const CoopArgs& a, uint32_t& k) {
 __device__ __forceinline__ int coop_shift(int p) { return PK_KEY + (p == 0 ? 0 : p == 1 ? 9 : p == 2 ? 18 : 26); }
 __device__ __forceinline__ int coop_bits(int p) { return p < 2 ? 9 : 8; }
 
+
+// ---- time-invariant keys: the incremental full order (reading B12, f1) ----
+// Every word of a slot that did not change since the previous step is the
+// word it had then, so the previous order minus the changed slots (U) is
+// still sorted.  The changed slots' current words (D, <= TI_DCAP, sorted in
+// one CTA) are merged in: a U word at compacted index u lands at
+// u + |{d in D : d < w}| (a binary search in shared memory), a D word at
+// index j at j + |{u in U : u < D[j]}| (U words counted by their rank in D;
+// words are unique).  Three grid barriers, then CTA 0 admits over the first
+// min(B, n) positions as in the full path.
+__device__ __forceinline__ uint32_t lower_bound_sm(const unsigned long long* v, uint32_t n, unsigned long long x) {
+  uint32_t lo = 0, hi = n;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (v[mid] < x) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+__device__ void ti_incremental(const CoopArgs& a, unsigned long long* sbuf, unsigned long long* xch, SelShm& sel,
+                               unsigned long long* wsum, unsigned long long& freed, long long& B_s, uint32_t& nbar) {
+  __shared__ uint32_t cnt_s[4], dn_s, base_s2, nu_s;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t G = gridDim.x, c = blockIdx.x;
+  const Slots& S = a.S;
+  const Coef k = S.coef[0];
+  const augsched_instance_params ip = S.ip[0];
+  const uint32_t E = S.ti_ep;
+  const uint32_t nprev = __ldcg(a.ti_n_in);
+  // CTA 0 builds D while CTAs 1 .. G-1 take the previous order in chunks
+  const uint32_t GU = G - 1, cu = c - 1;
+  const uint32_t chunk = ((nprev + GU - 1) / GU + 31) & ~31u;
+  const uint32_t c0 = c == 0 ? 0u : (cu * chunk < nprev ? cu * chunk : nprev);
+  const uint32_t c1 = c == 0 ? 0u : (c0 + chunk < nprev ? c0 + chunk : nprev);
+  // a chunk of <= 8 words per thread stays in registers from A to B
+  // (element c0 + warp * 256 + e * 32 + lane, e < 8)
+  constexpr int TE = 8;
+  const bool reg = c1 - c0 <= (uint32_t)CNT * TE;
+  unsigned long long rw[TE];
+  unsigned rb[TE];          // per e: the warp's ballot of unchanged words
+  uint32_t* pub = a.hist;   // [G][4]: kept words, and their tiers 0..2
+#ifdef AUGSCHED_COOP_TIMING
+#ifndef TT_CTA
+#define TT_CTA 0
+#endif
+  unsigned long long tt[8];
+#define TT(i) do { if (c == TT_CTA && tid == 0) tt[i] = gtime(); } while (0)
+#else
+#define TT(i) do {} while (0)
+#endif
+  TT(0);
+  // ---- A: count the unchanged words of the chunk (and their tiers); CTA 0
+  // builds D (the changed slots' current words, queued ones only), sorted
+  if (tid < 4) cnt_s[tid] = 0;
+  if (tid == 0) dn_s = 0;
+  __syncthreads();
+  {
+    uint32_t kc = 0, t0 = 0, t1 = 0;
+    if (reg) {
+      const uint32_t seg = c0 + (uint32_t)warp * 32 * TE;
+      uint32_t dm[TE];
+#pragma unroll
+      for (int e = 0; e < TE; ++e) {
+        const uint32_t i = seg + e * 32 + lane;
+        rw[e] = i < c1 ? __ldcg(&a.tiw_in[i]) : 0ull;
+      }
+#pragma unroll
+      for (int e = 0; e < TE; ++e) {
+        const uint32_t i = seg + e * 32 + lane;
+        dm[e] = i < c1 ? __ldcg(&S.dmark[(uint32_t)rw[e] & SLOT_MASK]) : E;
+      }
+#pragma unroll
+      for (int e = 0; e < TE; ++e) {
+        const bool keep = dm[e] != E;
+        rb[e] = __ballot_sync(FULL, keep);
+        if (keep) {
+          ++kc;
+          const uint32_t t = (uint32_t)(rw[e] >> PK_TIER);
+          t0 += t == 0; t1 += t == 1;
+        }
+      }
+    } else {
+      for (uint32_t i = c0 + tid; i < c1; i += CNT) {
+        const unsigned long long w = __ldcg(&a.tiw_in[i]);
+        if (__ldcg(&S.dmark[(uint32_t)w & SLOT_MASK]) != E) {
+          ++kc;
+          const uint32_t t = (uint32_t)(w >> PK_TIER);
+          t0 += t == 0; t1 += t == 1;
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      kc += __shfl_xor_sync(FULL, kc, o); t0 += __shfl_xor_sync(FULL, t0, o); t1 += __shfl_xor_sync(FULL, t1, o);
+    }
+    if (lane == 0) { atomicAdd(&cnt_s[0], kc); atomicAdd(&cnt_s[1], t0); atomicAdd(&cnt_s[2], t1); }
+  }
+  if (c == 0) {
+    if (tid == 0) {
+      B_s = token_limit(a.cfg, k, ip, a.cap, ld_ll(&S.A[0]), ld_ll(&S.P[0]));
+      a.budget[0] = B_s;
+    }
+    const uint32_t dc = __ldcg(&S.dcnt[E & 1]);
+    for (uint32_t j = tid; j < dc; j += CNT) {
+      const uint32_t g = __ldcg(&S.dlist[(E & 1) * TI_DCAP + j]);
+      const unsigned long long w = slot_word(k, ip, S.st[g], S.V[g], S.last[g], a.now, g);
+      if ((w >> PK_TIER) < 3) sbuf[atomicAdd(&dn_s, 1u)] = w;
+    }
+    __syncthreads();
+    const uint32_t nd = dn_s;
+    uint32_t P2 = 32;
+    while (P2 < nd) P2 <<= 1;
+    if (P2 <= 1024u) {
+      if ((uint32_t)tid < P2) {
+        unsigned long long v = (uint32_t)tid < nd ? sbuf[tid] : ~0ull;
+        bar_named(P2);
+        switch (P2) {
+          case 32: v = bitonic1<5>(v, sbuf, xch); break;
+          case 64: v = bitonic1<6>(v, sbuf, xch); break;
+          case 128: v = bitonic1<7>(v, sbuf, xch); break;
+          case 256: v = bitonic1<8>(v, sbuf, xch); break;
+          case 512: v = bitonic1<9>(v, sbuf, xch); break;
+          default: v = bitonic1<10>(v, sbuf, xch); break;
+        }
+        bar_named(P2);
+        sbuf[tid] = v;
+      }
+    } else if (P2 == 2048) pf_sortE<CNT, 11>(sbuf, xch, nd);
+    else if (P2 == 4096) pf_sortE<CNT, 12>(sbuf, xch, nd);
+    else pf_sortE<CNT, 13>(sbuf, xch, nd);
+    __syncthreads();
+    uint32_t dt0 = 0, dt1 = 0;
+    for (uint32_t j = tid; j < nd; j += CNT) {
+      a.kB[j] = sbuf[j];
+      const uint32_t t = (uint32_t)(sbuf[j] >> PK_TIER);
+      dt0 += t == 0; dt1 += t == 1;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) { dt0 += __shfl_xor_sync(FULL, dt0, o); dt1 += __shfl_xor_sync(FULL, dt1, o); }
+    __shared__ uint32_t dts[2];
+    if (tid == 0) { dts[0] = 0; dts[1] = 0; }
+    __syncthreads();
+    if (lane == 0) { atomicAdd(&dts[0], dt0); atomicAdd(&dts[1], dt1); }
+    __syncthreads();
+    if (tid == 0) { a.ti_misc[0] = nd; a.ti_misc[1] = dts[0]; a.ti_misc[2] = dts[1]; }
+  }
+  __syncthreads();
+  if (tid < 3) pub[c * 4 + tid] = cnt_s[tid];
+  TT(1);
+  coop_barrier(a, nbar);
+  TT(2);
+  // ---- B: compact the unchanged words (stable) into ubuf and place them
+  const uint32_t nd = __ldcg(&a.ti_misc[0]);
+  for (uint32_t j = tid; j < nd; j += CNT) sbuf[j] = __ldcg(&a.kB[j]);
+  if (tid < 32) {
+    uint32_t bsum = 0, tsum = 0;
+    uint32_t v[8];   // G <= 256: every load in flight at once
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const uint32_t cc = lane + 32 * q;
+      v[q] = cc < G ? __ldcg(&pub[cc * 4]) : 0u;
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      tsum += v[q];
+      if (lane + 32 * q < c) bsum += v[q];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) { bsum += __shfl_xor_sync(FULL, bsum, o); tsum += __shfl_xor_sync(FULL, tsum, o); }
+    if (lane == 0) { base_s2 = bsum; nu_s = tsum; }
+  }
+  __syncthreads();
+  uint32_t* lh = reinterpret_cast<uint32_t*>(xch);   // this CTA's unchanged words per D rank
+  for (uint32_t j = tid; j <= nd; j += CNT) lh[j] = 0;
+  if (reg && c1 > c0) {
+    // warp totals -> the warp's first compacted index
+    uint32_t wt = 0;
+#pragma unroll
+    for (int e = 0; e < TE; ++e) wt += __popc(rb[e]);
+    if (lane == 0) wsum[warp] = wt;
+    __syncthreads();
+    uint32_t u = base_s2;
+    for (int w2 = 0; w2 < warp; ++w2) u += (uint32_t)wsum[w2];
+    const uint32_t seg = c0 + (uint32_t)warp * 32 * TE;
+#pragma unroll
+    for (int e = 0; e < TE; ++e) {
+      const bool keep = (rb[e] >> lane) & 1u;
+      const uint32_t i = seg + e * 32 + lane;
+      uint32_t l = 0xFFFFFFFFu;
+      if (keep) {
+        const unsigned long long w = rw[e];
+        l = lower_bound_sm(sbuf, nd, w);
+        const uint32_t pos = u + __popc(rb[e] & ((1u << lane) - 1)) + l;
+        const uint32_t x = (uint32_t)w & SLOT_MASK;
+        a.tiw_out[pos] = w;
+        a.order[pos] = x;
+        a.keyout[pos] = (uint32_t)(w >> PK_KEY);
+        if (pos < a.max_limit) {
+          prefetch_l2(&S.ctx[x]); prefetch_l2(&S.kv[x]); prefetch_l2(&S.cpu[x]); prefetch_l2(&S.pend[x]);
+        }
+      }
+      (void)i;
+      if (nd > 0) {
+        const unsigned peers = __match_any_sync(FULL, l);
+        if (keep && lane == __ffs(peers) - 1) atomicAdd(&lh[l], (unsigned)__popc(peers));
+      }
+      u += __popc(rb[e]);
+    }
+  } else {
+    uint32_t run = base_s2;
+    for (uint32_t b0 = c0; b0 < c1; b0 += CNT) {     // block-uniform trip count
+      const uint32_t i = b0 + tid;
+      unsigned long long w = 0;
+      bool keep = false;
+      if (i < c1) {
+        w = __ldcg(&a.tiw_in[i]);
+        keep = __ldcg(&S.dmark[(uint32_t)w & SLOT_MASK]) != E;
+      }
+      const unsigned bal = __ballot_sync(FULL, keep);
+      if (lane == 0) wsum[warp] = __popc(bal);
+      __syncthreads();
+      uint32_t before = 0, tile = 0;
+      for (int w2 = 0; w2 < CNW; ++w2) { const uint32_t x = (uint32_t)wsum[w2]; before += w2 < warp ? x : 0u; tile += x; }
+      uint32_t l = 0xFFFFFFFFu;
+      if (keep) {
+        const uint32_t u = run + before + __popc(bal & ((1u << lane) - 1));
+        l = lower_bound_sm(sbuf, nd, w);
+        const uint32_t pos = u + l;
+        const uint32_t x = (uint32_t)w & SLOT_MASK;
+        a.tiw_out[pos] = w;
+        a.order[pos] = x;
+        a.keyout[pos] = (uint32_t)(w >> PK_KEY);
+        if (pos < a.max_limit) {
+          prefetch_l2(&S.ctx[x]); prefetch_l2(&S.kv[x]); prefetch_l2(&S.cpu[x]); prefetch_l2(&S.pend[x]);
+        }
+      }
+      // how many unchanged words fall below each D word: count them by
+      // their D rank l (a word is below D[j] iff l <= j); the ranks of a
+      // chunk's words are few and sorted, so one atomic per distinct rank
+      // and warp
+      if (nd > 0) {
+        const unsigned peers = __match_any_sync(FULL, l);
+        if (keep && lane == __ffs(peers) - 1) atomicAdd(&lh[l], (unsigned)__popc(peers));
+      }
+      run += tile;
+      __syncthreads();
+    }
+  }
+  // the CTA's counts per D rank to the global ones (a chunk's words are a
+  // narrow key range: few nonzero ranks)
+  __syncthreads();
+  if (nd > 0)
+    for (uint32_t j = tid; j <= nd; j += CNT)
+      if (lh[j]) atomicAdd(&a.gcnt[j], lh[j]);
+  TT(3);
+  coop_barrier(a, nbar);
+  TT(4);
+  // ---- C: place the changed words (D[j] lands at j + the unchanged words
+  // with rank <= j: an inclusive scan of the rank counts); queue size and
+  // tier starts
+  const uint32_t nu = nu_s;
+  if (c * CNT < nd) {
+    uint32_t* cs = reinterpret_cast<uint32_t*>(xch);   // inclusive scan of gcnt[0 .. nd)
+    constexpr int PER = TI_DCAP / CNT;
+    uint32_t v[PER], sum = 0;
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      const uint32_t j = tid * PER + q;
+      v[q] = j < nd ? __ldcg(&a.gcnt[j]) : 0u;
+      sum += v[q];
+    }
+    uint32_t inc = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(FULL, inc, o);
+      if (lane >= o) inc += y;
+    }
+    if (lane == 31) wsum[warp] = inc;
+    __syncthreads();
+    uint32_t run = inc - sum;
+    for (int w2 = 0; w2 < warp; ++w2) run += (uint32_t)wsum[w2];
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      run += v[q];
+      cs[tid * PER + q] = run;
+    }
+    __syncthreads();
+  }
+  for (uint32_t j = c * CNT + tid; j < nd; j += G * CNT) {
+    const unsigned long long w = sbuf[j];
+    const uint32_t pos = j + reinterpret_cast<const uint32_t*>(xch)[j];
+    const uint32_t x = (uint32_t)w & SLOT_MASK;
+    a.tiw_out[pos] = w;
+    a.order[pos] = x;
+    a.keyout[pos] = (uint32_t)(w >> PK_KEY);
+    if (pos < a.max_limit) {
+      prefetch_l2(&S.ctx[x]); prefetch_l2(&S.kv[x]); prefetch_l2(&S.cpu[x]); prefetch_l2(&S.pend[x]);
+    }
+  }
+  if (c == 0 && tid < 32) {
+    uint32_t u0 = 0, u1 = 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const uint32_t cc = lane + 32 * q;
+      if (cc < G) { u0 += __ldcg(&pub[cc * 4 + 1]); u1 += __ldcg(&pub[cc * 4 + 2]); }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) { u0 += __shfl_xor_sync(FULL, u0, o); u1 += __shfl_xor_sync(FULL, u1, o); }
+    if (lane == 0) {
+      const uint32_t n = nu + nd;
+      const uint32_t t0 = u0 + __ldcg(&a.ti_misc[1]), t1 = u1 + __ldcg(&a.ti_misc[2]);
+      a.n_active[0] = n;
+      *a.ti_n_out = n;
+      a.tier_off[0] = 0;
+      a.tier_off[1] = t0;
+      a.tier_off[2] = t0 + t1;
+    }
+  }
+  TT(5);
+  coop_barrier(a, nbar);
+  TT(6);
+#ifdef AUGSCHED_COOP_TIMING
+  if (c == TT_CTA && c != 0 && tid == 0)
+    printf("ti_t cta %u ns: nd %u | %llu %llu %llu %llu %llu %llu\n", c, nd, tt[1] - tt[0], tt[2] - tt[0],
+           tt[3] - tt[0], tt[4] - tt[0], tt[5] - tt[0], tt[6] - tt[0]);
+#endif
+  if (c != 0) return;
+  for (uint32_t j = tid; j <= nd; j += CNT) a.gcnt[j] = 0;   // clear for the next step
+  // ---- F: admission over the first min(B, n) positions (CTA 0)
+  const uint32_t n = __ldcg(&a.n_active[0]);
+  const long long B = B_s;
+  const uint32_t target = pf_target(B, n);
+  for (uint32_t i = tid; i < target; i += CNT) sbuf[i] = __ldcg(&a.tiw_out[i]);
+  const uint32_t prev = S.gdirty[0];
+  __syncthreads();
+  pf_finish<CNT, PF_SCAP / CNT, true>(S, a.cfg, a.cap, a.now, 0, 0, nullptr, sbuf, nullptr, target, target, B,
+                                      a.order, a.keyout, a.grant, a.admitted, a.gslot, sel, wsum, freed);
+  __syncthreads();
+  const uint32_t adm = a.admitted[0];
+  for (uint32_t j = adm + tid; j < prev && j < a.N; j += CNT) a.grant[j] = 0;
+  if (tid == 0) S.gdirty[0] = adm;
+#ifdef AUGSCHED_COOP_TIMING
+  TT(7);
+  if (tid == 0) printf("ti_t ns: nd %u | %llu %llu %llu %llu %llu %llu %llu\n", nd, tt[1] - tt[0], tt[2] - tt[0],
+                       tt[3] - tt[0], tt[4] - tt[0], tt[5] - tt[0], tt[6] - tt[0], tt[7] - tt[0]);
+#endif
+#undef TT
+}
+
 __global__ void __launch_bounds__(CNT, 1) full_coop_kernel(const __grid_constant__ CoopArgs a) {
   extern __shared__ __align__(16) unsigned long long fc_sm[];
   unsigned long long* sbuf = fc_sm;                                            // [PF_SCAP] (phase F)
@@ -1886,6 +2263,10 @@ __global__ void __launch_bounds__(CNT, 1) full_coop_kernel(const __grid_constant
   const uint32_t c0 = c * chunk < N ? c * chunk : N;
   const uint32_t c1 = c0 + chunk < N ? c0 + chunk : N;
   uint32_t nbar = 0;
+  if (a.ti_try && __ldcg(&S.dcnt[S.ti_ep & 1]) <= TI_DCAP) {   // uniform: the list is final at launch
+    ti_incremental(a, sbuf, reinterpret_cast<unsigned long long*>(wcnt), sel, wsum, freed, B_s, nbar);
+    return;
+  }
 #ifdef AUGSCHED_COOP_TIMING
   unsigned long long ct[32];
 #endif
@@ -1987,6 +2368,7 @@ __global__ void __launch_bounds__(CNT, 1) full_coop_kernel(const __grid_constant
       for (int d = 0; d < NB; ++d) tc[d >> 6] += tot_s[d];
       const uint32_t n = tc[0] + tc[1] + tc[2];
       a.n_active[0] = n;
+      if (a.ti) *a.ti_n_out = n;
       a.tier_off[0] = 0;
       a.tier_off[1] = tc[0];
       a.tier_off[2] = tc[0] + tc[1];
@@ -2038,6 +2420,7 @@ __global__ void __launch_bounds__(CNT, 1) full_coop_kernel(const __grid_constant
           a.order[pos] = x;
           a.keyout[pos] = (uint32_t)(xv[e] >> PK_KEY);
           if (pos < PF_SCAP) a.kpre[pos] = xv[e];
+          if (a.ti) a.tiw_out[pos] = xv[e];   // the order the next step merges into
           if (pos < a.max_limit) {   // the admission (phase F) reads these slots' token state
             prefetch_l2(&S.ctx[x]); prefetch_l2(&S.kv[x]); prefetch_l2(&S.cpu[x]); prefetch_l2(&S.pend[x]);
           }
@@ -2160,14 +2543,18 @@ int grow_records(StepState& st, uint32_t need, cudaStream_t s) {
 
 Slots slots_of(StepState& st, const augsched_instance_params* d_ip, uint32_t* d_err) {
   return Slots{st.st, st.V, st.last, st.ctx, st.kv, st.cpu, st.pend, st.A, st.P, st.Aevt, st.Asnap,
-               st.coef, d_ip, st.max_active, st.wkv, st.claimA, st.claimB, st.rec_batch, st.gdirty, d_err};
+               st.coef, d_ip, st.max_active, st.wkv, st.claimA, st.claimB, st.rec_batch, st.gdirty, d_err,
+               st.ti ? st.dmark : nullptr, st.dlist, st.dcnt, st.ti_ep};
 }
 
 }  // namespace
 
 static size_t pf_smem_bytes() { return sizeof(unsigned long long) * 2 * PF_SCAP; }
 static size_t coop_smem_bytes() {
-  return sizeof(unsigned long long) * PF_SCAP + sizeof(uint16_t) * CNW * CNB;
+  // sbuf [PF_SCAP] + the digit counters [CNW][CNB] (16-bit), which the
+  // incremental path reuses as the bitonic exchange buffer [PF_SCAP]
+  const size_t cnt = sizeof(uint16_t) * CNW * CNB, xch = sizeof(unsigned long long) * PF_SCAP;
+  return sizeof(unsigned long long) * PF_SCAP + (cnt > xch ? cnt : xch);
 }
 static size_t full_multi_smem(int NT, int E) {
   const size_t cnt = sizeof(uint16_t) * 512 * (NT / 32);
@@ -2278,6 +2665,21 @@ int step_ensure(StepState& st, uint32_t n_inst, uint32_t max_active, cudaStream_
     st.coop_bar_base = 0;
     if (st.sms < 128 || st.sms > 256) st.coop_grid = 0;   // column scan: <= 4 digits per CTA, one CTA per thread of a 256-thread group
     if (st.coop_grid > 0 && (rc = salloc(st, &st.coop_hist, 4 * ((size_t)st.coop_grid + 1) * CNB))) return rc;
+    if (st.ti && st.coop_grid > 0) {
+      if ((rc = salloc(st, &st.tiw, N)) || (rc = salloc(st, &st.tiw2, N)) || (rc = salloc(st, &st.ubuf, N)) ||
+          (rc = salloc(st, &st.ti_n, 2)) || (rc = salloc(st, &st.dmark, N)) ||
+          (rc = salloc(st, &st.dlist, 2 * (size_t)TI_DCAP)) || (rc = salloc(st, &st.dcnt, 2)) ||
+          (rc = salloc(st, &st.ti_misc, 4)) || (rc = salloc(st, &st.ti_gcnt, TI_DCAP + 1)))
+        return rc;
+      if ((rc = cuda_check(cudaMemsetAsync(st.ti_gcnt, 0, sizeof(uint32_t) * (TI_DCAP + 1), s), "step_ensure: clear")))
+        return rc;
+      if ((rc = cuda_check(cudaMemsetAsync(st.dmark, 0, sizeof(uint32_t) * N, s), "step_ensure: clear")) ||
+          (rc = cuda_check(cudaMemsetAsync(st.dcnt, 0, 2 * sizeof(uint32_t), s), "step_ensure: clear")) ||
+          (rc = cuda_check(cudaMemsetAsync(st.ti_n, 0, 2 * sizeof(uint32_t), s), "step_ensure: clear")))
+        return rc;
+    } else {
+      st.ti = false;
+    }
   }
   cudaFuncSetAttribute(pf_multi_kernel<PNT, PF_SCAP / PNT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)PF_MULTI_SMEM);
@@ -2345,6 +2747,16 @@ void run_records(StepState& st, Slots S, uint32_t* d_err, uint64_t now, cudaStre
 }  // namespace
 
 
+// Time-invariant handles: the step epoch of the dirty marks, and the clear
+// of the consumed list after the step's kernels.
+static void ti_begin(StepState& st) {
+  if (st.ti) ++st.ti_ep;
+}
+static int ti_end(StepState& st, cudaStream_t s) {
+  if (!st.ti) return AUGSCHED_OK;
+  return cuda_check(cudaMemsetAsync(st.dcnt + (st.ti_ep & 1), 0, sizeof(uint32_t), s), "step: clear");
+}
+
 int step_run_prefix(StepState& st, const augsched_config& cfg, int64_t cap,
                     const augsched_instance_params* d_ip, uint32_t* d_err, uint64_t now,
                     augsched_step_out* out, cudaStream_t s, uint64_t* launches) {
@@ -2355,8 +2767,10 @@ int step_run_prefix(StepState& st, const augsched_config& cfg, int64_t cap,
   const size_t msmem = sizeof(unsigned long long) * ((size_t)st.max_active + 2 * (size_t)scap);
   if (st.max_limit > PF_SCAP || (st.n_inst > 1 && msmem > PF_MULTI_SMEM))
     return step_run(st, cfg, cap, d_ip, d_err, now, out, s, launches);
+  ti_begin(st);
   Slots S = slots_of(st, d_ip, d_err);
   run_records(st, S, d_err, now, s, launches);
+  st.ti_valid = false;   // no full order: the next full step sorts
   if (st.n_inst > 1) {
 #ifndef AUGSCHED_PF_MULTI_SMALL
 #define AUGSCHED_PF_MULTI_SMALL (4 * 256)
@@ -2398,6 +2812,10 @@ int step_run_prefix(StepState& st, const augsched_config& cfg, int64_t cap,
                                               args, pf_smem_bytes(), s);
   if (e != cudaSuccess) return cuda_check(e, "step_prefix: cooperative launch");
   *launches += 1;
+  {
+    const int rc2 = ti_end(st, s);
+    if (rc2) return rc2;
+  }
   out->budget = reinterpret_cast<const int64_t*>(st.budget);
   out->n_active = pa.n_active;
   out->admitted = st.admitted;
@@ -2424,6 +2842,7 @@ static void launch_full_multi(const StepState& st, const Slots& S, const augsche
 int step_run(StepState& st, const augsched_config& cfg, int64_t cap,
              const augsched_instance_params* d_ip, uint32_t* d_err, uint64_t now,
              augsched_step_out* out, cudaStream_t s, uint64_t* launches) {
+  ti_begin(st);
   Slots S = slots_of(st, d_ip, d_err);
   const uint32_t ni = st.n_inst;
   run_records(st, S, d_err, now, s, launches);
@@ -2438,10 +2857,24 @@ int step_run(StepState& st, const augsched_config& cfg, int64_t cap,
     ca.bar_base = st.coop_bar_base;
     ca.budget = st.budget; ca.n_active = st.n_active; ca.tier_off = st.tier_off; ca.order = st.order;
     ca.keyout = st.key; ca.grant = st.grant; ca.admitted = st.admitted; ca.gslot = st.gslot;
+    const uint32_t cur = st.ti_ep & 1;
+    ca.ti = st.ti ? 1 : 0;
+    ca.ti_try = st.ti && st.ti_valid ? 1 : 0;
+    ca.tiw_in = st.tiw; ca.tiw_out = st.tiw2; ca.ubuf = st.ubuf;
+    ca.ti_n_in = st.ti_n ? st.ti_n + (cur ^ 1) : nullptr;
+    ca.ti_n_out = st.ti_n ? st.ti_n + cur : nullptr;
+    ca.ti_misc = st.ti_misc;
+    ca.gcnt = st.ti_gcnt;
     void* args[] = {&ca};
     cudaError_t e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(&full_coop_kernel), st.coop_grid,
                                                 CNT, args, coop_smem_bytes(), s);
     if (e != cudaSuccess) return cuda_check(e, "step: cooperative launch");
+    if (st.ti) {   // the sorted words of this order are the next step's input
+      std::swap(st.tiw, st.tiw2);
+      st.ti_valid = true;
+      int rc2 = ti_end(st, s);
+      if (rc2) return rc2;
+    }
     st.coop_bar_base += 12ull * (unsigned long long)st.coop_grid;   // twelve grid barriers per call
     *launches += 1;
     out->budget = reinterpret_cast<const int64_t*>(st.budget);
@@ -2505,6 +2938,11 @@ int step_run(StepState& st, const augsched_config& cfg, int64_t cap,
   admit_kernel<<<ni, ANT, 0, s>>>(S, cfg, cap, now, st.budget, st.tcnt, st.n_active, st.tier_off, st.order,
                                   st.grant, st.admitted);
   *launches += 1;
+  st.ti_valid = false;
+  {
+    const int rc2 = ti_end(st, s);
+    if (rc2) return rc2;
+  }
   out->budget = reinterpret_cast<const int64_t*>(st.budget);
   out->n_active = st.n_active;
   out->admitted = st.admitted;

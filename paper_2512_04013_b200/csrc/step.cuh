@@ -92,6 +92,19 @@ struct StepState {
   bool pf_dirty = false;                    // a full step ran since: counters need one clear
   int pf_grid = 0;                // prefix step: co-resident CTAs of the cooperative kernel
   int coop_grid = 0;              // full step, one instance: CTAs of the cooperative kernel (0: not used)
+  // time-invariant keys (ranking 3, one instance): the order is kept across
+  // steps; a step merges the slots changed since the last one into it
+  bool ti = false;
+  bool ti_valid = false;          // tiw holds the previous full step's sorted words
+  uint32_t ti_ep = 0;             // step epoch (dirty marks)
+  unsigned long long *tiw = nullptr, *tiw2 = nullptr;   // [N] sorted words (current, next)
+  uint32_t* ti_n = nullptr;       // [1] entries in tiw
+  uint32_t* dmark = nullptr;      // [N] epoch of the slot's last change
+  uint32_t* dlist = nullptr;      // [2][TI_DCAP] changed slots by epoch parity
+  uint32_t* dcnt = nullptr;       // [2] their counts
+  unsigned long long* ubuf = nullptr;   // [N] the unchanged words, compacted
+  uint32_t* ti_misc = nullptr;    // [4] per-call scratch: |D| after filtering, tier counts of D
+  uint32_t* ti_gcnt = nullptr;    // [TI_DCAP + 1] unchanged words per rank among the changed ones
   unsigned long long* coop_bar = nullptr;   // its grid-barrier counter (monotone)
   unsigned long long coop_bar_base = 0;     // the counter's value at the next call's start
   uint32_t* coop_hist = nullptr;            // [4][coop_grid][512] per-CTA digit histograms

@@ -19,7 +19,8 @@ import tempfile
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 SRC = os.path.join(ROOT, "oracle", "augsched_oracle.cpp")
-TESTS = ["tests/test_oracle_formulas.py", "tests/test_oracle_schedules.py", "tests/test_oracle_pins_r2.py"]
+TESTS = ["tests/test_oracle_formulas.py", "tests/test_oracle_schedules.py", "tests/test_oracle_pins_r2.py",
+         "tests/test_oracle_ti.py"]
 
 # name -> (passage, [(old, new), ...]); every `old` must occur exactly once
 MUTANTS = {
@@ -62,6 +63,8 @@ MUTANTS = {
                                "std::max<int64_t>(free_, 0);")]),
     "last_not_set_on_grant": ("R14 last = t on a grant > 0 (simulate)",
                               [("      r.last = t;\n      r.status = RUNNING;\n", "      r.status = RUNNING;\n")]),
+    "ti_key_sign": ("B12 time-invariant key V + alpha*last*T",
+                    [("double s = V + (alpha * ((double)last * Ts));", "double s = V - (alpha * ((double)last * Ts));")]),
     "tie_by_id_desc": ("R2 ties by id ascending (simulate order)",
                        [("    std::sort(ord.begin(), ord.end(), [](const Ent& a, const Ent& b) {\n      return std::tie(a.tier, a.key, a.id) < std::tie(b.tier, b.key, b.id);\n    });\n    // S7 admission: a prefix",
                          "    std::sort(ord.begin(), ord.end(), [](const Ent& a, const Ent& b) {\n      return std::tie(a.tier, a.key, b.id) < std::tie(b.tier, b.key, a.id);\n    });\n    // S7 admission: a prefix")]),
