@@ -322,6 +322,84 @@ def step_multi_bench(args, dev, stream, peak, n_inst=4096, ma=2048):
     return res
 
 
+def sharded_step_bench(args, dev, stream, world, rank, dist, backend, n_total=1_000_000):
+    """config 4's queue of n_total requests split over the
+    ranks (rank r owns global slots [r*n/G, (r+1)*n/G)); one step = the three
+    shard calls around an all-reduce of the ledgers and an all-gather of the
+    offers (NCCL on GPUs).  Time per step = max over ranks, L2 flushed."""
+    import torch
+    import paper_2512_04013_b200 as aug
+    G = world
+    MA = n_total // G
+    rec = _records(n_total)
+    ids = rec["id"].astype(np.int64)
+    m = (ids // MA) == rank
+    sub = {k: np.ascontiguousarray(v[m]) for k, v in rec.items()}
+    sub["id"] = (ids[m] - rank * MA).astype(np.uint32)
+    s = aug.Scheduler(tracegen.PRESET_CFG4, tracegen.inst_params(1), 1, MA, device=dev, stream=stream)
+    s.enqueue(0, sub)
+    ob = s.shard_offer_bytes()
+    led = torch.zeros(2, dtype=torch.int64, device=f"cuda:{dev}")
+    off = torch.zeros(ob, dtype=torch.uint8, device=f"cuda:{dev}")
+    allo = torch.zeros(G * ob, dtype=torch.uint8, device=f"cuda:{dev}")
+    flush = torch.empty(512 * 2**20, dtype=torch.uint8, device=f"cuda:{dev}")
+
+    def coll_sum(t):
+        if dist is None:
+            return t
+        if backend == "nccl":
+            dist.all_reduce(t)
+            return t
+        h = t.cpu()
+        dist.all_reduce(h)
+        t.copy_(h)
+        return t
+
+    def coll_gather(dst, src):
+        if dist is None:
+            dst.copy_(src)
+        elif backend == "nccl":
+            dist.all_gather_into_tensor(dst, src)
+        else:
+            parts = [torch.empty_like(src.cpu()) for _ in range(G)]
+            dist.all_gather(parts, src.cpu())
+            dst.copy_(torch.cat(parts))
+
+    def one(t):
+        s.shard_begin(t, led)
+        coll_sum(led)
+        s.shard_offer(led, off)
+        coll_gather(allo, off)
+        return s.shard_commit(allo, G, rank)
+
+    t = 65536
+    for _ in range(args.warmup):
+        one(t); t += 1
+    torch.cuda.synchronize()
+    ms = []
+    for _ in range(args.steps):
+        flush.zero_()
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream); one(t); b.record(stream); t += 1
+        torch.cuda.synchronize()
+        ms.append(a.elapsed_time(b))
+    mt = torch.tensor([float(np.median(ms))], dtype=torch.float64, device=f"cuda:{dev}")
+    if dist is not None:
+        if backend == "nccl":
+            dist.all_reduce(mt, op=dist.ReduceOp.MAX)
+        else:
+            h = mt.cpu(); dist.all_reduce(h, op=dist.ReduceOp.MAX); mt.copy_(h)
+    s.close()
+    m_ = float(mt[0])
+    return {"workload": f"cfg4: one queue of {n_total} requests split over {G} GPU(s) ({MA} slots each); "
+                        "per step: shard_begin, all-reduce of the ledgers, shard_offer, all-gather of the "
+                        "offers, shard_commit (global order prefix, admission, R20 over the gathered holders)",
+            "value": n_total / (m_ / 1e3), "unit": UNIT, "ms_per_step_cold_l2": m_, "offer_bytes_per_rank": ob}
+
+
 def hbm_peak():
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -554,8 +632,13 @@ def run_gpu(args):
                                     "achieved_gbs": r_sw["roofline"]["achieved"],
                                     "phys_frac": r_sw["roofline"].get("phys_frac")}
             line[key]["size_sweep"] = sweep
-        _REC_CACHE.clear()
         line["step_multi"] = step_multi_bench(args, dev, stream, peak)
+    if not args.no_step:
+        # f4: the single huge queue sharded over the ranks (every rank takes part)
+        line_sh = sharded_step_bench(args, dev, stream, world, rank, dist, backend)
+        if rank == 0:
+            line["step_sharded"] = line_sh
+        _REC_CACHE.clear()
     if rank == 0 and world == 1 and not args.no_cpu:
         line["cpu_baseline"] = oracle_window_rate(tr, ip, tid, W * args.warmup, W * (args.warmup + args.steps),
                                                   args.cpu_sample or 128, os.cpu_count() or 1)

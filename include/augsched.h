@@ -294,6 +294,46 @@ AUGSCHED_API int augsched_step_prefix(augsched_t* h, uint64_t now_iter, augsched
  * E_INVALID or E_CUDA (a latched device fault is left for augsched_sync). */
 AUGSCHED_API int augsched_step_export(augsched_t* h, uint32_t instance, int32_t* slots, int64_t* ledger);
 
+/* ---- sharded single queue --------------------------------
+ * One global queue whose slots are split over G ranks (one GPU each): rank
+ * r's handle is a single-instance handle (all ranks: the same config,
+ * parameters and max_active) holding global slots
+ * [r * max_active, (r + 1) * max_active).  Every queued request has demand
+ * >= 1, so the global admission prefix (Algorithm 1's fill loop)
+ * lies within the union of every shard's first min(B, n_r) order entries;
+ * the shards exchange only those (and, for the rare R20 resolution, their
+ * KV holders) once per step.  A step is three calls around two collectives
+ * the caller runs over its process group (rank-major, e.g. NCCL):
+ *   1. augsched_shard_begin(h, now, ledger): this step's CALL / FINISH
+ *      records, their C_other (Eq.5, R13) taken from the GLOBAL ledger the
+ *      last commit left; ledger = device int64[2] <- this shard's (A, P)
+ *      after them.
+ *        -> all-reduce(SUM) of ledger over the ranks: ledger_sum[0] is the
+ *           global S1 snapshot A_snap
+ *   2. augsched_shard_offer(h, ledger_sum, offer): RETURN / NEW / IMPORT
+ *      records against A_snap (Stage I/II policy predictions, R7/R12);
+ *      this shard's order (as augsched_step) and its offer: a device buffer
+ *      of augsched_shard_offer_bytes(h) bytes (header with the shard's
+ *      ledger, its first min(n_r, cap >= every limit) order entries
+ *      {packed word tier:2 | key:32 | local slot:30, demand, kv}, its
+ *      queued slots holding KV, its Preserve-paused slots).
+ *        -> all-gather of the offers (rank-major, G * offer bytes)
+ *   3. augsched_shard_commit(h, offers, G, rank, out): the limit B from
+ *      the global ledger (Eq.27-32), the merge of the offers, the global
+ *      admission prefix (R17), memory pressure resolved over the gathered
+ *      holders (R20), this shard's part applied (grants, last = now,
+ *      evictions, demotions) and the global ledger for the next step.  out: the global prefix
+ *      (order = global slot ids, grant, key) of length admitted[0], B in
+ *      budget[0], the global queue size in n_active[0] (device pointers
+ *      valid until the next call).  E_CAPACITY (latched, returned by
+ *      augsched_sync) if a shard had more KV holders than its offer holds and
+ *      the step needed them.  Asynchronous. */
+AUGSCHED_API uint64_t augsched_shard_offer_bytes(const augsched_t* h);
+AUGSCHED_API int augsched_shard_begin(augsched_t* h, uint64_t now_iter, int64_t* ledger);
+AUGSCHED_API int augsched_shard_offer(augsched_t* h, const int64_t* ledger_sum, void* offer);
+AUGSCHED_API int augsched_shard_commit(augsched_t* h, const void* offers, uint32_t n_ranks, uint32_t rank,
+                                       augsched_step_out* out);
+
 /* Run every instance's simulation (Algorithm 1 + engine model + metrics) until
  * all its requests finished or its iteration counter reaches max_iters.
  * inst_trace_id[i] selects instance i's trace.  results: n_instances records.

@@ -30,7 +30,8 @@ NBIN = 160
 RESULT_DTYPE = np.dtype([("f", np.uint64, (len(RESULT_FIELDS),)), ("hist_ttft", np.uint32, (NBIN,)),
                          ("hist_norm", np.uint32, (NBIN,))])
 EXPORTS = ["augsched_create", "augsched_enqueue", "augsched_step", "augsched_step_prefix", "augsched_simulate",
-           "augsched_generate", "augsched_step_export",
+           "augsched_generate", "augsched_step_export", "augsched_shard_offer_bytes", "augsched_shard_begin",
+           "augsched_shard_offer", "augsched_shard_commit",
            "augsched_sync", "augsched_launch_count", "augsched_destroy", "augsched_last_error"]
 
 
@@ -102,6 +103,14 @@ def lib():
         L.augsched_sync.argtypes = [vp]
         L.augsched_step_export.argtypes = [vp, u32, vp, vp]
         L.augsched_step_export.restype = C.c_int
+        L.augsched_shard_offer_bytes.argtypes = [vp]
+        L.augsched_shard_offer_bytes.restype = u64
+        L.augsched_shard_begin.argtypes = [vp, u64, vp]
+        L.augsched_shard_begin.restype = C.c_int
+        L.augsched_shard_offer.argtypes = [vp, vp, vp]
+        L.augsched_shard_offer.restype = C.c_int
+        L.augsched_shard_commit.argtypes = [vp, vp, u32, u32, C.POINTER(StepOut)]
+        L.augsched_shard_commit.restype = C.c_int
         L.augsched_launch_count.argtypes = [vp]
         L.augsched_launch_count.restype = u64
         L.augsched_destroy.argtypes = [vp]
@@ -363,6 +372,36 @@ class Scheduler:
         ap = np.zeros(2, np.int64)
         _check(self.L.augsched_step_export(self.h, instance, None, C.c_void_p(ap.ctypes.data)))
         return int(ap[0]), int(ap[1])
+
+    # ---- sharded single queue (f4): the three calls of one step; the caller
+    # runs the collectives (all-reduce of the ledger, all-gather of the offers)
+    def shard_offer_bytes(self) -> int:
+        return int(self.L.augsched_shard_offer_bytes(self.h))
+
+    def shard_begin(self, now: int, ledger):
+        """ledger: device int64 tensor [2] <- this shard's (A, P)."""
+        _check(self.L.augsched_shard_begin(self.h, int(now), C.c_void_p(ledger.data_ptr())))
+
+    def shard_offer(self, ledger_sum, offer):
+        """ledger_sum: device int64 [2] (the all-reduced ledger); offer: device
+        uint8 [shard_offer_bytes()] <- this shard's offer."""
+        _check(self.L.augsched_shard_offer(self.h, C.c_void_p(ledger_sum.data_ptr()), C.c_void_p(offer.data_ptr())))
+
+    def shard_commit(self, offers, n_ranks: int, rank: int) -> StepOut:
+        """offers: device uint8, the rank-major all-gather of every shard's offer."""
+        out = StepOut()
+        _check(self.L.augsched_shard_commit(self.h, C.c_void_p(offers.data_ptr()), n_ranks, rank, C.byref(out)))
+        return out
+
+    def shard_result(self, out: StepOut) -> dict:
+        """The global prefix of a committed step (synchronizes)."""
+        self.sync()
+        g = lambda ptr, cnt, dt: device_view(ptr, cnt, dt).cpu().numpy().copy()
+        adm = int(g(out.admitted, 1, "<u4")[0])
+        return dict(B=int(g(out.budget, 1, "<i8")[0]), n_active=int(g(out.n_active, 1, "<u4")[0]), admitted=adm,
+                    order=g(out.order, adm, "<u4") if adm else np.zeros(0, np.uint32),
+                    grant=g(out.grant, adm, "<u4") if adm else np.zeros(0, np.uint32),
+                    keys=g(out.key, adm, "<u4") if adm else np.zeros(0, np.uint32))
 
     def step_result(self, out: StepOut) -> dict:
         """Copy one step's outputs to host numpy (synchronizes)."""

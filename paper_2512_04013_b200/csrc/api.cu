@@ -467,6 +467,37 @@ int augsched_step_export(augsched_t* h, uint32_t instance, int32_t* slots, int64
   return AUGSCHED_OK;   // a latched device fault is left for augsched_sync
 }
 
+uint64_t augsched_shard_offer_bytes(const augsched_t* h) {
+  return h ? (uint64_t)step_shard_offer_bytes(h->st) : 0ull;
+}
+
+int augsched_shard_begin(augsched_t* h, uint64_t now_iter, int64_t* ledger) {
+  if (!h || !ledger) return fail(AUGSCHED_E_INVALID, "shard_begin: NULL argument");
+  CUDA_TRY(cudaSetDevice(h->device));
+  int rc = step_ensure(h->st, h->n_inst, h->max_active, h->stream, h->cfg, h->d_ip, &h->launches);
+  if (rc) return rc;
+  if ((rc = check_now(h, now_iter, "shard_begin"))) return rc;
+  h->st.shard_ledger = nullptr;
+  return step_shard_begin(h->st, h->d_ip, h->d_err, now_iter, ledger, h->stream, &h->launches);
+}
+
+int augsched_shard_offer(augsched_t* h, const int64_t* ledger_sum, void* offer) {
+  if (!h || !ledger_sum || !offer) return fail(AUGSCHED_E_INVALID, "shard_offer: NULL argument");
+  CUDA_TRY(cudaSetDevice(h->device));
+  return step_shard_offer(h->st, h->cfg, h->cap, h->d_ip, h->d_err, ledger_sum, offer, h->stream, &h->launches);
+}
+
+int augsched_shard_commit(augsched_t* h, const void* offers, uint32_t n_ranks, uint32_t rank,
+                          augsched_step_out* out) {
+  if (!h || !offers || !out) return fail(AUGSCHED_E_INVALID, "shard_commit: NULL argument");
+  if (!h->st.shard_ledger) return fail(AUGSCHED_E_INVALID, "shard_commit: no shard_offer in this step");
+  CUDA_TRY(cudaSetDevice(h->device));
+  const int rc = step_shard_commit(h->st, h->cfg, h->cap, h->d_ip, h->d_err, h->st.shard_ledger, offers, n_ranks,
+                                   rank, out, h->stream, &h->launches);
+  h->st.shard_ledger = nullptr;
+  return rc;
+}
+
 }  // extern "C"
 
 // error helper shared with step.cu

@@ -1857,7 +1857,49 @@ struct CoopArgs {
   uint32_t* ti_n_out;
   uint32_t* ti_misc;
   uint32_t* gcnt;                    // [TI_DCAP + 1] unchanged words per D rank (kept zero between steps)
+  // sharded single queue (f4): the limit from the global ledger and, instead
+  // of the admission, this shard's offer
+  const long long* ledger;           // [2] global (A, P) or null
+  unsigned char* offer;              // ShardOffer buffer or null
+  uint32_t ocap;
 };
+
+// Offer of one shard (augsched_shard_offer): header, the first min(B, n)
+// entries of its order, its queued slots holding KV, its Preserve-paused
+// slots (local slot ids; the commit adds the rank's base).
+struct ShardHdr { uint32_t n_offer, n_local, n_hq, n_hp, overflow, pad[3]; long long A, P; };
+struct OfferRec { unsigned long long w; uint32_t dem, kv; };
+constexpr uint32_t SH_HCAP = 8192;   // holders of each kind per shard
+__host__ __device__ __forceinline__ size_t shard_offer_bytes(uint32_t ocap) {
+  return sizeof(ShardHdr) + sizeof(OfferRec) * ((size_t)ocap + 2 * SH_HCAP);
+}
+__device__ __forceinline__ ShardHdr* sh_hdr(unsigned char* b) { return reinterpret_cast<ShardHdr*>(b); }
+__device__ __forceinline__ OfferRec* sh_off(unsigned char* b) { return reinterpret_cast<OfferRec*>(b + sizeof(ShardHdr)); }
+__device__ __forceinline__ OfferRec* sh_hq(unsigned char* b, uint32_t ocap) { return sh_off(b) + ocap; }
+__device__ __forceinline__ OfferRec* sh_hp(unsigned char* b, uint32_t ocap) { return sh_off(b) + ocap + SH_HCAP; }
+
+// Offer mode, CTA 0 after the order is complete: the first min(n, ocap)
+// words with their demand and KV (ocap >= every limit, so this holds the
+// shard's first min(B, n) entries for the global B the commit computes),
+// and the shard's ledger after its records.
+__device__ void pack_offer(const CoopArgs& a, const unsigned long long* words, uint32_t n, long long B) {
+  (void)B;
+  const Slots& S = a.S;
+  const uint32_t m = n < a.ocap ? n : a.ocap;
+  OfferRec* o = sh_off(a.offer);
+  for (uint32_t j = threadIdx.x; j < m; j += blockDim.x) {
+    const unsigned long long w = __ldcg(&words[j]);
+    const uint32_t x = (uint32_t)w & SLOT_MASK;
+    o[j] = OfferRec{w, demand_of(S.ctx[x], S.kv[x], S.cpu[x], S.pend[x], a.cfg.s_in), (uint32_t)S.kv[x]};
+  }
+  if (threadIdx.x == 0) {
+    ShardHdr* h = sh_hdr(a.offer);
+    h->n_offer = m;
+    h->n_local = n;
+    h->A = ld_ll(&S.A[0]);
+    h->P = ld_ll(&S.P[0]);
+  }
+}
 
 #ifdef AUGSCHED_COOP_TIMING
 __device__ unsigned long long g_coop_arr[16];   // latest arrival per barrier (ns)
@@ -1993,7 +2035,8 @@ __device__ void ti_incremental(const CoopArgs& a, unsigned long long* sbuf, unsi
   }
   if (c == 0) {
     if (tid == 0) {
-      B_s = token_limit(a.cfg, k, ip, a.cap, ld_ll(&S.A[0]), ld_ll(&S.P[0]));
+      B_s = a.ledger ? token_limit(a.cfg, k, ip, a.cap, ld_ll(&a.ledger[0]), ld_ll(&a.ledger[1]))
+                     : token_limit(a.cfg, k, ip, a.cap, ld_ll(&S.A[0]), ld_ll(&S.P[0]));
       a.budget[0] = B_s;
     }
     const uint32_t dc = __ldcg(&S.dcnt[E & 1]);
@@ -2225,6 +2268,7 @@ __device__ void ti_incremental(const CoopArgs& a, unsigned long long* sbuf, unsi
   // ---- F: admission over the first min(B, n) positions (CTA 0)
   const uint32_t n = __ldcg(&a.n_active[0]);
   const long long B = B_s;
+  if (a.offer) { pack_offer(a, a.tiw_out, n, B); return; }
   const uint32_t target = pf_target(B, n);
   for (uint32_t i = tid; i < target; i += CNT) sbuf[i] = __ldcg(&a.tiw_out[i]);
   const uint32_t prev = S.gdirty[0];
@@ -2302,7 +2346,8 @@ __global__ void __launch_bounds__(CNT, 1) full_coop_kernel(const __grid_constant
       }
     }
     if (c == 0 && tid == 0) {
-      B_s = token_limit(a.cfg, k, ip, a.cap, ld_ll(&S.A[0]), ld_ll(&S.P[0]));
+      B_s = a.ledger ? token_limit(a.cfg, k, ip, a.cap, ld_ll(&a.ledger[0]), ld_ll(&a.ledger[1]))
+                     : token_limit(a.cfg, k, ip, a.cap, ld_ll(&S.A[0]), ld_ll(&S.P[0]));
       a.budget[0] = B_s;
     }
   }
@@ -2462,6 +2507,7 @@ __global__ void __launch_bounds__(CNT, 1) full_coop_kernel(const __grid_constant
   // ---- F: admission over the first min(B, n) positions
   const uint32_t n = __ldcg(&a.n_active[0]);
   const long long B = B_s;
+  if (a.offer) { pack_offer(a, a.kpre, n, B); return; }
   const uint32_t target = pf_target(B, n);
   for (uint32_t i = tid; i < target; i += CNT) sbuf[i] = __ldcg(&a.kpre[i]);
   const uint32_t prev = S.gdirty[0];
@@ -2482,6 +2528,334 @@ __global__ void __launch_bounds__(CNT, 1) full_coop_kernel(const __grid_constant
     printf("\n");
   }
 #endif
+}
+
+// ====================================================================== sharded single queue (f4)
+// This shard's KV holders for the global R20 resolution: queued slots with
+// kv > 0 (their packed word) and Preserve-paused slots with kv > 0 (their
+// demotion key (2^32-1-kv) << 30 | slot: kv desc, slot asc).
+__global__ void shard_holders_kernel(Slots S, uint64_t now, uint32_t N, unsigned char* offer, uint32_t ocap) {
+  const uint32_t x = blockIdx.x * blockDim.x + threadIdx.x;
+  if (x >= N) return;
+  const uint32_t stv = S.st[x], s4 = stv & 15;
+  const int32_t kv = S.kv[x];
+  if (kv <= 0) return;
+  ShardHdr* h = sh_hdr(offer);
+  if (s4 >= ST_RUN && s4 <= ST_WAIT) {
+    const unsigned long long w = slot_word(S.coef[0], S.ip[0], stv, S.V[x], S.last[x], now, x);
+    const uint32_t q = atomicAdd(&h->n_hq, 1u);
+    if (q < SH_HCAP) sh_hq(offer, ocap)[q] = OfferRec{w, 0u, (uint32_t)kv};
+    else atomicOr(&h->overflow, 2u);
+  } else if (s4 == ST_PAUSED && ((stv >> 4) & 3) == POL_P) {
+    const uint32_t q = atomicAdd(&h->n_hp, 1u);
+    const unsigned long long key = ((unsigned long long)(0xFFFFFFFFu - (uint32_t)kv) << 30) | x;
+    if (q < SH_HCAP) sh_hp(offer, ocap)[q] = OfferRec{key, 0u, (uint32_t)kv};
+    else atomicOr(&h->overflow, 4u);
+  }
+}
+
+struct CommitArgs {
+  Slots S;
+  augsched_config cfg;
+  int64_t cap;
+  uint64_t now;
+  const unsigned char* offers;   // n_ranks blocks of shard_offer_bytes(ocap)
+  size_t obytes;
+  uint32_t ocap, n_ranks, rank, MA;
+  long long* gledger;            // [2] global (A, P) after this step (the next step's C_other base)
+  long long* budget;
+  uint32_t *n_active, *admitted, *order, *keyout, *grant, *err;
+};
+
+__device__ __forceinline__ const unsigned char* cm_blk(const CommitArgs& a, uint32_t r) { return a.offers + (size_t)r * a.obytes; }
+// global packed word of record j of rank r's list
+__device__ __forceinline__ unsigned long long cm_gword(const CommitArgs& a, uint32_t r, unsigned long long w) {
+  return (w & ~(unsigned long long)SLOT_MASK) | ((unsigned long long)r * a.MA + ((uint32_t)w & SLOT_MASK));
+}
+// the offer record of global word gw (it is in its rank's sorted offer list)
+__device__ const OfferRec* cm_find(const CommitArgs& a, unsigned long long gw) {
+  const uint32_t gs = (uint32_t)gw & SLOT_MASK, r = gs / a.MA;
+  const unsigned char* b = cm_blk(a, r);
+  const uint32_t n = reinterpret_cast<const ShardHdr*>(b)->n_offer;
+  const OfferRec* o = reinterpret_cast<const OfferRec*>(b + sizeof(ShardHdr));
+  const unsigned long long lw = (gw & ~(unsigned long long)SLOT_MASK) | (gs - r * a.MA);
+  uint32_t lo = 0, hi = n;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (o[mid].w < lw) lo = mid + 1; else hi = mid;
+  }
+  return &o[lo];
+}
+
+// One CTA: merge the offers (the target smallest global words by a count
+// select, then a bitonic sort), admit the global prefix (R17), resolve
+// memory pressure over the gathered holders (R20: demote Preserve-paused by
+// kv desc / slot asc, then evict from the tail of the global order over
+// entries with kv + g > 0), write the global prefix and apply this shard's
+// part.
+__global__ void __launch_bounds__(1024, 1) shard_commit_kernel(const __grid_constant__ CommitArgs a) {
+  constexpr int NT = 1024;
+  extern __shared__ __align__(16) unsigned long long cm_sm[];
+  unsigned long long* sbuf = cm_sm;            // [PF_SCAP] the admitted candidates, sorted
+  unsigned long long* xch = cm_sm + PF_SCAP;   // [PF_SCAP] sort exchange, then the grants (u32)
+  __shared__ SelShm sel;
+  __shared__ unsigned long long wsum[NT / 32 + 1];
+  __shared__ unsigned long long freed_s;
+  __shared__ uint32_t m_s, tot_off_s, n_tot_s, ovf_s;
+  __shared__ long long B_s;
+  const int tid = threadIdx.x;
+  const Slots& S = a.S;
+  const uint32_t G = a.n_ranks, OC = a.ocap;
+  __shared__ long long gA_s, gP_s;
+  if (tid == 0) {
+    const Coef k = S.coef[0];
+    uint32_t to = 0, nt = 0, ov = 0;
+    long long A = 0, P = 0;
+    for (uint32_t r = 0; r < G; ++r) {
+      const ShardHdr* h = reinterpret_cast<const ShardHdr*>(cm_blk(a, r));
+      to += h->n_offer; nt += h->n_local; ov |= h->overflow; A += h->A; P += h->P;
+    }
+    gA_s = A; gP_s = P;
+    B_s = token_limit(a.cfg, k, S.ip[0], a.cap, A, P);   // Eq.27-32 on the global ledger
+    tot_off_s = to; n_tot_s = nt; ovf_s = ov; m_s = 0;
+    a.budget[0] = B_s;
+    a.n_active[0] = nt;
+  }
+  __syncthreads();
+  const long long B = B_s;
+  const uint32_t target = pf_target(B, tot_off_s);
+  auto off_get = [&](uint32_t i, uint64_t& key, uint32_t& w) -> bool {
+    const uint32_t r = i / OC, j = i - r * OC;
+    const unsigned char* b = cm_blk(a, r);
+    if (j >= reinterpret_cast<const ShardHdr*>(b)->n_offer) return false;
+    key = cm_gword(a, r, reinterpret_cast<const OfferRec*>(b + sizeof(ShardHdr))[j].w);
+    w = 1u;
+    return true;
+  };
+  if (target > 0) {
+    wselect<NT>(sel, G * OC, target, 64, off_get);
+    const unsigned long long tau = sel.r.found ? sel.r.k : ~0ull;
+    for (uint32_t i = tid; i < G * OC; i += NT) {
+      uint64_t key; uint32_t w;
+      if (off_get(i, key, w) && key <= tau) sbuf[atomicAdd(&m_s, 1u)] = key;
+    }
+    __syncthreads();
+    const uint32_t mt = m_s;
+    uint32_t P2 = 32;
+    while (P2 < mt) P2 <<= 1;
+    if (P2 <= 1024u) {
+      if ((uint32_t)tid < P2) {
+        unsigned long long v = (uint32_t)tid < mt ? sbuf[tid] : ~0ull;
+        bar_named(P2);
+        switch (P2) {
+          case 32: v = bitonic1<5>(v, sbuf, xch); break;
+          case 64: v = bitonic1<6>(v, sbuf, xch); break;
+          case 128: v = bitonic1<7>(v, sbuf, xch); break;
+          case 256: v = bitonic1<8>(v, sbuf, xch); break;
+          case 512: v = bitonic1<9>(v, sbuf, xch); break;
+          default: v = bitonic1<10>(v, sbuf, xch); break;
+        }
+        bar_named(P2);
+        sbuf[tid] = v;
+      }
+    } else if (P2 == 2048) pf_sortE<NT, 11>(sbuf, xch, mt);
+    else if (P2 == 4096) pf_sortE<NT, 12>(sbuf, xch, mt);
+    else pf_sortE<NT, 13>(sbuf, xch, mt);
+    __syncthreads();
+  }
+  uint32_t* gs = reinterpret_cast<uint32_t*>(xch);   // grant of prefix position j
+  // ---- a6 admission over the global prefix (P_{j-1} < B, partial last, R17)
+  unsigned long long Prun = 0, gsum = 0;
+  uint32_t adm = 0;
+  for (uint32_t j0 = 0; j0 < target && (long long)Prun < B; j0 += NT) {
+    const uint32_t j = j0 + tid;
+    unsigned long long d = 0;
+    if (j < target) d = cm_find(a, sbuf[j])->dem;
+    unsigned long long tot;
+    const unsigned long long inc = block_incl_scan_u64<NT>(d, wsum, &tot);
+    const unsigned long long ex = Prun + inc - d;
+    const bool in = j < target && (long long)ex < B;
+    if (j < target) gs[j] = 0;
+    if (in) {
+      const unsigned long long g = d < (unsigned long long)B - ex ? d : (unsigned long long)B - ex;
+      gs[j] = (uint32_t)g;
+      gsum += g;
+    }
+    adm += __syncthreads_count(in);
+    Prun += tot;
+  }
+  unsigned long long need;
+  block_incl_scan_u64<NT>(gsum, wsum, &need);
+  long long fr = a.cap - gA_s - gP_s;
+  // ---- a7 resolution over the gathered holders (rare)
+  bool demote = false, evict = false;
+  unsigned long long k0 = 0, k1 = 0;
+  bool f0 = false, f1 = false;
+  auto hp_get = [&](uint32_t i, uint64_t& key, uint32_t& w) -> bool {
+    const uint32_t r = i / SH_HCAP, j = i - r * SH_HCAP;
+    const unsigned char* b = cm_blk(a, r);
+    const uint32_t n = reinterpret_cast<const ShardHdr*>(b)->n_hp;
+    if (j >= (n < SH_HCAP ? n : SH_HCAP)) return false;
+    const OfferRec rec = reinterpret_cast<const OfferRec*>(b + sizeof(ShardHdr))[OC + SH_HCAP + j];
+    key = (rec.w & ~(unsigned long long)SLOT_MASK) | ((unsigned long long)r * a.MA + ((uint32_t)rec.w & SLOT_MASK));
+    w = rec.kv;
+    return true;
+  };
+  // eviction candidates: holders_q (kv + their grant if admitted) and the
+  // admitted entries that hold no KV (their grant); key = ~word (tail first)
+  auto adm_pos = [&](unsigned long long gw) -> int {
+    uint32_t lo = 0, hi = adm;
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (sbuf[mid] < gw) lo = mid + 1; else hi = mid;
+    }
+    return lo < adm && sbuf[lo] == gw ? (int)lo : -1;
+  };
+  auto ev_get = [&](uint32_t i, uint64_t& key, uint32_t& w) -> bool {
+    if (i < G * SH_HCAP) {
+      const uint32_t r = i / SH_HCAP, j = i - r * SH_HCAP;
+      const unsigned char* b = cm_blk(a, r);
+      const uint32_t n = reinterpret_cast<const ShardHdr*>(b)->n_hq;
+      if (j >= (n < SH_HCAP ? n : SH_HCAP)) return false;
+      const OfferRec rec = reinterpret_cast<const OfferRec*>(b + sizeof(ShardHdr))[OC + j];
+      const unsigned long long gw = cm_gword(a, r, rec.w);
+      const int p = adm_pos(gw);
+      w = rec.kv + (p >= 0 ? gs[p] : 0u);
+      key = ~gw;
+      return w > 0;
+    }
+    const uint32_t j = i - G * SH_HCAP;
+    if (j >= adm || gs[j] == 0) return false;
+    if (cm_find(a, sbuf[j])->kv > 0) return false;   // listed with the holders
+    key = ~sbuf[j];
+    w = gs[j];
+    return true;
+  };
+  if ((long long)need > fr) {
+    if (ovf_s & 6u) { if (tid == 0) atomicOr(a.err, 2u); }   // a shard's holder list overflowed
+    demote = true;
+    wselect<NT>(sel, G * SH_HCAP, (uint64_t)((long long)need - fr), 62, hp_get);
+    f0 = sel.r.found != 0;
+    k0 = sel.r.k;
+    if (tid == 0) freed_s = 0;
+    __syncthreads();
+    for (uint32_t i = tid; i < G * SH_HCAP; i += NT) {
+      uint64_t key; uint32_t w;
+      if (hp_get(i, key, w) && (!f0 || key <= k0)) atomicAdd(&freed_s, (unsigned long long)w);
+    }
+    __syncthreads();
+    fr += (long long)freed_s;
+    if (tid == 0) gP_s -= (long long)freed_s;   // demoted KV leaves P
+    if ((long long)need > fr) {
+      evict = true;
+      wselect<NT>(sel, G * SH_HCAP + adm, (uint64_t)((long long)need - fr), 64, ev_get);
+      f1 = sel.r.found != 0;
+      k1 = sel.r.k;
+      __syncthreads();
+      // admitted entries that are evicted (their candidate key passes; kv + g > 0
+      // holds for them): grant cancelled, marked until this shard applied it
+      for (uint32_t j = tid; j < adm; j += NT)
+        if (gs[j] > 0 && (!f1 || ~sbuf[j] <= k1)) gs[j] = 0xFFFFFFFFu;
+      // KV released by the evicted holders of every shard leaves A
+      if (tid == 0) freed_s = 0;
+      __syncthreads();
+      for (uint32_t i = tid; i < G * SH_HCAP; i += NT) {
+        const uint32_t r = i / SH_HCAP, j = i - r * SH_HCAP;
+        const unsigned char* b = cm_blk(a, r);
+        const uint32_t n = reinterpret_cast<const ShardHdr*>(b)->n_hq;
+        if (j >= (n < SH_HCAP ? n : SH_HCAP)) continue;
+        const OfferRec rec = reinterpret_cast<const OfferRec*>(b + sizeof(ShardHdr))[OC + j];
+        if (!f1 || ~cm_gword(a, r, rec.w) <= k1) atomicAdd(&freed_s, (unsigned long long)rec.kv);
+      }
+      __syncthreads();
+      if (tid == 0) gA_s -= (long long)freed_s;
+    }
+  }
+  __syncthreads();
+  // ---- outputs (every rank the same) and this shard's part
+  const uint32_t base = a.rank * a.MA;
+  long long dA = 0, dP = 0;
+  for (uint32_t j = tid; j < adm; j += NT) {
+    const unsigned long long gw = sbuf[j];
+    const uint32_t g = gs[j];
+    a.order[j] = (uint32_t)gw & SLOT_MASK;
+    a.keyout[j] = (uint32_t)(gw >> PK_KEY);
+    a.grant[j] = g == 0xFFFFFFFFu ? 0u : g;
+    const uint32_t gsl = (uint32_t)gw & SLOT_MASK;
+    if (g == 0xFFFFFFFFu && gsl >= base && gsl < base + a.MA) {
+      // this shard's evicted admitted entry: whole context recomputed (B2);
+      // its KV (if any) is released by the holder loop below
+      const uint32_t x = gsl - base;
+      S.cpu[x] = 0;
+      S.st[x] = ST_WAIT | (S.st[x] & 0x30u);
+      mark_dirty(S, x, S.ti_ep + 1);
+    }
+  }
+  if (evict) {   // this shard's evicted holders (queued, kv > 0) and admitted KV-free entries
+    const unsigned char* b = cm_blk(a, a.rank);
+    const uint32_t nq = reinterpret_cast<const ShardHdr*>(b)->n_hq;
+    const OfferRec* hq = reinterpret_cast<const OfferRec*>(b + sizeof(ShardHdr)) + OC;
+    for (uint32_t j = tid; j < (nq < SH_HCAP ? nq : SH_HCAP); j += NT) {
+      const unsigned long long gw = cm_gword(a, a.rank, hq[j].w);
+      if (!f1 || ~gw <= k1) {
+        const uint32_t x = (uint32_t)hq[j].w & SLOT_MASK;
+        dA -= S.kv[x];
+        S.kv[x] = 0; S.cpu[x] = 0;
+        S.st[x] = ST_WAIT | (S.st[x] & 0x30u);
+        mark_dirty(S, x, S.ti_ep + 1);
+      }
+    }
+  }
+  if (demote) {
+    const unsigned char* b = cm_blk(a, a.rank);
+    const uint32_t np = reinterpret_cast<const ShardHdr*>(b)->n_hp;
+    const OfferRec* hp = reinterpret_cast<const OfferRec*>(b + sizeof(ShardHdr)) + OC + SH_HCAP;
+    for (uint32_t j = tid; j < (np < SH_HCAP ? np : SH_HCAP); j += NT) {
+      const uint32_t x = (uint32_t)hp[j].w & SLOT_MASK;
+      const unsigned long long key = (hp[j].w & ~(unsigned long long)SLOT_MASK) | (base + x);
+      if (!f0 || key <= k0) {
+        dP -= S.kv[x];
+        S.kv[x] = 0;
+        S.st[x] = ST_PAUSED | ((uint32_t)POL_D << 4);
+      }
+    }
+  }
+  __syncthreads();
+  for (uint32_t j = tid; j < adm; j += NT) {
+    const uint32_t gsl = (uint32_t)sbuf[j] & SLOT_MASK;
+    const uint32_t gr = gs[j];
+    if (gsl < base || gsl >= base + a.MA || gr == 0 || gr == 0xFFFFFFFFu) continue;
+    const uint32_t x = gsl - base;
+    int32_t ctx = S.ctx[x], kv = S.kv[x], cpu = S.cpu[x], pend = S.pend[x];
+    if (cpu > 0) { cpu -= (int32_t)gr; kv += (int32_t)gr; }
+    else if ((ctx - kv) + pend > 0) {
+      const int32_t rc = (int32_t)gr < ctx - kv ? (int32_t)gr : ctx - kv;
+      kv += rc;
+      const int32_t pp = (int32_t)gr - rc;
+      pend -= pp; ctx += pp; kv += pp;
+    } else { ctx += 1; kv += 1; }
+    dA += gr;
+    S.ctx[x] = ctx; S.kv[x] = kv; S.cpu[x] = cpu; S.pend[x] = pend;
+    S.last[x] = (uint32_t)a.now;
+    S.st[x] = ST_RUN | (S.st[x] & 0x30u);
+    mark_dirty(S, x, S.ti_ep + 1);
+  }
+  // tokens granted over all shards (every admitted grant that stands)
+  unsigned long long gt = 0;
+  for (uint32_t j = tid; j < adm; j += NT) gt += gs[j] == 0xFFFFFFFFu ? 0u : gs[j];
+  unsigned long long tA, tP, tG;
+  block_incl_scan_u64<NT>((unsigned long long)dA, wsum, &tA);
+  block_incl_scan_u64<NT>((unsigned long long)dP, wsum, &tP);
+  block_incl_scan_u64<NT>(gt, wsum, &tG);
+  if (tid == 0) {
+    a.gledger[0] = gA_s + (long long)tG;
+    a.gledger[1] = gP_s;
+    a.admitted[0] = adm;
+    const long long A = ld_ll(&S.A[0]) + (long long)tA;
+    S.A[0] = A;
+    S.Aevt[0] = A;
+    S.P[0] = ld_ll(&S.P[0]) + (long long)tP;
+  }
 }
 }  // namespace
 
@@ -2605,7 +2979,7 @@ int step_ensure(StepState& st, uint32_t n_inst, uint32_t max_active, cudaStream_
       (rc = salloc(st, &st.pf_nact, 2)) || (rc = salloc(st, &st.n_active, n_inst)) ||
       (rc = salloc(st, &st.tier_off, 3 * (size_t)n_inst)) || (rc = salloc(st, &st.claimA, N)) ||
       (rc = salloc(st, &st.claimB, N)) || (rc = salloc(st, &st.gdirty, n_inst)) ||
-      (rc = salloc(st, &st.coop_bar, 1)))
+      (rc = salloc(st, &st.coop_bar, 1)) || (rc = salloc(st, &st.gA, 2)))
     return rc;
   // one memset per full step clears the tier counts, histograms and tile counters
   st.zwords = zwords;
@@ -2633,6 +3007,7 @@ int step_ensure(StepState& st, uint32_t n_inst, uint32_t max_active, cudaStream_
       {st.admitted, 0, sizeof(uint32_t) * n_inst},
       {st.gdirty, 0, sizeof(uint32_t) * n_inst},
       {st.coop_bar, 0, sizeof(unsigned long long)},
+      {st.gA, 0, 2 * sizeof(long long)},
       {st.n_active, 0, sizeof(uint32_t) * n_inst},
       {st.tier_off, 0, 3 * sizeof(uint32_t) * n_inst},
       {st.A, 0, sizeof(long long) * n_inst},
@@ -2801,7 +3176,7 @@ int step_run_prefix(StepState& st, const augsched_config& cfg, int64_t cap,
   }
   if (++st.pf_epoch >= (1u << 30)) st.pf_epoch = 1;
   const uint32_t ep = st.pf_epoch;
-  PfArgs pa;
+  PfArgs pa{};
   pa.S = S; pa.cfg = cfg; pa.cap = cap; pa.now = now; pa.N = (uint32_t)st.N; pa.spec = st.pf_spec ? 1 : 0;
   pa.k0 = st.k0; pa.A = st.pf_A; pa.C = st.pf_C; pa.theta = st.pf_theta; pa.H = st.pf_H; pa.ghist = st.ghist;
   pa.cnt = st.pf_cnt; pa.ep = ep; pa.n_active = st.pf_nact + (ep & 1u); pa.n_active_next = st.pf_nact + ((ep + 1u) & 1u);
@@ -2850,7 +3225,7 @@ int step_run(StepState& st, const augsched_config& cfg, int64_t cap,
   // one instance: one cooperative kernel (keys, four sort passes with grid
   // barriers, admission by CTA 0)
   if (ni == 1 && st.max_limit <= PF_SCAP && st.coop_grid > 0) {
-    CoopArgs ca;
+    CoopArgs ca{};
     ca.S = S; ca.cfg = cfg; ca.cap = cap; ca.now = now; ca.N = (uint32_t)st.N; ca.max_limit = st.max_limit;
     ca.kA = st.k0; ca.kB = st.k1; ca.kpre = st.pf_A; ca.hist = st.coop_hist; ca.bar = st.coop_bar;
     ca.tot = st.coop_hist + 4 * (size_t)st.coop_grid * CNB;
@@ -2912,7 +3287,7 @@ int step_run(StepState& st, const augsched_config& cfg, int64_t cap,
   st.pf_dirty = true;
   int rc = cuda_check(cudaMemsetAsync(st.zbuf, 0, sizeof(uint32_t) * st.zwords, s), "step: clear");
   if (rc) return rc;
-  KeyArgs ka;
+  KeyArgs ka{};
   ka.S = S; ka.cfg = cfg; ka.cap = cap; ka.now = now; ka.k0 = st.k0;
   ka.ghist = st.ghist; ka.tcnt = st.tcnt; ka.budget = st.budget; ka.npass = st.npass;
   for (int p = 0; p < st.npass; ++p) ka.passes[p] = st.passes[p];
@@ -2923,7 +3298,7 @@ int step_run(StepState& st, const augsched_config& cfg, int64_t cap,
   *launches += 1;
   unsigned long long *kin = st.k0, *kout = st.k1;
   for (int p = 0; p < st.npass; ++p) {
-    SortArgs sa;
+    SortArgs sa{};
     sa.kin = kin; sa.kout = kout; sa.n = (uint32_t)st.N; sa.d = st.passes[p];
     sa.MA = st.max_active; sa.ghist = st.ghist + st.passes[p].hoff; sa.status = st.lb_status;
     sa.gstatus = st.lb_gstatus; sa.G = st.G;
@@ -2951,6 +3326,127 @@ int step_run(StepState& st, const augsched_config& cfg, int64_t cap,
   out->key = st.key;
   out->tier_off = st.tier_off;
   return cuda_check(cudaGetLastError(), "step");
+}
+
+// ---- sharded single queue (f4) ----------------------------------------------
+static uint32_t shard_ocap(const StepState& st) {
+  uint32_t c = 32;
+  while (c < st.max_limit) c <<= 1;
+  return c;
+}
+size_t step_shard_offer_bytes(const StepState& st) { return shard_offer_bytes(shard_ocap(st)); }
+
+int step_shard_begin(StepState& st, const augsched_instance_params* d_ip, uint32_t* d_err, uint64_t now,
+                     int64_t* ledger, cudaStream_t s, uint64_t* launches) {
+  if (st.n_inst != 1 || st.coop_grid <= 0 || st.max_limit > PF_SCAP)
+    return set_error(AUGSCHED_E_INVALID, "shard: needs a single-instance handle with limits <= 8192 on a GPU "
+                                         "that runs the cooperative step");
+  ti_begin(st);
+  Slots S = slots_of(st, d_ip, d_err);
+  // CALL / FINISH of the last forward: C_other of the issued calls from the
+  // GLOBAL ledger before the events (R13; every shard holds it after the
+  // last commit); the caller all-reduces this shard's A after them into the
+  // global snapshot A_snap (S1) that the intake of shard_offer uses
+  S.Aevt = st.gA;
+  st.shard_batch = st.r_n ? ++st.rec_batch : 0u;
+  if (st.r_n) {
+    S.batch = st.shard_batch;
+    Rec r{st.r_kind, st.r_id, st.r_la, st.r_lb, st.r_lc, st.r_flags, st.r_last, st.r_ctx, st.r_kv,
+          st.r_cpu, st.r_pend, st.r_ta};
+    rec_phaseA<<<(st.r_n + 255) / 256, 256, 0, s>>>(r, st.r_n, S, d_err);
+    *launches += 1;
+  }
+  st.shard_now = now;
+  int rc;
+  if ((rc = cuda_check(cudaMemcpyAsync(ledger, st.A, sizeof(long long), cudaMemcpyDeviceToDevice, s), "shard")) ||
+      (rc = cuda_check(cudaMemcpyAsync(ledger + 1, st.P, sizeof(long long), cudaMemcpyDeviceToDevice, s), "shard")))
+    return rc;
+  return cuda_check(cudaGetLastError(), "shard_begin");
+}
+
+int step_shard_offer(StepState& st, const augsched_config& cfg, int64_t cap, const augsched_instance_params* d_ip,
+                     uint32_t* d_err, const int64_t* ledger_sum, void* offer, cudaStream_t s, uint64_t* launches) {
+  Slots S = slots_of(st, d_ip, d_err);
+  if (st.r_n) {   // RETURN / NEW / IMPORT against the global snapshot A_snap = ledger_sum[0]
+    S.batch = st.shard_batch;
+    S.Asnap = const_cast<long long*>(reinterpret_cast<const long long*>(ledger_sum));
+    Rec r{st.r_kind, st.r_id, st.r_la, st.r_lb, st.r_lc, st.r_flags, st.r_last, st.r_ctx, st.r_kv,
+          st.r_cpu, st.r_pend, st.r_ta};
+    rec_phaseBC<<<(st.r_n + 255) / 256, 256, 0, s>>>(r, st.r_n, S, st.shard_now, d_err);
+    *launches += 1;
+    st.r_n = 0;
+    S = slots_of(st, d_ip, d_err);
+  }
+  const uint32_t ocap = shard_ocap(st);
+  int rc = cuda_check(cudaMemsetAsync(offer, 0, sizeof(ShardHdr), s), "shard_offer: clear");
+  if (rc) return rc;
+  CoopArgs ca{};
+  ca.S = S; ca.cfg = cfg; ca.cap = cap; ca.now = st.shard_now; ca.N = (uint32_t)st.N; ca.max_limit = st.max_limit;
+  ca.kA = st.k0; ca.kB = st.k1; ca.kpre = st.pf_A; ca.hist = st.coop_hist; ca.bar = st.coop_bar;
+  ca.tot = st.coop_hist + 4 * (size_t)st.coop_grid * CNB;
+  ca.bar_base = st.coop_bar_base;
+  ca.budget = st.budget; ca.n_active = st.n_active; ca.tier_off = st.tier_off; ca.order = st.order;
+  ca.keyout = st.key; ca.grant = st.grant; ca.admitted = st.admitted; ca.gslot = st.gslot;
+  const uint32_t cur = st.ti_ep & 1;
+  ca.ti = st.ti ? 1 : 0;
+  ca.ti_try = st.ti && st.ti_valid ? 1 : 0;
+  ca.tiw_in = st.tiw; ca.tiw_out = st.tiw2; ca.ubuf = st.ubuf;
+  ca.ti_n_in = st.ti_n ? st.ti_n + (cur ^ 1) : nullptr;
+  ca.ti_n_out = st.ti_n ? st.ti_n + cur : nullptr;
+  ca.ti_misc = st.ti_misc;
+  ca.gcnt = st.ti_gcnt;
+  ca.ledger = nullptr;            // the limit is the commit's (global ledger); the offer holds min(n, ocap)
+  st.shard_ledger = ledger_sum;
+  ca.offer = static_cast<unsigned char*>(offer);
+  ca.ocap = ocap;
+  void* args[] = {&ca};
+  cudaError_t e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(&full_coop_kernel), st.coop_grid,
+                                              CNT, args, coop_smem_bytes(), s);
+  if (e != cudaSuccess) return cuda_check(e, "shard_offer: cooperative launch");
+  st.coop_bar_base += 12ull * (unsigned long long)st.coop_grid;
+  shard_holders_kernel<<<(uint32_t)((st.N + 255) / 256), 256, 0, s>>>(S, st.shard_now, (uint32_t)st.N,
+                                                                       static_cast<unsigned char*>(offer), ocap);
+  *launches += 2;
+  if (st.ti) {
+    std::swap(st.tiw, st.tiw2);
+    st.ti_valid = true;
+    if ((rc = ti_end(st, s))) return rc;
+  }
+  return cuda_check(cudaGetLastError(), "shard_offer");
+}
+
+int step_shard_commit(StepState& st, const augsched_config& cfg, int64_t cap, const augsched_instance_params* d_ip,
+                      uint32_t* d_err, const int64_t* ledger_sum, const void* offers, uint32_t n_ranks,
+                      uint32_t rank, augsched_step_out* out, cudaStream_t s, uint64_t* launches) {
+  if (n_ranks == 0 || rank >= n_ranks || (uint64_t)n_ranks * st.max_active >= (1ull << 30))
+    return set_error(AUGSCHED_E_INVALID, "shard_commit: bad rank count / rank, or ranks x max_active >= 2^30");
+  Slots S = slots_of(st, d_ip, d_err);
+  CommitArgs ca{};
+  ca.S = S; ca.cfg = cfg; ca.cap = cap; ca.now = st.shard_now;
+  ca.offers = static_cast<const unsigned char*>(offers);
+  ca.ocap = shard_ocap(st);
+  ca.obytes = shard_offer_bytes(ca.ocap);
+  ca.n_ranks = n_ranks; ca.rank = rank; ca.MA = st.max_active;
+  (void)ledger_sum;
+  ca.gledger = st.gA;
+  ca.budget = st.budget; ca.n_active = st.n_active; ca.admitted = st.admitted; ca.order = st.order;
+  ca.keyout = st.key; ca.grant = st.grant; ca.err = d_err;
+  static bool attr = false;
+  const size_t smem = 2 * sizeof(unsigned long long) * PF_SCAP;
+  if (!attr) {
+    cudaFuncSetAttribute(shard_commit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  shard_commit_kernel<<<1, 1024, smem, s>>>(ca);
+  *launches += 1;
+  out->budget = reinterpret_cast<const int64_t*>(st.budget);
+  out->n_active = st.n_active;
+  out->admitted = st.admitted;
+  out->order = st.order;
+  out->grant = st.grant;
+  out->key = st.key;
+  out->tier_off = nullptr;
+  return cuda_check(cudaGetLastError(), "shard_commit");
 }
 
 void step_free(StepState& st) {

@@ -56,6 +56,10 @@ struct StepState {
   float* r_ta = nullptr;
   uint32_t r_cap = 0, r_n = 0;
   uint64_t last_now = 0;         // last `now` passed to a step (time must not run backwards)
+  uint64_t shard_now = 0;        // sharded queue (f4): the iteration of the step in progress
+  const int64_t* shard_ledger = nullptr;
+  uint32_t shard_batch = 0;      // the record batch split over shard_begin / shard_offer
+  long long* gA = nullptr;       // [2] global (A, P) after the last commit
   bool have_now = false;
   // duplicate-record detection: per slot, the winning record of the batch in
   // each record phase (CALL/FINISH; RETURN/NEW/IMPORT), key
@@ -126,6 +130,14 @@ int step_run_prefix(StepState& st, const augsched_config& cfg, int64_t cap,
 int step_run(StepState& st, const augsched_config& cfg, int64_t cap,
              const augsched_instance_params* d_ip, uint32_t* d_err, uint64_t now,
              augsched_step_out* out, cudaStream_t s, uint64_t* launches);
+size_t step_shard_offer_bytes(const StepState& st);
+int step_shard_begin(StepState& st, const augsched_instance_params* d_ip, uint32_t* d_err, uint64_t now,
+                     int64_t* ledger, cudaStream_t s, uint64_t* launches);
+int step_shard_offer(StepState& st, const augsched_config& cfg, int64_t cap, const augsched_instance_params* d_ip,
+                     uint32_t* d_err, const int64_t* ledger_sum, void* offer, cudaStream_t s, uint64_t* launches);
+int step_shard_commit(StepState& st, const augsched_config& cfg, int64_t cap, const augsched_instance_params* d_ip,
+                      uint32_t* d_err, const int64_t* ledger_sum, const void* offers, uint32_t n_ranks,
+                      uint32_t rank, augsched_step_out* out, cudaStream_t s, uint64_t* launches);
 void step_free(StepState& st);
 int set_error(int code, const char* msg);
 
