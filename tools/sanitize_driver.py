@@ -56,4 +56,52 @@ for n_inst, MA, prefix in cases:
                 prefix=prefix)
     sc.sync()
     sc.close()
+# time-invariant keys: incremental full order over several steps
+rng = np.random.default_rng(5)
+cfg = dict(tracegen.PRESET_G0, g_total=1000 + 500, g_model=1000)
+ipt = tracegen.inst_params(1, base=tracegen.INST_G0, ranking=3, budget_mode=0, target_max=100, alpha=1.5)
+st = oracle.Step(cfg, ipt, 600)
+sc = aug.Scheduler(cfg, ipt, 1, 600)
+for t in range(6):
+    rec = random_events(rng, st.slots(0), t, p_new=0.6 if t == 0 else 0.1)
+    if rec is not None:
+        st.enqueue(0, rec)
+        sc.enqueue(0, rec)
+    compare(sc.step_result(sc.step(t)), st.step(t), 1, "sanitize ti")
+sc.sync()
+sc.close()
+# sharded queue: 2 shards
+G, MA = 2, 300
+ips = tracegen.inst_params(1, base=tracegen.INST_G0, budget_mode=0, target_max=100, alpha=1.5)
+st = oracle.Step(cfg, ips, G * MA)
+hs = [aug.Scheduler(cfg, ips, 1, MA) for _ in range(G)]
+ob = hs[0].shard_offer_bytes()
+led = [torch.zeros(2, dtype=torch.int64, device="cuda") for _ in range(G)]
+off = [torch.zeros(ob, dtype=torch.uint8, device="cuda") for _ in range(G)]
+for t in range(5):
+    rec = random_events(rng, st.slots(0), t, p_new=0.5 if t == 0 else 0.1)
+    if rec is not None:
+        st.enqueue(0, rec)
+        ids = rec["id"].astype(np.int64)
+        for r in range(G):
+            m = (ids // MA) == r
+            if m.any():
+                sub = {k: np.ascontiguousarray(v[m]) for k, v in rec.items()}
+                sub["id"] = (ids[m] - r * MA).astype(np.uint32)
+                hs[r].enqueue(0, sub)
+    o = st.step(t)
+    for r in range(G):
+        hs[r].shard_begin(t, led[r])
+    ls = torch.stack(led).sum(0)
+    for r in range(G):
+        hs[r].shard_offer(ls, off[r])
+    allo = torch.cat(off)
+    outs = [hs[r].shard_commit(allo, G, r) for r in range(G)]
+    g = hs[0].shard_result(outs[0])
+    a = int(o["admitted"][0])
+    assert g["admitted"] == a and g["order"].tolist() == o["order"][0][:a].tolist()
+    assert g["grant"].tolist() == o["grant"][0][:a].tolist()
+for h in hs:
+    h.sync()
+    h.close()
 print("sanitize driver ok")
