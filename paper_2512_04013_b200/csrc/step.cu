@@ -130,7 +130,7 @@ __global__ void rec_phaseA(Rec r, uint32_t n, Slots S, uint32_t* err) {
   const uint32_t st = S.st[g] & 15;
   if (k == AUGSCHED_K_FINISH) {
     if (st < ST_RUN || st > ST_WAIT) { flag_err(err, 1u); return; }
-    ledger_add(&S.A[inst], -(long long)S.kv[g]);
+    if (S.kv[g] != 0) ledger_add(&S.A[inst], -(long long)S.kv[g]);
     S.st[g] = ST_NONE; S.kv[g] = 0; S.ctx[g] = 0; S.cpu[g] = 0; S.pend[g] = 0;
     return;
   }
@@ -199,8 +199,11 @@ __global__ void rec_phaseBC(Rec r, uint32_t n, Slots S, uint64_t now, uint32_t* 
   S.ctx[g] = (int32_t)r.ctx[j]; S.kv[g] = (int32_t)r.kv[j]; S.cpu[g] = (int32_t)r.cpu[j];
   S.pend[g] = (int32_t)r.pend[j];
   if (r.kv[j] > 0 && !(ns == ST_RUN || ns == ST_SWAP || (ns == ST_PAUSED && pol == POL_P))) atomicOr(S.wkv, 1u);
-  if (ns == ST_PAUSED && pol == POL_P) ledger_add(&S.P[inst], (long long)r.kv[j]);
-  else ledger_add(&S.A[inst], (long long)r.kv[j]);
+  // one address per instance: skip the atomic for the (common) KV-free import
+  if (r.kv[j] != 0) {
+    if (ns == ST_PAUSED && pol == POL_P) ledger_add(&S.P[inst], (long long)r.kv[j]);
+    else ledger_add(&S.A[inst], (long long)r.kv[j]);
+  }
 }
 
 // ------------------------------------------------------------------ keys

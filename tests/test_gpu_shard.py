@@ -130,3 +130,46 @@ def test_sharded_cfg4_million():
     for r in range(G):
         assert np.array_equal(hs[r].slots(0), osl[r * MA:(r + 1) * MA])
         hs[r].close()
+
+
+def test_sharded_edge_cases():
+    """Degenerate shards: one shard holds no request at all (its slots are
+    never used), a static limit of 0 for a few steps (nothing admitted), one
+    shard alone (G = 1)."""
+    for G, MA, used in ((3, 200, [0, 2]), (1, 300, [0])):
+        rng = np.random.default_rng(G)
+        cfg = dict(tracegen.PRESET_G0, g_total=1000 + 500, g_model=1000)
+        for lim in (0, 150):
+            ip = tracegen.inst_params(1, base=tracegen.INST_G0, budget_mode=1, l_static=lim, target_max=100)
+            st = oracle.Step(cfg, ip, G * MA)
+            hs = [aug.Scheduler(cfg, ip, 1, MA) for _ in range(G)]
+            ob = hs[0].shard_offer_bytes()
+            led = [torch.zeros(2, dtype=torch.int64, device="cuda") for _ in range(G)]
+            off = [torch.zeros(ob, dtype=torch.uint8, device="cuda") for _ in range(G)]
+            for t in range(8):
+                slots = st.slots(0)
+                rec = random_events(rng, slots, t, p_new=0.5 if t == 0 else 0.1)
+                if rec is not None:
+                    keep = np.isin(rec["id"].astype(np.int64) // MA, used)
+                    rec = {k: np.ascontiguousarray(v[keep]) for k, v in rec.items()}
+                if rec is not None and len(rec["id"]):
+                    assert st.enqueue(0, rec) == 0
+                    for r, sub in enumerate(split_records(rec, G, MA)):
+                        if sub is not None:
+                            hs[r].enqueue(0, sub)
+                o = st.step(t)
+                for r in range(G):
+                    hs[r].shard_begin(t, led[r])
+                ls = torch.stack(led).sum(0)
+                for r in range(G):
+                    hs[r].shard_offer(ls, off[r])
+                allo = torch.cat(off)
+                outs = [hs[r].shard_commit(allo, G, r) for r in range(G)]
+                g = hs[0].shard_result(outs[0])
+                a = int(o["admitted"][0])
+                assert g["admitted"] == a and g["B"] == int(o["B"][0]) and g["n_active"] == int(o["n_active"][0])
+                assert g["order"].tolist() == o["order"][0][:a].tolist()
+                assert g["grant"].tolist() == o["grant"][0][:a].tolist()
+            for h in hs:
+                h.sync()
+                h.close()

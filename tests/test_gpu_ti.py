@@ -100,3 +100,30 @@ def test_batched_mode3_stream():
             compare(g, o, n_inst, f"batched ti step {t}", prefix=pre)
         compare_slots(s, st, n_inst, f"batched ti step {t}")
     s.close()
+
+
+def test_incremental_edge_cases():
+    """Mode 3 with alpha = 0 (the order equals R3's), a static limit of 0
+    (nothing admitted, so no grant changes a word), and a queue that empties
+    (every slot finishes) and refills."""
+    rng = np.random.default_rng(77)
+    MA = 500
+    cfg = dict(tracegen.PRESET_G0, g_total=1000 + 10**6, g_model=1000)
+    for kw in (dict(alpha=0.0, budget_mode=0), dict(alpha=2.0, budget_mode=1, l_static=0)):
+        ip = tracegen.inst_params(1, base=tracegen.INST_G0, ranking=3, target_max=100, **kw)
+        st = oracle.Step(cfg, ip, MA)
+        s = aug.Scheduler(cfg, ip, 1, MA)
+        for t in range(16):
+            if t == 8:   # finish every queued request, then new arrivals
+                sl = st.slots(0)
+                ids = [j for j in range(MA) if sl[j][0] in (1, 2, 3)]
+                rec = oracle.records(len(ids), kind=oracle.K_FINISH, id=ids) if ids else None
+            else:
+                rec = random_events(rng, st.slots(0), t, p_new=0.5 if t in (0, 9) else 0.05)
+            if rec is not None:
+                st.enqueue(0, rec)
+                s.enqueue(0, rec)
+            o = st.step(t)
+            compare(s.step_result(s.step(t)), o, 1, f"ti edge {kw} step {t}")
+        compare_slots(s, st, 1, "ti edge")
+        s.close()
