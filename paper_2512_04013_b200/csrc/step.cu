@@ -93,6 +93,7 @@ constexpr uint32_t TI_DCAP = 8192;   // changed slots one incremental step merge
 
 __device__ __forceinline__ void mark_dirty(const Slots& S, uint32_t g, uint32_t ep) {
   if (!S.dmark) return;
+  if (!S.dlist) { S.dmark[g] = ep; return; }   // batched handles: marks only, no list
   if (atomicExch(&S.dmark[g], ep) != ep) {
     const uint32_t q = atomicAdd(&S.dcnt[ep & 1], 1u);
     if (q < TI_DCAP) S.dlist[(ep & 1) * TI_DCAP + q] = g;
@@ -225,6 +226,7 @@ struct KeyArgs {
 constexpr int PK_KEY = 30;
 constexpr int PK_TIER = 62;
 constexpr uint32_t SLOT_MASK = (1u << 30) - 1;
+constexpr uint32_t INVALID_SLOT = 0xFFFFFFFFu;
 
 __device__ __forceinline__ uint32_t digit_of(unsigned long long x, const PassDesc& d, uint32_t MA) {
   if (d.src == 0) return (uint32_t)(x >> d.shift) & ((1u << d.bits) - 1u);
@@ -1651,11 +1653,69 @@ __global__ void __launch_bounds__(NT) pf_multi_kernel(Slots S, augsched_config c
 #ifndef AUGSCHED_FM_MINB
 #define AUGSCHED_FM_MINB 4     // resident CTAs per SM the register budget targets (256 threads, E = 8; 5 spills: slower)
 #endif
+constexpr uint32_t FM_DCAP = 1024;   // incremental order: out-of-place / changed words merged (else a full sort)
+#ifdef AUGSCHED_FM_TIMING
+// per-phase clocks of full_multi_kernel summed over CTAs: [0..5] phases,
+// [8] CTAs, [9] CTAs that merged incrementally, [10] sum of |D| there
+__device__ unsigned long long g_fm_t[16];
+#define FMT(i) do { if (threadIdx.x == 0) { const long long c_ = clock64(); atomicAdd(&g_fm_t[i], (unsigned long long)(c_ - fm_c)); fm_c = c_; } } while (0)
+#else
+#define FMT(i) do {} while (0)
+#endif
+
+// Block-wide exclusive scans over NT threads (every thread calls; two
+// __syncthreads).  Max of u64 (identity 0) and sum of u32.
+template <int NT>
+__device__ __forceinline__ unsigned long long block_excl_max(unsigned long long v, unsigned long long* tmp) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned long long inc = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long y = __shfl_up_sync(FULL, inc, o);
+    if (lane >= o && y > inc) inc = y;
+  }
+  if (lane == 31) tmp[warp] = inc;
+  __syncthreads();
+  unsigned long long run = 0;
+  for (int w = 0; w < warp; ++w) run = tmp[w] > run ? tmp[w] : run;
+  unsigned long long ex = __shfl_up_sync(FULL, inc, 1);
+  if (lane == 0) ex = 0;
+  __syncthreads();
+  return ex > run ? ex : run;
+}
+template <int NT>
+__device__ __forceinline__ uint32_t block_excl_sum(uint32_t v, uint32_t* tmp, uint32_t& total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t inc = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(FULL, inc, o);
+    if (lane >= o) inc += y;
+  }
+  if (lane == 31) tmp[warp] = inc;
+  __syncthreads();
+  uint32_t run = 0, tot = 0;
+  for (int w = 0; w < NT / 32; ++w) { if (w < warp) run += tmp[w]; tot += tmp[w]; }
+  total = tot;
+  __syncthreads();
+  return run + inc - v;
+}
+// Entries of the sorted a[0, n) below x.
+__device__ __forceinline__ uint32_t lower_rank(const unsigned long long* a, uint32_t n, unsigned long long x) {
+  uint32_t lo = 0, hi = n;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (a[mid] < x) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
 template <int NT, int E>
 __global__ void __launch_bounds__(NT, (NT == 256 && E == 8) ? AUGSCHED_FM_MINB : 1) full_multi_kernel(Slots S, augsched_config cfg, int64_t cap, uint64_t now,
                                                         long long* budget, uint32_t* n_active, uint32_t* tier_off,
                                                         uint32_t* order, uint32_t* keyout, uint32_t* grant,
-                                                        uint32_t* admitted, uint32_t* gslot) {
+                                                        uint32_t* admitted, uint32_t* gslot,
+                                                        uint32_t* mord, uint32_t* mord_n, int inc) {
   constexpr int NW = NT / 32;
   constexpr int NBMAX = 512;
   constexpr uint32_t MP = (uint32_t)NT * E;      // padded slot count (>= MA)
@@ -1671,6 +1731,7 @@ __global__ void __launch_bounds__(NT, (NT == 256 && E == 8) ? AUGSCHED_FM_MINB :
   __shared__ unsigned long long freed;
   __shared__ uint32_t tc_s[3], tsum[NT / 32];
   __shared__ long long B_s;
+  __shared__ uint32_t chgb[MP / 32];              // incremental order: slot changed since the last step
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const unsigned lt = (1u << lane) - 1;
   const uint32_t inst = blockIdx.x;
@@ -1678,23 +1739,34 @@ __global__ void __launch_bounds__(NT, (NT == 256 && E == 8) ? AUGSCHED_FM_MINB :
   const size_t base = (size_t)inst * MA;
   const Coef k = S.coef[inst];
   const augsched_instance_params ip = S.ip[inst];
-  if (tid == 0) {
-    B_s = token_limit(cfg, k, ip, cap, ld_ll(&S.A[inst]), ld_ll(&S.P[inst]));
-    budget[inst] = B_s;
-    tc_s[0] = tc_s[1] = tc_s[2] = 0;
-  }
+  // uniform: the incremental order is tried when the previous step left this
+  // handle's order (the host's flag) and the ranking is not a fresh shuffle
+  const bool inc_try = inc && S.dmark && ip.ranking != AUGSCHED_RANK_RANDOM;
+#ifdef AUGSCHED_FM_TIMING
+  long long fm_c = clock64();
+  if (tid == 0) atomicAdd(&g_fm_t[8], 1ull);
+#endif
+  if (tid == 0) tc_s[0] = tc_s[1] = tc_s[2] = 0;
   __syncthreads();   // the tier counters are clear before any warp adds to them
   // ---- words of every slot (a4), per-tier counts
   uint32_t tcount[3] = {0u, 0u, 0u};
   {
-    // the E slots of this thread loaded together (independent loads in flight)
-    uint32_t stv[E], lst[E];
+    // the E slots of this thread loaded together (independent loads in flight),
+    // with their dirty marks when the incremental order is tried
+    uint32_t stv[E], lst[E], dm[E];
     double V[E];
 #pragma unroll
     for (int e = 0; e < E; ++e) {
       const uint32_t x = tid + e * NT;
-      stv[e] = 0u; lst[e] = 0u; V[e] = 0.0;
-      if (x < MA) { stv[e] = S.st[base + x]; V[e] = S.V[base + x]; lst[e] = S.last[base + x]; }
+      stv[e] = 0u; lst[e] = 0u; V[e] = 0.0; dm[e] = 0u;
+      if (x < MA) {
+        stv[e] = S.st[base + x]; V[e] = S.V[base + x]; lst[e] = S.last[base + x];
+        if (inc_try) dm[e] = __ldcg(&S.dmark[base + x]);
+      }
+    }
+    if (tid == 0) {   // the limit's ledger loads overlap the slot loads
+      B_s = token_limit(cfg, k, ip, cap, ld_ll(&S.A[inst]), ld_ll(&S.P[inst]));
+      budget[inst] = B_s;
     }
 #pragma unroll
     for (int e = 0; e < E; ++e) {
@@ -1707,6 +1779,15 @@ __global__ void __launch_bounds__(NT, (NT == 256 && E == 8) ? AUGSCHED_FM_MINB :
       }
       buf0[x] = w;
     }
+    if (inc_try) {
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const uint32_t x = tid + e * NT;
+        const bool c = x < MA && dm[e] == S.ti_ep;
+        const unsigned b = __ballot_sync(FULL, c);
+        if (lane == 0) chgb[(warp * 32 + e * NT) / 32] = b;
+      }
+    }
   }
 #pragma unroll
   for (int t = 0; t < 3; ++t) {
@@ -1715,6 +1796,111 @@ __global__ void __launch_bounds__(NT, (NT == 256 && E == 8) ? AUGSCHED_FM_MINB :
     for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(FULL, c, o);
     if (lane == 0 && c) atomicAdd(&tc_s[t], c);
   }
+  // ---- incremental order (rankings with an order that persists: the value
+  // order of Eq.26 under R3 or B12, FCFS).  The previous step's order of this
+  // instance minus the slots changed since then (dirty marks: records,
+  // grants, evictions) and minus the unchanged words that are now out of
+  // place (not above the running maximum of the unchanged words before them:
+  // under R3 every waiting score moves by the same alpha*T per step, so only
+  // rounding to fp32 reorders them) is sorted (K); the rest (D) is sorted
+  // here and merged in by rank.  The result is the sorted order of the same
+  // words, so it equals the full sort's; the full sort runs instead when D
+  // does not fit its buffer (or the counts disagree).
+  __syncthreads();   // tier counters and the changed bitmap are complete
+  FMT(0);
+  bool inc_ok = false;
+  if (inc_try) {
+    unsigned long long* dbuf = reinterpret_cast<unsigned long long*>(wcnt);   // [FM_DCAP]
+    const uint32_t m = mord_n[inst];
+    const uint32_t nq = tc_s[0] + tc_s[1] + tc_s[2];
+    auto chg = [&](uint32_t x) { return (chgb[x >> 5] >> (x & 31)) & 1u; };
+    // this thread's E consecutive positions of the previous order: the
+    // unchanged queued words (0 marks a changed or departed slot)
+    unsigned long long pw[E];
+    unsigned long long tmax = 0;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const uint32_t j = (uint32_t)tid * E + e;
+      const uint32_t x = j < m ? __ldcg(&mord[base + j]) : INVALID_SLOT;
+      pw[e] = 0;
+      if (x < MA && !chg(x)) {
+        const unsigned long long w = buf0[x];
+        if ((uint32_t)(w >> PK_TIER) < 3) pw[e] = w;
+      }
+      tmax = pw[e] > tmax ? pw[e] : tmax;
+    }
+    unsigned long long run = block_excl_max<NT>(tmax, wsum);
+    uint32_t keepm = 0, outm = 0, chm = 0;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      if (pw[e]) {
+        if (pw[e] > run) { keepm |= 1u << e; run = pw[e]; }
+        else outm |= 1u << e;
+      }
+      const uint32_t x = tid + e * NT;
+      if (x < MA && chg(x) && (uint32_t)(buf0[x] >> PK_TIER) < 3) chm |= 1u << e;
+    }
+    uint32_t KD = 0;   // both counts in one scan: kept << 16 | D (each <= 8,192)
+    const uint32_t ofs = block_excl_sum<NT>(((uint32_t)__popc(keepm) << 16) | (uint32_t)(__popc(outm) + __popc(chm)),
+                                            tsum, KD);
+    const uint32_t kofs0 = ofs >> 16, dofs0 = ofs & 0xFFFFu, Kt = KD >> 16, Dt = KD & 0xFFFFu;
+    if (Dt <= FM_DCAP && Kt + Dt == nq) {   // uniform
+      uint32_t ko = kofs0, d0 = dofs0;
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        if ((keepm >> e) & 1u) buf1[ko++] = pw[e];
+        if ((outm >> e) & 1u) dbuf[d0++] = pw[e];
+        if ((chm >> e) & 1u) dbuf[d0++] = buf0[tid + e * NT];
+      }
+      __syncthreads();   // buf0 is no longer read: it serves the sort's exchange, then holds the order
+      uint32_t P2 = 32;
+      while (P2 < Dt) P2 <<= 1;
+      if (Dt > 1) {
+        if (P2 <= (uint32_t)NT) {
+          if ((uint32_t)tid < P2) {
+            unsigned long long v = (uint32_t)tid < Dt ? dbuf[tid] : ~0ull;
+            bar_named(P2);
+            switch (P2) {
+              case 32: v = bitonic1<5>(v, dbuf, buf0); break;
+              case 64: v = bitonic1<6>(v, dbuf, buf0); break;
+              case 128: v = bitonic1<7>(v, dbuf, buf0); break;
+              case 256: v = bitonic1<8>(v, dbuf, buf0); break;
+              default: v = bitonic1<9>(v, dbuf, buf0); break;
+            }
+            bar_named(P2);
+            dbuf[tid] = v;
+          }
+        } else if (NT == 256) {
+          if (P2 == 512) pf_sortE<256, 9>(dbuf, buf0, Dt);
+          else pf_sortE<256, 10>(dbuf, buf0, Dt);
+        } else {
+          pf_sortE<512, 10>(dbuf, buf0, Dt);
+        }
+      }
+      __syncthreads();
+      {   // this thread's kept words are consecutive: one search, then a walk
+        uint32_t r = 0;
+        const uint32_t nk = (uint32_t)__popc(keepm);
+        for (uint32_t q = 0; q < nk; ++q) {
+          const uint32_t i = kofs0 + q;
+          const unsigned long long w = buf1[i];
+          if (q == 0) r = lower_rank(dbuf, Dt, w);
+          else while (r < Dt && dbuf[r] < w) ++r;
+          buf0[i + r] = w;
+        }
+      }
+      for (uint32_t j = tid; j < Dt; j += NT) {
+        const unsigned long long w = dbuf[j];
+        buf0[j + lower_rank(buf1, Kt, w)] = w;
+      }
+      for (uint32_t j = nq + tid; j < MP; j += NT) buf0[j] = ~0ull;
+      inc_ok = true;
+#ifdef AUGSCHED_FM_TIMING
+      if (tid == 0) { atomicAdd(&g_fm_t[9], 1ull); atomicAdd(&g_fm_t[10], (unsigned long long)Dt); }
+#endif
+    }
+    __syncthreads();
+  }
   // ---- LSD radix sort of bits [30, 64) (tier:2 | key:32), stable.
   // Counters are warp-major (wcnt[w * NBMAX + d]: the leaders of one warp hit
   // distinct banks unless their digits agree mod 32); thread t owns digits
@@ -1722,7 +1908,7 @@ __global__ void __launch_bounds__(NT, (NT == 256 && E == 8) ? AUGSCHED_FM_MINB :
   unsigned long long* src = buf0;
   unsigned long long* dst = buf1;
 #pragma unroll 1
-  for (int p = 0; p < 4; ++p) {
+  for (int p = 0; p < (inc_ok ? 0 : 4); ++p) {
     const int shift = PK_KEY + (p == 0 ? 0 : p == 1 ? 9 : p == 2 ? 18 : 26), bits = p < 2 ? 9 : 8;
     const int NB = 1 << bits;
     for (int i = tid; i < NBMAX * NW; i += NT) wcnt[i] = 0;
@@ -1785,15 +1971,22 @@ __global__ void __launch_bounds__(NT, (NT == 256 && E == 8) ? AUGSCHED_FM_MINB :
     __syncthreads();
     unsigned long long* t = src; src = dst; dst = t;
   }
+  FMT(1);
   // ---- admission (R17), resolution (R20), grant accounting over the order
   const uint32_t c0 = tc_s[0], c1 = tc_s[1], c2 = tc_s[2];
   const uint32_t n = c0 + c1 + c2;
   const long long B = B_s;
   const uint32_t target = pf_target(B, n);
   const uint32_t prev = S.gdirty[inst];
+  if (mord) {   // this order is the next step's starting point
+    for (uint32_t j = tid; j < n; j += NT) mord[base + j] = (uint32_t)src[j] & SLOT_MASK;
+    if (tid == 0) mord_n[inst] = n;
+  }
+  FMT(2);
   pf_finish<NT, 8, true>(S, cfg, cap, now, inst, base, src, src, dst, n, target, B, order, keyout, grant,
                          admitted, gslot, sel, wsum, freed, nullptr, 0, n);
   __syncthreads();
+  FMT(3);
   // ---- the rest of the order; zero grants beyond the prefix (R16)
   const uint32_t adm = admitted[inst];   // written by thread 0 at the end of pf_finish
   for (uint32_t j = adm + tid; j < n; j += NT) {
@@ -1802,6 +1995,8 @@ __global__ void __launch_bounds__(NT, (NT == 256 && E == 8) ? AUGSCHED_FM_MINB :
     keyout[base + j] = (uint32_t)(w >> PK_KEY);
   }
   for (uint32_t j = adm + tid; j < prev && j < MA; j += NT) grant[base + j] = 0;
+  __syncthreads();
+  FMT(4);
   if (tid == 0) {
     S.gdirty[inst] = adm;
     n_active[inst] = n;
@@ -2921,10 +3116,21 @@ int grow_records(StepState& st, uint32_t need, cudaStream_t s) {
 Slots slots_of(StepState& st, const augsched_instance_params* d_ip, uint32_t* d_err) {
   return Slots{st.st, st.V, st.last, st.ctx, st.kv, st.cpu, st.pend, st.A, st.P, st.Aevt, st.Asnap,
                st.coef, d_ip, st.max_active, st.wkv, st.claimA, st.claimB, st.rec_batch, st.gdirty, d_err,
-               st.ti ? st.dmark : nullptr, st.dlist, st.dcnt, st.ti_ep};
+               (st.ti || st.minc) ? st.dmark : nullptr, st.ti ? st.dlist : nullptr, st.dcnt, st.ti_ep};
 }
 
 }  // namespace
+
+#ifdef AUGSCHED_FM_TIMING
+extern "C" AUGSCHED_API int augsched_fm_timing(unsigned long long* host, int reset) {
+  if (cudaMemcpyFromSymbol(host, g_fm_t, sizeof(g_fm_t)) != cudaSuccess) return -3;
+  if (reset) {
+    static const unsigned long long z[16] = {};
+    if (cudaMemcpyToSymbol(g_fm_t, z, sizeof(z)) != cudaSuccess) return -3;
+  }
+  return 0;
+}
+#endif
 
 static size_t pf_smem_bytes() { return sizeof(unsigned long long) * 2 * PF_SCAP; }
 static size_t coop_smem_bytes() {
@@ -3059,6 +3265,21 @@ int step_ensure(StepState& st, uint32_t n_inst, uint32_t max_active, cudaStream_
       st.ti = false;
     }
   }
+  // batched full step: each instance's order is kept for the next step, which
+  // merges the changed slots into it (full_multi_kernel)
+  st.minc = false;
+  st.minc_valid = false;
+#ifndef AUGSCHED_NO_MINC
+  if (n_inst > 1 && max_active <= 8192) {
+    if ((rc = salloc(st, &st.mord, N)) || (rc = salloc(st, &st.mord_n, n_inst)) ||
+        (rc = salloc(st, &st.dmark, N)))
+      return rc;
+    if ((rc = cuda_check(cudaMemsetAsync(st.dmark, 0, sizeof(uint32_t) * N, s), "step_ensure: clear")) ||
+        (rc = cuda_check(cudaMemsetAsync(st.mord_n, 0, sizeof(uint32_t) * n_inst, s), "step_ensure: clear")))
+      return rc;
+    st.minc = true;
+  }
+#endif
   cudaFuncSetAttribute(pf_multi_kernel<PNT, PF_SCAP / PNT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)PF_MULTI_SMEM);
   st.epoch = 0;
@@ -3128,7 +3349,7 @@ void run_records(StepState& st, Slots S, uint32_t* d_err, uint64_t now, cudaStre
 // Time-invariant handles: the step epoch of the dirty marks, and the clear
 // of the consumed list after the step's kernels.
 static void ti_begin(StepState& st) {
-  if (st.ti) ++st.ti_ep;
+  if (st.ti || st.minc) ++st.ti_ep;
 }
 static int ti_end(StepState& st, cudaStream_t s) {
   if (!st.ti) return AUGSCHED_OK;
@@ -3138,6 +3359,7 @@ static int ti_end(StepState& st, cudaStream_t s) {
 int step_run_prefix(StepState& st, const augsched_config& cfg, int64_t cap,
                     const augsched_instance_params* d_ip, uint32_t* d_err, uint64_t now,
                     augsched_step_out* out, cudaStream_t s, uint64_t* launches) {
+  st.minc_valid = false;   // the batched full step's kept order does not see this step's changes
   // the prefix selection is bounded by PF_SCAP; several instances need their
   // slots on chip (one CTA per instance)
   uint32_t scap = 32;
@@ -3214,7 +3436,8 @@ static void launch_full_multi(const StepState& st, const Slots& S, const augsche
     attr = true;
   }
   full_multi_kernel<NT, E><<<st.n_inst, NT, smem, s>>>(S, cfg, cap, now, st.budget, st.n_active, st.tier_off,
-                                                        st.order, st.key, st.grant, st.admitted, st.gslot);
+                                                        st.order, st.key, st.grant, st.admitted, st.gslot,
+                                                        st.mord, st.mord_n, st.minc_valid ? 1 : 0);
 }
 
 int step_run(StepState& st, const augsched_config& cfg, int64_t cap,
@@ -3276,6 +3499,7 @@ int step_run(StepState& st, const augsched_config& cfg, int64_t cap,
     else if (MA <= 2048) launch_full_multi<256, 8>(st, S, cfg, cap, now, s);
     else if (MA <= 4096) launch_full_multi<256, 16>(st, S, cfg, cap, now, s);
     else launch_full_multi<512, 16>(st, S, cfg, cap, now, s);
+    st.minc_valid = st.minc;   // this step's order is the next one's starting point
     *launches += 1;
     out->budget = reinterpret_cast<const int64_t*>(st.budget);
     out->n_active = st.n_active;

@@ -109,6 +109,12 @@ struct StepState {
   unsigned long long* ubuf = nullptr;   // [N] the unchanged words, compacted
   uint32_t* ti_misc = nullptr;    // [4] per-call scratch: |D| after filtering, tier counts of D
   uint32_t* ti_gcnt = nullptr;    // [TI_DCAP + 1] unchanged words per rank among the changed ones
+  // batched full step (full_multi_kernel): each instance's order is kept
+  // across steps and the next step merges what changed into it
+  bool minc = false;
+  bool minc_valid = false;        // mord holds the previous full step's order of every instance
+  uint32_t* mord = nullptr;       // [N] order by instance (local slots)
+  uint32_t* mord_n = nullptr;     // [n_inst] its length
   unsigned long long* coop_bar = nullptr;   // its grid-barrier counter (monotone)
   unsigned long long coop_bar_base = 0;     // the counter's value at the next call's start
   uint32_t* coop_hist = nullptr;            // [4][coop_grid][512] per-CTA digit histograms

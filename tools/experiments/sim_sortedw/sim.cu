@@ -19,16 +19,15 @@
 namespace augsched {
 
 constexpr int MAXPOP = 32;   // pop rounds before falling back to a radix select over W
-
-#ifdef AUGSCHED_SIM_STATS
-// Path counters and phase clocks of the stats build (tools/sim_stats.py).
-__device__ unsigned long long g_sim_stats[64];
-#define SSTAT(i, v) do { if ((threadIdx.x % SIM_NT) == 0) atomicAdd(&g_sim_stats[i], (unsigned long long)(v)); } while (0)
-#define PT(i) do { if ((threadIdx.x % SIM_NT) == 0) s.pt[i] = clock64(); } while (0)
-#else
-#define SSTAT(i, v) do { } while (0)
-#define PT(i) do { } while (0)
+#ifndef AUGSCHED_SIM_SORTEDW
+#define AUGSCHED_SIM_SORTEDW 1
 #endif
+constexpr bool SIM_SORTEDW = AUGSCHED_SIM_SORTEDW != 0;   // sorted W list (value rankings)
+#ifndef AUGSCHED_SIM_TAILMERGE
+#define AUGSCHED_SIM_TAILMERGE 16
+#endif
+constexpr uint32_t TAIL_MERGE = AUGSCHED_SIM_TAILMERGE;   // tail length that triggers a rebuild
+constexpr uint32_t MH_MAX = 32;                           // main holes that trigger a rebuild
 
 struct __align__(16) SimShm {
   union {
@@ -54,6 +53,16 @@ struct __align__(16) SimShm {
                                         // folded into cnt when the instance's window ends
   unsigned int holes[2][HOLE_CAP];   // hole positions of R (0) and W (1)
   unsigned int nholes[2];
+  unsigned int bpos[SIM_CAND];       // sorted-W selection: W positions of the band candidates
+  // W list layout: sorted main [wh, ws) holding mh holes, unsorted tail
+  // [ws, we), buffer wbuf; sorted = the instance keeps main sorted by u
+  unsigned int wh, ws, we, mh, wbuf;
+  unsigned int tclean;               // the tail is sorted by u in memory
+  int sorted;
+#ifdef AUGSCHED_SIM_STATS
+  long long pt[9];                   // stats build: clock at the step's phase points
+  int full;                          //   the step ran to its end
+#endif
   unsigned int wtot[SIM_NW + 1];
   Coef coef;                         // per-instance constants (§8(c).1)
   augsched_instance_params ip;
@@ -65,10 +74,6 @@ struct __align__(16) SimShm {
   unsigned int inst;
   unsigned int trace, r0, n;         // the instance's trace and its request range
   int run, idle, abort;
-#ifdef AUGSCHED_SIM_STATS
-  long long pt[9];                   // stats build: clock at the step's phase points
-  int full;                          //   the step ran to its end
-#endif
 };
 
 enum : int {
@@ -159,6 +164,12 @@ struct List {
   }
 };
 
+// W list of instance `inst` in buffer `buf` (sim.cuh Arena).
+__device__ __forceinline__ List w_list(const SimParams& p, uint32_t inst, uint32_t buf) {
+  const size_t o = ((size_t)inst * 2 + buf) * p.w_stride;
+  return List{p.ar.w_q + o, p.ar.w_dem + o};
+}
+
 struct Ctx {
   const SimParams& p;
   SimShm& s;
@@ -222,7 +233,9 @@ __device__ void do_return(Ctx& c, uint32_t id) {
   // last is not reset on return (R14)
   if (tier < 2) c.R.put(atomicAdd(&s.n_r, 1u), id | (tier << 30), V, r.lastc, dem);
   else {
-    c.W.put(atomicAdd(&s.n_w, 1u), id | (2u << 30), V, r.lastc, dem);
+    c.W.put(atomicAdd(&s.we, 1u), id | (2u << 30), V, r.lastc, dem);   // W tail
+    atomicAdd(&s.n_w, 1u);
+    s.tclean = 0;
     atomicAdd(&s.w2, (unsigned long long)dem);
   }
 }
@@ -253,6 +266,41 @@ __device__ void do_arrival(Ctx& c, uint32_t id, uint32_t pos, uint64_t t) {
   atomicAdd(&c.s.w2, (unsigned long long)L);
 }
 
+// Fill the holes (e == INVALID) among positions [lo, lo + n) of list l with
+// the valid entries at the range's end (order not kept).  h[0..nh) lists
+// hole positions (nh <= HOLE_CAP; positions outside the range are ignored;
+// h is reused as scratch).  Warp-parallel: destinations (holes below the new
+// end) and sources (valid entries at or above it) are paired by rank.
+// Returns the number of holes inside the range.
+__device__ __noinline__ uint32_t fill_holes(const List& l, uint32_t* h, uint32_t nh, uint32_t lo, uint32_t n) {
+  const int lane = ITID;
+  const unsigned lt = (1u << lane) - 1;
+  const uint32_t ha = (uint32_t)lane < nh ? h[lane] : INVALID;
+  const uint32_t hb = (uint32_t)lane + 32 < nh ? h[lane + 32] : INVALID;
+  const bool ina = ha != INVALID && ha >= lo && ha - lo < n;
+  const bool inb = hb != INVALID && hb >= lo && hb - lo < n;
+  const uint32_t nt = __popc(__ballot_sync(FULL, ina)) + __popc(__ballot_sync(FULL, inb));
+  const uint32_t end = lo + n - nt;
+  const bool da = ina && ha < end, db = inb && hb < end;
+  const unsigned mda = __ballot_sync(FULL, da), mdb = __ballot_sync(FULL, db);
+  const uint32_t pa = end + lane, pb = end + 32 + lane;
+  QEnt xa, xb;
+  xa.e = INVALID;
+  xb.e = INVALID;
+  if (pa < lo + n) xa = l.q[pa];
+  if (pb < lo + n) xb = l.q[pb];
+  const bool sa = xa.e != INVALID, sb = xb.e != INVALID;
+  const unsigned msa = __ballot_sync(FULL, sa), msb = __ballot_sync(FULL, sb);
+  ISYNC();   // every lane has read h
+  if (da) h[__popc(mda & lt)] = ha;
+  if (db) h[__popc(mda) + __popc(mdb & lt)] = hb;
+  ISYNC();
+  if (sa) { const uint32_t d = h[__popc(msa & lt)]; l.q[d] = xa; l.dem[d] = l.dem[pa]; }
+  if (sb) { const uint32_t d = h[__popc(msa) + __popc(msb & lt)]; l.q[d] = xb; l.dem[d] = l.dem[pb]; }
+  ISYNC();
+  return nt;
+}
+
 // Remove the entries of list `L` (0 = R, 1 = W) whose id is INVALID.
 __device__ void compact_list(SimShm& s, const List& l, int L, unsigned int& n_ref) {
   const int tid = ITID;
@@ -261,28 +309,8 @@ __device__ void compact_list(SimShm& s, const List& l, int L, unsigned int& n_re
   if (nh == 0) return;
   ISYNC();   // every lane has read nholes before thread 0 clears it
   if (nh <= HOLE_CAP) {
-    if (tid == 0) {
-      const uint32_t n = n_ref, n_new = n - nh;
-      uint32_t* h = s.holes[L];
-      for (uint32_t a = 1; a < nh; ++a) {  // insertion sort (few holes)
-        uint32_t x = h[a];
-        int b = (int)a - 1;
-        while (b >= 0 && h[b] > x) { h[b + 1] = h[b]; --b; }
-        h[b + 1] = x;
-      }
-      int j = (int)nh - 1;
-      int src = (int)n - 1;
-      for (uint32_t a = 0; a < nh; ++a) {
-        const uint32_t hp = h[a];
-        if (hp >= n_new) break;
-        while (j >= 0 && (int)h[j] == src) { --j; --src; }
-        l.q[hp] = l.q[src];
-        l.dem[hp] = l.dem[src];
-        --src;
-      }
-      n_ref = n_new;
-      s.nholes[L] = 0;
-    }
+    const uint32_t nt = fill_holes(l, s.holes[L], nh, 0, n_ref);
+    if (tid == 0) { n_ref -= nt; s.nholes[L] = 0; }
     ISYNC();
     return;
   }
@@ -330,6 +358,488 @@ __device__ void compact_paused(Ctx& c) {
   }
   if (tid == 0) s.n_pz = s.wpos;
   ISYNC();
+}
+
+// ---------------------------------------------------------------------------
+// Sorted W list (instances ranked by value: AUGSCHED_RANK_AUGSERVE and _TI).
+//
+// At iteration t a waiting entry's score is s = V - alpha*((t - last)*Ts)
+// (R3) or V + alpha*(last*Ts) (B12).  Both are u - alpha*t*Ts up to
+// rounding, with the time-invariant u = V + alpha*(last*Ts) (ti_key's
+// operand).  V and last do not change while an entry waits (they change
+// only when it is granted, and then it leaves W), so W is kept ordered by u
+// across steps: a sorted main part [wh, ws) (removed entries leave holes,
+// the head advances), and an unsorted tail [ws, we) of the entries inserted
+// since the last rebuild (arrivals, returns, evictions), merged into main
+// when it reaches TAIL_MERGE entries.
+//
+// The admission prefix is then found near the head instead of by a pass
+// over all of W.  Let m be the entry where the W demand, taken in u order,
+// first reaches the budget left after R, and X = |u_m| + 4|alpha t Ts|.
+// Rounding moves s - (u - alpha t Ts) by at most 2^-51 X for the entries
+// near u_m, and fp32 spacing there is at most 2^-23 X, so with
+// delta = 2^-19 X (+ 2^-140 for subnormals) any two entries whose u differ
+// by more than delta have strictly ordered fp32 keys (X < 2^120: the band
+// stays inside fp32's finite range; an entry far outside it may round to
+// an infinity, which is still on the right side).  Hence (i) the last
+// admitted entry k* of the exact (key, id) order has |u - u_m| <= delta
+// (an entry further below would be reached by demand taken strictly below
+// u_m, which is short of the budget; one further above would follow every
+// entry up to m, whose demand already reaches it); (ii) every entry with
+// u < u_m - 2 delta precedes k* and is admitted in full, every entry with
+// u > u_m + 2 delta follows it.  The step computes exact keys only for the
+// entries below u_m + 2 delta (usually a handful), selects k* among the
+// band |u - u_m| <= 2 delta with the demand below it as the base, and
+// grants exactly what the sorted-order definition grants.  Whenever a
+// bound does not hold (band or prefix larger than the shared lists, a
+// non-finite score), the step rebuilds W densely and takes the general
+// path below.
+// ---------------------------------------------------------------------------
+#ifdef AUGSCHED_SIM_STATS
+// Path counters of the stats build (tools/sim_stats.py): which W path each
+// step takes, why the sorted path fell back, rebuild causes, work sizes.
+__device__ unsigned long long g_sim_stats[64];
+#define SSTAT(i, v) do { if (ITID == 0) atomicAdd(&g_sim_stats[i], (unsigned long long)(v)); } while (0)
+#define PT(i) do { if (ITID == 0) s.pt[i] = clock64(); } while (0)
+#else
+#define SSTAT(i, v) do { } while (0)
+#define PT(i) do { } while (0)
+#endif
+
+__device__ __forceinline__ double dinf() { return __longlong_as_double(0x7ff0000000000000ll); }
+
+// The time-invariant order value of a W entry (ti_key's operand, B12).
+__device__ __forceinline__ double w_u(const Coef& k, const QEnt& x) {
+  return dadd(x.V, dmul(k.alpha, dmul(u2d(x.last), k.Ts)));
+}
+
+__device__ __forceinline__ unsigned long long wscan_add(unsigned long long v, int lane) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long y = __shfl_up_sync(FULL, v, o);
+    if (lane >= o) v += y;
+  }
+  return v;
+}
+__device__ __forceinline__ double wscan_max(double v, int lane) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double y = __shfl_up_sync(FULL, v, o);
+    if (lane >= o && y > v) v = y;
+  }
+  return v;
+}
+__device__ __forceinline__ unsigned long long wmin_u64(unsigned long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long y = __shfl_xor_sync(FULL, v, o);
+    v = y < v ? y : v;
+  }
+  return v;
+}
+// The lanes hold a non-decreasing sequence a; the number of lanes with
+// a < x (LE: a <= x).  Binary search by shuffles.
+template <bool LE>
+__device__ __forceinline__ int wcount(double a, double x) {
+  int pos = 0;
+#pragma unroll
+  for (int st = 16; st > 0; st >>= 1) {
+    const double v = __shfl_sync(FULL, a, pos + st - 1);
+    if (LE ? v <= x : v < x) pos += st;
+  }
+  const double v = __shfl_sync(FULL, a, pos);
+  return pos + ((LE ? v <= x : v < x) ? 1 : 0);
+}
+// Bitonic sort of one (u, demand, position) triple per lane, ascending by
+// (u, position); empty lanes carry (+inf, 0, INVALID) and sort last.
+__device__ __forceinline__ void wsort(double& u, uint32_t& d, uint32_t& pos, int lane) {
+#pragma unroll
+  for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      const double ou = __shfl_xor_sync(FULL, u, j);
+      const uint32_t od = __shfl_xor_sync(FULL, d, j), op = __shfl_xor_sync(FULL, pos, j);
+      const bool less = ou < u || (ou == u && op < pos);     // the partner orders first
+      const bool more = ou > u || (ou == u && op > pos);
+      const bool keep_min = ((lane & j) == 0) == ((lane & k) == 0);
+      if (keep_min ? less : more) { u = ou; d = od; pos = op; }
+    }
+  }
+}
+
+// Rebuild W into the other buffer: the main survivors merged with the tail
+// in u order, holes dropped (tail merged 32 entries per round).  Leaves
+// wh = 0, ws = we = live count, mh = 0, and c.W on the new buffer.
+__device__ __noinline__ void w_rebuild(const SimParams& p, SimShm& s) {
+  const int lane = ITID;
+  const unsigned lt = (1u << lane) - 1;
+  ISYNC();
+  SSTAT(7, 1);
+  SSTAT(19, s.we - s.wh);
+  for (;;) {
+    const uint32_t wh = s.wh, ws = s.ws, we = s.we, buf = s.wbuf;
+    const List src = w_list(p, s.inst, buf), dst = w_list(p, s.inst, buf ^ 1u);
+    const uint32_t k = we - ws < 32u ? we - ws : 32u;
+    double tu = dinf();
+    uint32_t td = 0, tp = INVALID;
+    if ((uint32_t)lane < k) {
+      const QEnt x = src.q[ws + lane];
+      if (x.e != INVALID) { tu = w_u(s.coef, x); td = src.dem[ws + lane]; tp = ws + lane; }
+    }
+    wsort(tu, td, tp, lane);
+    const uint32_t kv = __popc(__ballot_sync(FULL, tp != INVALID));
+    uint32_t mout = 0, tle = 0;   // main survivors written; (tail lane) those with u <= tu
+    double carry = -dinf();
+    for (uint32_t b = wh; b < ws; b += 32) {
+      const uint32_t i = b + lane;
+      QEnt x;
+      x.e = INVALID;
+      uint32_t d = 0;
+      if (i < ws) { x = src.q[i]; if (x.e != INVALID) d = src.dem[i]; }
+      const bool ok = x.e != INVALID;
+      const double u = ok ? w_u(s.coef, x) : 0.0;
+      // non-decreasing copy of the chunk: holes take the running maximum
+      double um = wscan_max(ok ? u : (i < ws ? -dinf() : dinf()), lane);
+      um = um > carry ? um : carry;
+      carry = __shfl_sync(FULL, um, 31);
+      const unsigned okm = __ballot_sync(FULL, ok);
+      const int below = wcount<false>(tu, u);          // tail entries ordered before this one
+      if (ok) {
+        const uint32_t o = mout + __popc(okm & lt) + (uint32_t)below;
+        dst.q[o] = x;
+        dst.dem[o] = d;
+      }
+      const int cle = wcount<true>(um, tu);            // chunk entries ordered before tail lane
+      tle += __popc(okm & (cle >= 32 ? FULL : ((1u << cle) - 1u)));
+      mout += __popc(okm);
+    }
+    if (tp != INVALID) {
+      const uint32_t o = tle + (uint32_t)lane;
+      dst.q[o] = src.q[tp];
+      dst.dem[o] = td;
+    }
+    // the rest of the tail stays unsorted behind the merged part
+    uint32_t o2 = mout + kv;
+    for (uint32_t b = ws + k; b < we; b += 32) {
+      const uint32_t i = b + lane;
+      QEnt x;
+      x.e = INVALID;
+      uint32_t d = 0;
+      if (i < we) { x = src.q[i]; if (x.e != INVALID) d = src.dem[i]; }
+      const bool ok = x.e != INVALID;
+      const unsigned okm = __ballot_sync(FULL, ok);
+      if (ok) { dst.q[o2 + __popc(okm & lt)] = x; dst.dem[o2 + __popc(okm & lt)] = d; }
+      o2 += __popc(okm);
+    }
+    ISYNC();
+    if (lane == 0) { s.wbuf = buf ^ 1u; s.wh = 0; s.ws = mout + kv; s.we = o2; s.mh = 0; s.tclean = 0; }
+    ISYNC();
+    if (s.we == s.ws) break;
+  }
+  if (lane == 0) s.tclean = 1;
+#ifdef AUGSCHED_DEBUG
+  if (lane == 0 && s.we != s.n_w) err_set(p, 8u);
+#endif
+}
+
+template <class T>
+__device__ __forceinline__ int wcount_le(T a, T x) {   // lanes with a <= x (a non-decreasing)
+  int pos = 0;
+#pragma unroll
+  for (int st = 16; st > 0; st >>= 1) {
+    const T v = __shfl_sync(FULL, a, pos + st - 1);
+    if (v <= x) pos += st;
+  }
+  const T v = __shfl_sync(FULL, a, pos);
+  return pos + (v <= x ? 1 : 0);
+}
+
+// Sort the tail [ws, we) (at most 32 entries, no holes) by (u, position) in
+// place, unless it is already sorted.
+__device__ __noinline__ void w_tail_sort(const SimParams& p, SimShm& s) {
+  const int lane = ITID;
+  ISYNC();
+  if (s.tclean) return;
+  const uint32_t ws = s.ws, k = s.we - ws;
+  const List W = w_list(p, s.inst, s.wbuf);
+  QEnt x;
+  x.e = INVALID;
+  x.V = 0.0;
+  x.last = 0;
+  double u = dinf();
+  uint32_t d = 0, src = INVALID;
+  if ((uint32_t)lane < k) { x = W.q[ws + lane]; d = W.dem[ws + lane]; u = w_u(s.coef, x); src = lane; }
+  wsort(u, d, src, lane);
+  const int sl = src == INVALID ? 0 : (int)src;
+  const double V = __shfl_sync(FULL, x.V, sl);
+  const uint32_t last = __shfl_sync(FULL, x.last, sl), e = __shfl_sync(FULL, x.e, sl);
+  ISYNC();
+  if ((uint32_t)lane < k) {
+    QEnt y;
+    y.V = V; y.last = last; y.e = e;
+    W.q[ws + lane] = y;
+    W.dem[ws + lane] = d;
+  }
+  ISYNC();
+  if (lane == 0) s.tclean = 1;
+  ISYNC();
+}
+
+// Merge the sorted tail (at most 32 entries) into the sorted main in place:
+// walking main from its end, each slot moves up by the number of tail
+// entries ordered before it (main first on equal u; a hole moves with the
+// next valid slot to its right), until a chunk whose first slot stays; then
+// each tail entry drops into the gap left for it.  The cost is the part of
+// main above the smallest tail entry, not all of W.
+__device__ __noinline__ void w_merge_tail(const SimParams& p, SimShm& s) {
+  const int lane = ITID;
+  ISYNC();
+  const uint32_t wh = s.wh, ws = s.ws, k = s.we - ws;
+  const List W = w_list(p, s.inst, s.wbuf);
+  QEnt tq;
+  tq.e = INVALID;
+  double tu = dinf();
+  uint32_t td = 0;
+  if ((uint32_t)lane < k) { tq = W.q[ws + lane]; td = W.dem[ws + lane]; tu = w_u(s.coef, tq); }
+  constexpr int BIG = 1 << 20;
+  int carry = (int)k;      // shift of the nearest valid slot to the right
+  uint32_t gt = 0;         // (tail lane j) main slots ordered after tail entry j
+  for (uint32_t b_hi = ws; b_hi > wh && carry > 0;) {
+    const uint32_t b_lo = b_hi - wh > 32u ? b_hi - 32u : wh;
+    const uint32_t i = b_lo + lane;
+    const bool in = i < b_hi;
+    QEnt x;
+    x.e = INVALID;
+    uint32_t d = 0;
+    if (in) { x = W.q[i]; d = W.dem[i]; }
+    const bool ok = in && x.e != INVALID;
+    const double u = ok ? w_u(s.coef, x) : 0.0;
+    const int nlt = wcount<false>(tu, u);   // tail entries strictly below u
+    int v = ok ? nlt : BIG;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {     // suffix minimum: holes take the next valid shift
+      const int y = __shfl_down_sync(FULL, v, o);
+      if (lane + o < 32 && y < v) v = y;
+    }
+    v = v < carry ? v : carry;
+    carry = __shfl_sync(FULL, v, 0);
+    ISYNC();   // the chunk is read before any slot of it is overwritten
+    if (in && v > 0) { W.q[i + v] = x; W.dem[i + v] = d; }
+    const int n_in = (int)(b_hi - b_lo);
+    const int le = wcount_le<int>(in ? v : BIG, lane);   // (tail lane j = lane) slots with shift <= j
+    gt += (uint32_t)(n_in - le);
+    b_hi = b_lo;
+  }
+  ISYNC();
+  if ((uint32_t)lane < k) { const uint32_t o = ws - gt + lane; W.q[o] = tq; W.dem[o] = td; }
+  ISYNC();
+  if (lane == 0) { s.ws = s.we; s.tclean = 1; }
+  ISYNC();
+}
+
+// End-of-step W compaction.  Holes of this step in the tail are filled from
+// the tail's end; holes in the sorted main stay (counted in mh) and the head
+// skips those in front; a sorted instance rebuilds when the tail, the holes
+// or the wasted space grow too large.  n_w drops by the step's removals.
+__device__ __noinline__ void w_compact(const SimParams& p, SimShm& s) {
+  const List W = w_list(p, s.inst, s.wbuf);
+  const int lane = ITID;
+  ISYNC();
+  const uint32_t nh = s.nholes[1];
+  ISYNC();   // every lane has read nholes before lane 0 clears it
+  if (nh > HOLE_CAP) {
+    if (lane == 0) { s.n_w -= nh; s.nholes[1] = 0; }
+    ISYNC();
+    if (s.sorted) {
+      w_rebuild(p, s);
+    } else {
+      unsigned int n_ref = s.we;
+      if (lane == 0) s.nholes[1] = HOLE_CAP + 1;   // take compact_list's streaming path
+      compact_list(s, W, 1, n_ref);
+      if (lane == 0) s.we = n_ref;
+      ISYNC();
+    }
+  } else if (nh > 0) {
+    const uint32_t ws = s.ws;
+    const uint32_t nt = fill_holes(W, s.holes[1], nh, ws, s.we - ws);
+    if (lane == 0) {
+      s.we -= nt;
+      s.mh += nh - nt;
+      s.n_w -= nh;
+      s.nholes[1] = 0;
+      if (nt) s.tclean = 0;
+    }
+    ISYNC();
+  }
+  if (!s.sorted) return;
+  // skip the holes at the head of the sorted main
+  for (;;) {
+    const uint32_t wh = s.wh, ws = s.ws;
+    if (s.mh == 0 || wh >= ws) break;
+    const uint32_t i = wh + lane;
+    const bool ok = i < ws && W.q[i].e != INVALID;
+    const unsigned m = __ballot_sync(FULL, ok);
+    const uint32_t lim = ws - wh < 32u ? ws - wh : 32u;
+    const uint32_t skip = m ? (uint32_t)(__ffs(m) - 1) : lim;
+    ISYNC();
+    if (lane == 0) { s.wh = wh + skip; s.mh -= skip; }
+    ISYNC();
+    if (m) break;
+  }
+  if (lane == 0 && s.wh == s.ws && s.ws == s.we) { s.wh = 0; s.ws = 0; s.we = 0; s.tclean = 1; }  // empty
+  ISYNC();
+  if (s.mh > MH_MAX || s.we + (s.n - s.n_w) > p.w_stride) {
+    SSTAT(9, 1);
+    w_rebuild(p, s);
+  } else if (s.we - s.ws >= TAIL_MERGE) {
+    SSTAT(21, 1);
+    w_tail_sort(p, s);
+    w_merge_tail(p, s);
+  }
+}
+
+// The admission prefix of W on a sorted list (see above).  Bu: the budget;
+// wR: the demand of R (every R entry precedes W; wR < Bu).  On success the
+// step's granted W entries are the popped list (s.pk/pw/pp, WMODE_POP) and
+// s.res holds k* as the general path would.  False: take the general path.
+__device__ __noinline__ bool w_sorted_select(const SimParams& p, SimShm& s, uint64_t t, unsigned long long Bu,
+                                             unsigned long long wR) {
+  const int lane = ITID;
+  const unsigned lt = (1u << lane) - 1;
+  if (s.we - s.ws > 32u) { SSTAT(8, 1); w_rebuild(p, s); }
+  else w_tail_sort(p, s);
+  const uint32_t wh = s.wh, ws = s.ws, we = s.we;
+  SSTAT(15, we - ws);
+  const uint32_t k = we - ws;
+  const List W = w_list(p, s.inst, s.wbuf);
+  const Coef& K = s.coef;
+  // tail: one entry per lane, in u order; tcum = demand up to it in tail order
+  double tu = dinf();
+  uint32_t td = 0, tp = INVALID;
+  if ((uint32_t)lane < k) { tu = w_u(K, W.q[ws + lane]); td = W.dem[ws + lane]; tp = ws + lane; }
+  const unsigned long long tcum = wscan_add(td, lane);
+  const unsigned long long Bw = Bu - wR;
+  // ---- pass A: u_m, the first entry (in u order, main before tail on ties)
+  // whose cumulative W demand reaches Bw.  Cumulative demand strictly grows
+  // over entries with demand > 0, so m is the crossing entry of least sum.
+  unsigned long long mc = 0, best = ~0ull;
+  unsigned long long tres = 0;   // (tail lane) main demand ordered before it
+  bool tdone = false;
+  double carry = -dinf(), bu = 0.0;
+  auto tail_best = [&](bool all) -> unsigned long long {
+    const bool known = tdone || all;
+    const unsigned long long pre = tdone ? tres : mc;
+    return (known && tp != INVALID && td > 0 && pre + tcum >= Bw) ? pre + tcum : ~0ull;
+  };
+  for (uint32_t b = wh; b < ws; b += 32) {
+    const uint32_t i = b + lane;
+    QEnt x;
+    x.e = INVALID;
+    uint32_t d = 0;
+    if (i < ws) { x = W.q[i]; if (x.e != INVALID) d = W.dem[i]; }
+    const bool ok = x.e != INVALID;
+    const double u = ok ? w_u(K, x) : 0.0;
+    double um = wscan_max(ok ? u : (i < ws ? -dinf() : dinf()), lane);
+    um = um > carry ? um : carry;
+    carry = __shfl_sync(FULL, um, 31);
+    const unsigned long long incl = wscan_add(d, lane);
+    const int nlt = wcount<false>(tu, u);
+    const unsigned long long tl = __shfl_sync(FULL, tcum, nlt > 0 ? nlt - 1 : 0);
+    const unsigned long long cum = mc + incl + (nlt > 0 ? tl : 0ull);
+    const unsigned long long cand = (ok && d > 0 && cum >= Bw) ? cum : ~0ull;
+    const int cle = wcount<true>(um, tu);
+    const unsigned long long pre = __shfl_sync(FULL, incl, cle > 0 ? cle - 1 : 0);
+    if (!tdone && tp != INVALID && cle < 32) { tdone = true; tres = mc + (cle > 0 ? pre : 0ull); }
+    mc += __shfl_sync(FULL, incl, 31);
+    SSTAT(11, 1);
+    const unsigned long long tc = tail_best(false);
+    best = wmin_u64(cand < tc ? cand : tc);
+    if (best != ~0ull) {
+      const unsigned bl = __ballot_sync(FULL, cand == best || tc == best);
+      bu = __shfl_sync(FULL, cand == best ? u : tu, __ffs(bl) - 1);
+      break;
+    }
+  }
+  if (best == ~0ull) {   // main exhausted: the tail's remaining entries follow all of it
+    const unsigned long long tc = tail_best(true);
+    best = wmin_u64(tc);
+    if (best == ~0ull) { SSTAT(2, 1); return false; }   // not reachable: the W total reaches Bw
+    const unsigned bl = __ballot_sync(FULL, tc == best);
+    bu = __shfl_sync(FULL, tu, __ffs(bl) - 1);
+  }
+  const double X = fabs(bu) + 4.0 * fabs(dmul(K.alpha, dmul(u2d(t), K.Ts)));
+  // band scores beyond 2^120 could round to fp32 infinity (equal keys):
+  // non-finite or huge scores take the general path
+  if (!(X < 0x1p120)) { SSTAT(3, 1); return false; }
+  const double del2 = 2.0 * (X * 0x1p-19 + 0x1p-140);
+  const double lo = bu - del2, hi = bu + del2;
+  // ---- pass B: entries below the band are granted in full, the band's are
+  // candidates for k*; exact keys for both
+  uint32_t npop = 0, nband = 0;
+  unsigned long long bsum = 0;
+  bool over = false;
+  auto place = [&](bool ok, double u, const QEnt& x, uint32_t d, uint32_t pos) {
+    const bool below = ok && u < lo, band = ok && !below && u <= hi;
+    uint64_t key = 0;
+    if (below || band) key = order_key(x.e, rank_key(K, s.ip, x.V, t, x.last, x.e & 0xFFFF));
+    const unsigned mb = __ballot_sync(FULL, below), mn = __ballot_sync(FULL, band);
+    if (below) {
+      const uint32_t q = npop + __popc(mb & lt);
+      if (q < MAXPOP) { s.pk[q] = key; s.pw[q] = d; s.pp[q] = pos; }
+    }
+    if (band) {
+      const uint32_t q = nband + __popc(mn & lt);
+      if (q < SIM_CAND) { s.u.c.ck[0][q] = key; s.u.c.cw[0][q] = d; s.bpos[q] = pos; }
+    }
+    unsigned long long bs = below ? d : 0ull;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) bs += __shfl_xor_sync(FULL, bs, o);
+    bsum += bs;
+    npop += __popc(mb);
+    nband += __popc(mn);
+    if (npop > MAXPOP || nband > SIM_CAND) over = true;
+  };
+  {   // tail lanes (sorted or not, each lane classifies its own entry)
+    QEnt x;
+    x.e = INVALID;
+    if (tp != INVALID) x = W.q[tp];
+    place(tp != INVALID, tu, x, td, tp);
+  }
+  for (uint32_t b = wh; b < ws && !over; b += 32) {
+    const uint32_t i = b + lane;
+    QEnt x;
+    x.e = INVALID;
+    uint32_t d = 0;
+    if (i < ws) { x = W.q[i]; if (x.e != INVALID) d = W.dem[i]; }
+    const bool ok = x.e != INVALID;
+    const double u = ok ? w_u(K, x) : 0.0;
+    SSTAT(12, 1);
+    place(ok, u, x, d, i);
+    if (__any_sync(FULL, ok && u > hi)) break;   // sorted: everything after is above the band
+  }
+  if (over) { SSTAT(4, 1); return false; }
+  SSTAT(13, nband);
+  ISYNC();
+  rank_select<SIM_NT, SIM_CAND>(s.u.c, 0, s.res, (int)nband, Bu, wR + bsum);
+  if (!s.res.found) { SSTAT(5, 1); return false; }   // not reachable (k* lies in the band)
+  const uint64_t ks = s.res.k;
+  for (uint32_t a0 = 0; a0 < nband; a0 += 32) {
+    const uint32_t a = a0 + lane;
+    const bool g = a < nband && s.u.c.ck[0][a] <= ks;
+    const unsigned mg = __ballot_sync(FULL, g);
+    if (g) {
+      const uint32_t q = npop + __popc(mg & lt);
+      if (q < MAXPOP) { s.pk[q] = s.u.c.ck[0][a]; s.pw[q] = s.u.c.cw[0][a]; s.pp[q] = s.bpos[a]; }
+    }
+    npop += __popc(mg);
+  }
+  if (npop > MAXPOP) { SSTAT(6, 1); return false; }
+  SSTAT(1, 1);
+  SSTAT(14, npop);
+  ISYNC();
+  if (lane == 0) s.npop = npop;
+  ISYNC();
+  return true;
 }
 
 // Selections, kept out of line: one instantiation of each serves every call
@@ -395,7 +905,7 @@ __device__ bool inst_begin(const SimParams& p, SimShm& s, uint32_t inst) {
   ISYNC();
   Ctx c{p, s, s.coef, s.ip, a.rs + off,
         List{a.r_q + off, a.r_dem + off},
-        List{a.w_q + off, a.w_dem + off},
+        w_list(p, inst, s.wbuf),
         a.pz_id + off, a.ret + off, a.kscr + off, a.wscr + off, a.kscr2 + off, a.wscr2 + off, 0, 0, 0};
   c.trace = p.inst_trace[inst];
   c.r0 = p.tr.req_off[c.trace];
@@ -416,9 +926,13 @@ __device__ bool inst_begin(const SimParams& p, SimShm& s, uint32_t inst) {
       H.t = 0; H.A = 0; H.P = 0; H.min_ret = ~0ull; H.next_arr = 0; H.n_r = 0; H.n_w = 0; H.n_pz = 0;
       H.w2 = 0;
       H.n_fin = 0; H.started = 1;
+      H.wh = 0; H.ws = 0; H.we = 0; H.mh = 0; H.wbuf = 0; H.tclean = 1;
     }
     s.t = H.t; s.A = H.A; s.P = H.P; s.min_ret = H.min_ret; s.next_arr = H.next_arr;
     s.n_r = H.n_r; s.n_w = H.n_w; s.n_pz = H.n_pz; s.n_fin = H.n_fin; s.w2 = H.w2;
+    s.wh = H.wh; s.ws = H.ws; s.we = H.we; s.mh = H.mh; s.wbuf = H.wbuf; s.tclean = H.tclean;
+    s.sorted = SIM_SORTEDW && (s.ip.ranking == AUGSCHED_RANK_AUGSERVE ||
+                               s.ip.ranking == AUGSCHED_RANK_AUGSERVE_TI);
     s.nholes[0] = s.nholes[1] = 0;
     s.abort = 0;
     s.next_tick = s.next_arr < n ? p.tr.arr_tick[c.r0 + s.next_arr] : ~0ull;
@@ -448,7 +962,7 @@ __device__ bool inst_step(const SimParams& p, SimShm& s) {
   const Arena& a = p.ar;
   Ctx c{p, s, s.coef, s.ip, a.rs + off,
         List{a.r_q + off, a.r_dem + off},
-        List{a.w_q + off, a.w_dem + off},
+        w_list(p, inst, s.wbuf),
         a.pz_id + off, a.ret + off, a.kscr + off, a.wscr + off, a.kscr2 + off, a.wscr2 + off, 0, 0, 0};
   c.trace = s.trace;
   c.r0 = s.r0;
@@ -481,10 +995,11 @@ __device__ bool inst_step(const SimParams& p, SimShm& s) {
       const uint32_t j = s.next_arr + tid;
       const bool arrive = j < n && p.tr.arr_tick[c.r0 + j] <= tT;
       const int cnt = isync_count(arrive);
-      if (arrive) do_arrival(c, j, s.n_w + tid, t);
+      if (arrive) do_arrival(c, j, s.we + tid, t);   // W tail
       ISYNC();
       if (tid == 0) {
-        s.n_w += cnt; s.next_arr += cnt; s.cnt[AUGSCHED_R_ARRIVED] += cnt;
+        s.n_w += cnt; s.we += cnt; s.next_arr += cnt;
+        if (cnt) s.tclean = 0; s.cnt[AUGSCHED_R_ARRIVED] += cnt;
         if (cnt < SIM_NT) s.next_tick = s.next_arr < n ? p.tr.arr_tick[c.r0 + s.next_arr] : ~0ull;
       }
       ISYNC();
@@ -567,19 +1082,14 @@ __device__ bool inst_step(const SimParams& p, SimShm& s) {
     const unsigned long long w0 = s.tw[0], w1 = s.tw[1];
     int wmode = WMODE_NONE;
     SSTAT(18, 1);
-    SSTAT(30, nR);
-    SSTAT(31, nW);
     if (B <= 0) {
       if (tid == 0) { s.res.found = 1; s.res.k = 0; s.res.wbelow = 0; }  // nothing admitted
     } else if (w0 >= Bu) {
-      SSTAT(17, 1);
-      SSTAT(25, s.tc[0]);
-      if (s.tc[0] <= SIM_CAND) { SSTAT(23, 1); select_cand(s, 0, (int)s.tc[0], Bu, 0); }
-      else { SSTAT(24, 1); select_arr(s, c.K, c.Ws, nR, Bu, KBITS, false); }
+      if (s.tc[0] <= SIM_CAND) select_cand(s, 0, (int)s.tc[0], Bu, 0);
+      else select_arr(s, c.K, c.Ws, nR, Bu, KBITS, false);
     } else if (w0 + w1 >= Bu) {
-      SSTAT(22, 1);
-      if (s.tc[1] <= SIM_CAND) { SSTAT(23, 1); select_cand(s, 1, (int)s.tc[1], Bu, w0); }
-      else { SSTAT(24, 1); select_arr(s, c.K, c.Ws, nR, Bu, KBITS, false); }
+      if (s.tc[1] <= SIM_CAND) select_cand(s, 1, (int)s.tc[1], Bu, w0);
+      else select_arr(s, c.K, c.Ws, nR, Bu, KBITS, false);
     } else {
       // the prefix reaches W.  The W demand total is maintained
       // incrementally; when everything fits no W key is needed.
@@ -587,9 +1097,20 @@ __device__ bool inst_step(const SimParams& p, SimShm& s) {
       SSTAT(0, 1);
       if (wall < Bu) {
         SSTAT(16, 1);
+        if (s.wh != 0 || s.mh != 0) {   // the general paths address W densely
+          SSTAT(10, 1);
+          w_rebuild(p, s);
+          c.W = w_list(p, inst, s.wbuf);
+        }
         if (tid == 0) { s.res.found = 0; s.res.total = wall; }   // everything admitted
         wmode = WMODE_ALL;
+      } else if (s.sorted && w_sorted_select(p, s, t, Bu, w0 + w1)) {
+        c.W = w_list(p, inst, s.wbuf);
+        wmode = WMODE_POP;   // the prefix found near the head of the sorted W list
       } else {
+        SSTAT(20, 1);
+        if (s.wh != 0 || s.mh != 0) { SSTAT(10, 1); w_rebuild(p, s); }
+        c.W = w_list(p, inst, s.wbuf);
         // one pass over W: this lane's two smallest keys and their positions
         // (one 16-byte load per entry), then their demands
         uint64_t c1 = ~0ull, c2 = ~0ull;
@@ -642,9 +1163,7 @@ __device__ bool inst_step(const SimParams& p, SimShm& s) {
           }
           if (bk == ~0ull) break;  // not reachable: the W total reaches B
           if (tid == 0) { s.pk[r] = bk; s.pw[r] = bw; s.pp[r] = bp; }
-          SSTAT(27, 1);
           if (wb + bw >= Bu) {
-            SSTAT(26, 1);
             if (tid == 0) { s.res.found = 1; s.res.k = bk; s.res.wbelow = wb; s.npop = r + 1; }
             wmode = WMODE_POP;
             break;
@@ -653,7 +1172,6 @@ __device__ bool inst_step(const SimParams& p, SimShm& s) {
           if (myk == bk) {
             if (++cons == 1) { myk = c2; myw = cw2; myp = cp2; }
             else {
-              SSTAT(28, 1);
               uint64_t nk = ~0ull;
               uint32_t nw = 0, np = 0;
               for (uint32_t i = tid; i < nW; i += SIM_NT) {
@@ -665,7 +1183,6 @@ __device__ bool inst_step(const SimParams& p, SimShm& s) {
           }
         }
         if (wmode != WMODE_POP) {
-          SSTAT(20, 1);
           // many small W demands: materialise every key and radix-select
           for (uint32_t i = tid; i < nW; i += SIM_NT) {
             c.K[nR + i] = w_order_key(s, c.W.q, i, t);
@@ -698,7 +1215,6 @@ __device__ bool inst_step(const SimParams& p, SimShm& s) {
   phase_bar<2>(nb);
   // ---- S8 memory resolution (R20) -------------------------------------------
   if (need > freev) {
-    SSTAT(29, 1);
     // (1) demote Preserve-paused contexts, kv desc, id asc
     const uint64_t D0 = (uint64_t)(need - freev);
     const uint32_t npz = s.n_pz;
@@ -798,7 +1314,9 @@ __device__ bool inst_step(const SimParams& p, SimShm& s) {
           r.meta = meta_with(r.meta, ST_WAIT, meta_pol(r.meta));
           c.rs[id] = r;
           const uint32_t nd = demand_of(r.ctx, 0, 0, r.pend, p.cfg.s_in);
-          c.W.put(atomicAdd(&s.n_w, 1u), id | (2u << 30), x.V, x.last, nd);
+          c.W.put(atomicAdd(&s.we, 1u), id | (2u << 30), x.V, x.last, nd);   // W tail
+          atomicAdd(&s.n_w, 1u);
+          s.tclean = 0;
           atomicAdd(&s.w2, (unsigned long long)nd);
           c.R.q[v].e = INVALID;
           c.K[v] |= KEVICT;
@@ -952,7 +1470,7 @@ __device__ bool inst_step(const SimParams& p, SimShm& s) {
   phase_bar<3>(nb);
   PT(7);
   compact_list(s, c.R, 0, s.n_r);  // syncs
-  compact_list(s, c.W, 1, s.n_w);
+  w_compact(p, s);
   if (tid == 0) {
     if (s.A < 0 || s.P < 0 || s.A + s.P > cap) s.cnt[AUGSCHED_R_ERR] |= 1;
 #ifdef AUGSCHED_DEBUG
@@ -990,6 +1508,7 @@ __device__ void inst_end(const SimParams& p, SimShm& s) {
   if (tid == 0) {
     H.t = s.t; H.A = s.A; H.P = s.P; H.min_ret = s.min_ret; H.next_arr = s.next_arr;
     H.n_r = s.n_r; H.n_w = s.n_w; H.n_pz = s.n_pz; H.n_fin = s.n_fin; H.w2 = s.w2;
+    H.wh = s.wh; H.ws = s.ws; H.we = s.we; H.mh = s.mh; H.wbuf = s.wbuf; H.tclean = s.tclean;
     s.cnt[AUGSCHED_R_FINAL_T] = s.t;
     s.cnt[AUGSCHED_R_INCOMPLETE] = s.n - s.n_fin;   // R28
   }
@@ -1025,7 +1544,7 @@ __global__ void __launch_bounds__(SIM_NT * SIM_WPC, (SIM_MINB / SIM_WPC > 0 ? SI
       if (!__syncthreads_or(active)) return;
 #ifdef AUGSCHED_SIM_STATS
       // per CTA iteration: the phase times of the slowest full step and the
-      // sums over the CTA's full steps
+      // sums over the CTA's full steps (sim_stats.py)
       if (threadIdx.x == 0) {
         SimShm* a = reinterpret_cast<SimShm*>(smem_raw);
         long long best = -1, d[6], bd[6] = {0, 0, 0, 0, 0, 0}, sd[6] = {0, 0, 0, 0, 0, 0};
@@ -1049,6 +1568,7 @@ __global__ void __launch_bounds__(SIM_NT * SIM_WPC, (SIM_MINB / SIM_WPC > 0 ? SI
           atomicAdd(&g_sim_stats[46], (unsigned long long)nf);
           atomicAdd(&g_sim_stats[47], 1ull);
         }
+        static_assert(SIM_WPC <= 32, "stats scan");
       }
       __syncthreads();
 #endif
