@@ -181,7 +181,7 @@ int augsched_create(const augsched_config* cfg, const augsched_instance_params* 
   if (rc) return rc;
   std::vector<augsched_instance_params> ip(n_instances);
   uint32_t max_limit = 0;
-  bool any_random = false, all_ti = true;
+  bool any_random = false, all_ti = true, all_vi = true;
   for (uint32_t i = 0; i < n_instances; ++i) {
     ip[i] = per_inst ? per_inst[i] : cfg->defaults;
     if ((rc = validate_params(ip[i], i))) return rc;
@@ -191,6 +191,7 @@ int augsched_create(const augsched_config* cfg, const augsched_instance_params* 
     max_limit = lim > max_limit ? lim : max_limit;
     any_random = any_random || ip[i].ranking == AUGSCHED_RANK_RANDOM;
     all_ti = all_ti && ip[i].ranking == AUGSCHED_RANK_AUGSERVE_TI;
+    all_vi = all_vi && (ip[i].ranking == AUGSCHED_RANK_AUGSERVE || ip[i].ranking == AUGSCHED_RANK_FCFS);
   }
   int ndev = 0;
   CUDA_TRY(cudaGetDeviceCount(&ndev));
@@ -204,6 +205,9 @@ int augsched_create(const augsched_config* cfg, const augsched_instance_params* 
   h->st.max_limit = max_limit;
   h->st.pf_spec = !any_random;   // a fresh shuffle every iteration leaves no anchor
   h->st.ti = all_ti && n_instances == 1;   // incremental full order (reading B12, f1)
+#ifndef AUGSCHED_NO_VI
+  h->st.vi = all_vi && n_instances == 1;   // the same for R3 / FCFS keys, order checked every step
+#endif
   h->device = device;
   h->stream = reinterpret_cast<cudaStream_t>(cuda_stream);
   h->cap = (int64_t)((cfg->g_total - (cfg->g_model + cfg->g_runtime + cfg->g_safety)) /

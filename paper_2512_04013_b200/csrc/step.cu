@@ -2047,8 +2047,9 @@ struct CoopArgs {
   long long* budget;
   uint32_t *n_active, *tier_off, *order, *keyout, *grant, *admitted, *gslot;
   // time-invariant keys (reading B12): the previous order's words and the
-  // output of this one; ti_try: merge the changed slots into tiw_in
-  int ti, ti_try;
+  // output of this one; ti_try: merge the changed slots into tiw_in.
+  // vi: the same for R3 / FCFS keys (words recomputed, order checked)
+  int ti, ti_try, vi;
   const unsigned long long* tiw_in;
   unsigned long long *tiw_out, *ubuf;
   const uint32_t* ti_n_in;
@@ -2153,7 +2154,16 @@ __device__ __forceinline__ uint32_t lower_bound_sm(const unsigned long long* v, 
   return lo;
 }
 
-__device__ void ti_incremental(const CoopArgs& a, unsigned long long* sbuf, unsigned long long* xch, SelShm& sel,
+// vi (R3 / FCFS keys): every key moves with time, so an unchanged slot's
+// word is read from kA (this step's words by slot, written by the caller's
+// K phase) and the unchanged words, taken in the previous order, must still
+// be strictly increasing; each CTA checks its chunk, then every CTA checks
+// the chunk boundaries.  When they are not (fp32 rounding re-ordered two
+// waiting requests), it returns false before writing any output and the
+// caller sorts.  Under R3 every waiting score moves by the same alpha*T per
+// step, so this is rare.
+template <bool vi>
+__device__ bool ti_incremental(const CoopArgs& a, unsigned long long* sbuf, unsigned long long* xch, SelShm& sel,
                                unsigned long long* wsum, unsigned long long& freed, long long& B_s, uint32_t& nbar) {
   __shared__ uint32_t cnt_s[4], dn_s, base_s2, nu_s;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -2172,9 +2182,16 @@ __device__ void ti_incremental(const CoopArgs& a, unsigned long long* sbuf, unsi
   // (element c0 + warp * 256 + e * 32 + lane, e < 8)
   constexpr int TE = 8;
   const bool reg = c1 - c0 <= (uint32_t)CNT * TE;
+  // vi checks the order on chunks held in registers (the host enables it
+  // only for queues whose chunks fit; a looping chunk falls back here)
+  if (vi && chunk > (uint32_t)CNT * TE) return false;
   unsigned long long rw[TE];
   unsigned rb[TE];          // per e: the warp's ballot of unchanged words
-  uint32_t* pub = a.hist;   // [G][4]: kept words, and their tiers 0..2
+  uint32_t* pub = a.hist;   // [G][4]: kept words, their tiers 0..2, (vi) chunk out of order
+  // vi: [G][2] first and last unchanged word of each chunk
+  unsigned long long* pv = reinterpret_cast<unsigned long long*>(a.hist + ((4 * G + 1) & ~1u));
+  __shared__ unsigned long long vfl[2 * CNW];   // vi: per warp first / last unchanged word
+  __shared__ uint32_t vbad;
 #ifdef AUGSCHED_COOP_TIMING
 #ifndef TT_CTA
 #define TT_CTA 0
@@ -2188,7 +2205,7 @@ __device__ void ti_incremental(const CoopArgs& a, unsigned long long* sbuf, unsi
   // ---- A: count the unchanged words of the chunk (and their tiers); CTA 0
   // builds D (the changed slots' current words, queued ones only), sorted
   if (tid < 4) cnt_s[tid] = 0;
-  if (tid == 0) dn_s = 0;
+  if (tid == 0) { dn_s = 0; vbad = 0; }
   __syncthreads();
   {
     uint32_t kc = 0, t0 = 0, t1 = 0;
@@ -2205,6 +2222,13 @@ __device__ void ti_incremental(const CoopArgs& a, unsigned long long* sbuf, unsi
         const uint32_t i = seg + e * 32 + lane;
         dm[e] = i < c1 ? __ldcg(&S.dmark[(uint32_t)rw[e] & SLOT_MASK]) : E;
       }
+      if (vi) {   // this step's word of every unchanged slot
+#pragma unroll
+        for (int e = 0; e < TE; ++e)
+          if (dm[e] != E) rw[e] = __ldcg(&a.kA[(uint32_t)rw[e] & SLOT_MASK]);
+      }
+      unsigned long long prev = 0, first = ~0ull;   // vi: last unchanged word so far in this warp's segment
+      bool bad = false;
 #pragma unroll
       for (int e = 0; e < TE; ++e) {
         const bool keep = dm[e] != E;
@@ -2214,6 +2238,21 @@ __device__ void ti_incremental(const CoopArgs& a, unsigned long long* sbuf, unsi
           const uint32_t t = (uint32_t)(rw[e] >> PK_TIER);
           t0 += t == 0; t1 += t == 1;
         }
+        if (vi && rb[e]) {
+          // the unchanged word before each one in order: the nearest lower
+          // unchanged lane, else the previous rounds' last
+          const unsigned below = rb[e] & ((1u << lane) - 1);
+          const int src = below ? 31 - __clz(below) : lane;
+          const unsigned long long pw = __shfl_sync(FULL, rw[e], src);
+          if (keep) bad |= (below ? pw : prev) >= rw[e] && (below || prev != 0);
+          const int lastl = 31 - __clz(rb[e]), firstl = __ffs(rb[e]) - 1;
+          if (first == ~0ull) first = __shfl_sync(FULL, rw[e], firstl);
+          prev = __shfl_sync(FULL, rw[e], lastl);
+        }
+      }
+      if (vi) {
+        if (__any_sync(FULL, bad) && lane == 0) vbad = 1;
+        if (lane == 0) { vfl[2 * warp] = first; vfl[2 * warp + 1] = prev; }
       }
     } else {
       for (uint32_t i = c0 + tid; i < c1; i += CNT) {
@@ -2283,9 +2322,60 @@ __device__ void ti_incremental(const CoopArgs& a, unsigned long long* sbuf, unsi
   }
   __syncthreads();
   if (tid < 3) pub[c * 4 + tid] = cnt_s[tid];
+  if (vi && tid == 0) {   // the chunk's warps in order: increasing across warp boundaries too
+    unsigned long long f = ~0ull, l = 0;
+    uint32_t bad = vbad;
+    for (int w2 = 0; w2 < CNW; ++w2) {
+      const unsigned long long wf = vfl[2 * w2], wl = vfl[2 * w2 + 1];
+      if (wf == ~0ull) continue;
+      if (l != 0 && wf <= l) bad = 1;
+      if (f == ~0ull) f = wf;
+      l = wl;
+    }
+    if (c == 0) { f = ~0ull; l = 0; }   // CTA 0 takes no chunk (it builds D)
+    pub[c * 4 + 3] = bad;
+    pv[2 * c] = f;
+    pv[2 * c + 1] = l;
+  }
   TT(1);
   coop_barrier(a, nbar);
   TT(2);
+  if (vi) {
+    // every CTA: the chunks' unchanged words must increase across chunks
+    __shared__ int vok;
+    if (tid < 32) {
+      unsigned long long f[8], l[8];
+      uint32_t bad = 0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const uint32_t cc = lane * 8 + q;
+        f[q] = ~0ull; l[q] = 0;
+        if (cc < G) { f[q] = __ldcg(&pv[2 * cc]); l[q] = __ldcg(&pv[2 * cc + 1]); bad |= __ldcg(&pub[cc * 4 + 3]); }
+      }
+      unsigned long long lf = ~0ull, ll = 0;   // this lane's 8 chunks, in order
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        if (f[q] == ~0ull) continue;
+        if (ll != 0 && f[q] <= ll) bad = 1;
+        if (lf == ~0ull) lf = f[q];
+        ll = l[q];
+      }
+      // the last word of the lanes before this one (words increase if all is well: a max scan)
+      unsigned long long m = ll;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long y = __shfl_up_sync(FULL, m, o);
+        if (lane >= o && y > m) m = y;
+      }
+      unsigned long long ex = __shfl_up_sync(FULL, m, 1);
+      if (lane == 0) ex = 0;
+      if (lf != ~0ull && ex != 0 && lf <= ex) bad = 1;
+      const bool any_bad = __any_sync(FULL, bad != 0);
+      if (lane == 0) vok = any_bad ? 0 : 1;
+    }
+    __syncthreads();
+    if (!vok) return false;   // uniform: every CTA read the same summaries
+  }
   // ---- B: compact the unchanged words (stable) into ubuf and place them
   const uint32_t nd = __ldcg(&a.ti_misc[0]);
   for (uint32_t j = tid; j < nd; j += CNT) sbuf[j] = __ldcg(&a.kB[j]);
@@ -2461,12 +2551,12 @@ __device__ void ti_incremental(const CoopArgs& a, unsigned long long* sbuf, unsi
     printf("ti_t cta %u ns: nd %u | %llu %llu %llu %llu %llu %llu\n", c, nd, tt[1] - tt[0], tt[2] - tt[0],
            tt[3] - tt[0], tt[4] - tt[0], tt[5] - tt[0], tt[6] - tt[0]);
 #endif
-  if (c != 0) return;
+  if (c != 0) return true;
   for (uint32_t j = tid; j <= nd; j += CNT) a.gcnt[j] = 0;   // clear for the next step
   // ---- F: admission over the first min(B, n) positions (CTA 0)
   const uint32_t n = __ldcg(&a.n_active[0]);
   const long long B = B_s;
-  if (a.offer) { pack_offer(a, a.tiw_out, n, B); return; }
+  if (a.offer) { pack_offer(a, a.tiw_out, n, B); return true; }
   const uint32_t target = pf_target(B, n);
   for (uint32_t i = tid; i < target; i += CNT) sbuf[i] = __ldcg(&a.tiw_out[i]);
   const uint32_t prev = S.gdirty[0];
@@ -2483,8 +2573,13 @@ __device__ void ti_incremental(const CoopArgs& a, unsigned long long* sbuf, unsi
                        tt[3] - tt[0], tt[4] - tt[0], tt[5] - tt[0], tt[6] - tt[0], tt[7] - tt[0]);
 #endif
 #undef TT
+  return true;
 }
 
+// VI: the instantiation for value (R3) / FCFS keys (K phase first, then the
+// checked merge or the sort); the other one serves time-invariant keys and
+// handles without a kept order.
+template <bool VI>
 __global__ void __launch_bounds__(CNT, 1) full_coop_kernel(const __grid_constant__ CoopArgs a) {
   extern __shared__ __align__(16) unsigned long long fc_sm[];
   unsigned long long* sbuf = fc_sm;                                            // [PF_SCAP] (phase F)
@@ -2505,10 +2600,12 @@ __global__ void __launch_bounds__(CNT, 1) full_coop_kernel(const __grid_constant
   const uint32_t c0 = c * chunk < N ? c * chunk : N;
   const uint32_t c1 = c0 + chunk < N ? c0 + chunk : N;
   uint32_t nbar = 0;
-  if (a.ti_try && __ldcg(&S.dcnt[S.ti_ep & 1]) <= TI_DCAP) {   // uniform: the list is final at launch
-    ti_incremental(a, sbuf, reinterpret_cast<unsigned long long*>(wcnt), sel, wsum, freed, B_s, nbar);
+  const bool inc = a.ti_try && __ldcg(&S.dcnt[S.ti_ep & 1]) <= TI_DCAP;   // uniform: the list is final at launch
+  if (!VI && inc && a.ti) {
+    ti_incremental<false>(a, sbuf, reinterpret_cast<unsigned long long*>(wcnt), sel, wsum, freed, B_s, nbar);
     return;
   }
+  const bool vi = VI && inc && a.vi;   // R3 / FCFS: the words first (K), then the merge or, failing that, the sort
 #ifdef AUGSCHED_COOP_TIMING
   unsigned long long ct[32];
 #endif
@@ -2516,7 +2613,7 @@ __global__ void __launch_bounds__(CNT, 1) full_coop_kernel(const __grid_constant
   // A chunk that fits one sub-tile stays in registers between the phases
   // (xr, element i = c0 + warp * 256 + e * 32 + lane, the ranking order):
   // the words are not written by K, and each pass's input is read once.
-  const bool reg = c1 - c0 <= CSUB;
+  const bool reg = c1 - c0 <= CSUB && !vi;   // vi gathers this step's words from kA
   unsigned long long xr[CEPT];
   // ---- K: words of the chunk + histogram of pass 0
   {
@@ -2548,6 +2645,12 @@ __global__ void __launch_bounds__(CNT, 1) full_coop_kernel(const __grid_constant
                      : token_limit(a.cfg, k, ip, a.cap, ld_ll(&S.A[0]), ld_ll(&S.P[0]));
       a.budget[0] = B_s;
     }
+  }
+  if (vi) {
+    coop_barrier(a, nbar);   // kA complete
+    if (ti_incremental<VI>(a, sbuf, reinterpret_cast<unsigned long long*>(wcnt), sel, wsum, freed, B_s, nbar))
+      return;
+    // out of order: sort (kA and the pass-0 histogram h are intact)
   }
   unsigned long long* src = a.kA;
   unsigned long long* dst = a.kB;
@@ -2611,7 +2714,7 @@ __global__ void __launch_bounds__(CNT, 1) full_coop_kernel(const __grid_constant
       for (int d = 0; d < NB; ++d) tc[d >> 6] += tot_s[d];
       const uint32_t n = tc[0] + tc[1] + tc[2];
       a.n_active[0] = n;
-      if (a.ti) *a.ti_n_out = n;
+      if (a.ti || a.vi) *a.ti_n_out = n;
       a.tier_off[0] = 0;
       a.tier_off[1] = tc[0];
       a.tier_off[2] = tc[0] + tc[1];
@@ -2663,7 +2766,7 @@ __global__ void __launch_bounds__(CNT, 1) full_coop_kernel(const __grid_constant
           a.order[pos] = x;
           a.keyout[pos] = (uint32_t)(xv[e] >> PK_KEY);
           if (pos < PF_SCAP) a.kpre[pos] = xv[e];
-          if (a.ti) a.tiw_out[pos] = xv[e];   // the order the next step merges into
+          if (a.ti || a.vi) a.tiw_out[pos] = xv[e];   // the order the next step merges into
           if (pos < a.max_limit) {   // the admission (phase F) reads these slots' token state
             prefetch_l2(&S.ctx[x]); prefetch_l2(&S.kv[x]); prefetch_l2(&S.cpu[x]); prefetch_l2(&S.pend[x]);
           }
@@ -3116,7 +3219,8 @@ int grow_records(StepState& st, uint32_t need, cudaStream_t s) {
 Slots slots_of(StepState& st, const augsched_instance_params* d_ip, uint32_t* d_err) {
   return Slots{st.st, st.V, st.last, st.ctx, st.kv, st.cpu, st.pend, st.A, st.P, st.Aevt, st.Asnap,
                st.coef, d_ip, st.max_active, st.wkv, st.claimA, st.claimB, st.rec_batch, st.gdirty, d_err,
-               (st.ti || st.minc) ? st.dmark : nullptr, st.ti ? st.dlist : nullptr, st.dcnt, st.ti_ep};
+               (st.ti || st.vi || st.minc) ? st.dmark : nullptr, (st.ti || st.vi) ? st.dlist : nullptr, st.dcnt,
+               st.ti_ep};
 }
 
 }  // namespace
@@ -3242,14 +3346,21 @@ int step_ensure(StepState& st, uint32_t n_inst, uint32_t max_active, cudaStream_
   }
   cudaFuncSetAttribute(pf_multi_kernel<256, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PF_MULTI_SMEM);
   if (n_inst == 1) {
-    cudaFuncSetAttribute(full_coop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)coop_smem_bytes());
-    int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, full_coop_kernel, CNT, coop_smem_bytes());
+    cudaFuncSetAttribute(full_coop_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)coop_smem_bytes());
+    cudaFuncSetAttribute(full_coop_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)coop_smem_bytes());
+    int occ = 0, occ_vi = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, full_coop_kernel<false>, CNT, coop_smem_bytes());
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_vi, full_coop_kernel<true>, CNT, coop_smem_bytes());
+    if (occ_vi < 1) st.vi = false;
+    // vi checks the order on chunks of <= 8,192 words held in registers (one
+    // per CTA but CTA 0): larger queues sort with the plain kernel, whose
+    // sort is faster there than a looping merge (measured at 4M / 16M)
+    if (N > (size_t)(st.sms - 1) * 8192) st.vi = false;
     st.coop_grid = occ >= 1 ? st.sms : 0;   // one CTA per SM
     st.coop_bar_base = 0;
     if (st.sms < 128 || st.sms > 256) st.coop_grid = 0;   // column scan: <= 4 digits per CTA, one CTA per thread of a 256-thread group
     if (st.coop_grid > 0 && (rc = salloc(st, &st.coop_hist, 4 * ((size_t)st.coop_grid + 1) * CNB))) return rc;
-    if (st.ti && st.coop_grid > 0) {
+    if ((st.ti || st.vi) && st.coop_grid > 0) {
       if ((rc = salloc(st, &st.tiw, N)) || (rc = salloc(st, &st.tiw2, N)) || (rc = salloc(st, &st.ubuf, N)) ||
           (rc = salloc(st, &st.ti_n, 2)) || (rc = salloc(st, &st.dmark, N)) ||
           (rc = salloc(st, &st.dlist, 2 * (size_t)TI_DCAP)) || (rc = salloc(st, &st.dcnt, 2)) ||
@@ -3263,6 +3374,7 @@ int step_ensure(StepState& st, uint32_t n_inst, uint32_t max_active, cudaStream_
         return rc;
     } else {
       st.ti = false;
+      st.vi = false;
     }
   }
   // batched full step: each instance's order is kept for the next step, which
@@ -3349,10 +3461,10 @@ void run_records(StepState& st, Slots S, uint32_t* d_err, uint64_t now, cudaStre
 // Time-invariant handles: the step epoch of the dirty marks, and the clear
 // of the consumed list after the step's kernels.
 static void ti_begin(StepState& st) {
-  if (st.ti || st.minc) ++st.ti_ep;
+  if (st.ti || st.vi || st.minc) ++st.ti_ep;
 }
 static int ti_end(StepState& st, cudaStream_t s) {
-  if (!st.ti) return AUGSCHED_OK;
+  if (!st.ti && !st.vi) return AUGSCHED_OK;
   return cuda_check(cudaMemsetAsync(st.dcnt + (st.ti_ep & 1), 0, sizeof(uint32_t), s), "step: clear");
 }
 
@@ -3369,6 +3481,10 @@ int step_run_prefix(StepState& st, const augsched_config& cfg, int64_t cap,
     return step_run(st, cfg, cap, d_ip, d_err, now, out, s, launches);
   ti_begin(st);
   Slots S = slots_of(st, d_ip, d_err);
+  // a prefix step leaves no full order, so the next full step sorts: no
+  // change of this step needs a dirty mark
+  S.dmark = nullptr;
+  S.dlist = nullptr;
   run_records(st, S, d_err, now, s, launches);
   st.ti_valid = false;   // no full order: the next full step sorts
   if (st.n_inst > 1) {
@@ -3460,17 +3576,20 @@ int step_run(StepState& st, const augsched_config& cfg, int64_t cap,
     ca.keyout = st.key; ca.grant = st.grant; ca.admitted = st.admitted; ca.gslot = st.gslot;
     const uint32_t cur = st.ti_ep & 1;
     ca.ti = st.ti ? 1 : 0;
-    ca.ti_try = st.ti && st.ti_valid ? 1 : 0;
+    ca.vi = st.vi ? 1 : 0;
+    ca.ti_try = (st.ti || st.vi) && st.ti_valid ? 1 : 0;
     ca.tiw_in = st.tiw; ca.tiw_out = st.tiw2; ca.ubuf = st.ubuf;
     ca.ti_n_in = st.ti_n ? st.ti_n + (cur ^ 1) : nullptr;
     ca.ti_n_out = st.ti_n ? st.ti_n + cur : nullptr;
     ca.ti_misc = st.ti_misc;
     ca.gcnt = st.ti_gcnt;
     void* args[] = {&ca};
-    cudaError_t e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(&full_coop_kernel), st.coop_grid,
+    const void* kfn = st.vi ? reinterpret_cast<const void*>(&full_coop_kernel<true>)
+                            : reinterpret_cast<const void*>(&full_coop_kernel<false>);
+    cudaError_t e = cudaLaunchCooperativeKernel(kfn, st.coop_grid,
                                                 CNT, args, coop_smem_bytes(), s);
     if (e != cudaSuccess) return cuda_check(e, "step: cooperative launch");
-    if (st.ti) {   // the sorted words of this order are the next step's input
+    if (st.ti || st.vi) {   // the sorted words of this order are the next step's input
       std::swap(st.tiw, st.tiw2);
       st.ti_valid = true;
       int rc2 = ti_end(st, s);
@@ -3616,7 +3735,8 @@ int step_shard_offer(StepState& st, const augsched_config& cfg, int64_t cap, con
   ca.keyout = st.key; ca.grant = st.grant; ca.admitted = st.admitted; ca.gslot = st.gslot;
   const uint32_t cur = st.ti_ep & 1;
   ca.ti = st.ti ? 1 : 0;
-  ca.ti_try = st.ti && st.ti_valid ? 1 : 0;
+  ca.vi = st.vi ? 1 : 0;
+  ca.ti_try = (st.ti || st.vi) && st.ti_valid ? 1 : 0;
   ca.tiw_in = st.tiw; ca.tiw_out = st.tiw2; ca.ubuf = st.ubuf;
   ca.ti_n_in = st.ti_n ? st.ti_n + (cur ^ 1) : nullptr;
   ca.ti_n_out = st.ti_n ? st.ti_n + cur : nullptr;
@@ -3627,14 +3747,16 @@ int step_shard_offer(StepState& st, const augsched_config& cfg, int64_t cap, con
   ca.offer = static_cast<unsigned char*>(offer);
   ca.ocap = ocap;
   void* args[] = {&ca};
-  cudaError_t e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(&full_coop_kernel), st.coop_grid,
+  const void* kfn = st.vi ? reinterpret_cast<const void*>(&full_coop_kernel<true>)
+                          : reinterpret_cast<const void*>(&full_coop_kernel<false>);
+  cudaError_t e = cudaLaunchCooperativeKernel(kfn, st.coop_grid,
                                               CNT, args, coop_smem_bytes(), s);
   if (e != cudaSuccess) return cuda_check(e, "shard_offer: cooperative launch");
   st.coop_bar_base += 12ull * (unsigned long long)st.coop_grid;
   shard_holders_kernel<<<(uint32_t)((st.N + 255) / 256), 256, 0, s>>>(S, st.shard_now, (uint32_t)st.N,
                                                                        static_cast<unsigned char*>(offer), ocap);
   *launches += 2;
-  if (st.ti) {
+  if (st.ti || st.vi) {
     std::swap(st.tiw, st.tiw2);
     st.ti_valid = true;
     if ((rc = ti_end(st, s))) return rc;

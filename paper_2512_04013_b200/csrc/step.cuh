@@ -99,6 +99,7 @@ struct StepState {
   // time-invariant keys (ranking 3, one instance): the order is kept across
   // steps; a step merges the slots changed since the last one into it
   bool ti = false;
+  bool vi = false;                // the same for value (R3) / FCFS keys: words recomputed, order checked
   bool ti_valid = false;          // tiw holds the previous full step's sorted words
   uint32_t ti_ep = 0;             // step epoch (dirty marks)
   unsigned long long *tiw = nullptr, *tiw2 = nullptr;   // [N] sorted words (current, next)
