@@ -265,7 +265,9 @@ def step_bench(args, dev, stream, peak, prefix=False, n_override=None, ranking=0
             "one CTA sorts and admits the candidates)" if prefix else
             "augsched_step, time-invariant keys (ranking 3, reading B12): one cooperative kernel merges the "
             "slots changed since the last step into the previous order, then admits" if ranking == 3 else
-            "augsched_step: one cooperative kernel (keys, 4 stable LSD passes with grid barriers, admission)")
+            "augsched_step: one cooperative kernel (keys; the previous order minus the slots changed since, "
+            "checked to still increase, merged with the sorted changed slots -- the 4-pass stable LSD sort "
+            "with grid barriers on the first step or when fp32 rounding re-ordered; admission)")
     traffic = None
     try:   # ncu DRAM bytes per steady launch of the same command (profiles/step_*_traffic.json)
         tj = json.load(open(os.path.join(ROOT, "profiles", "step_prefix_traffic.json" if prefix
@@ -317,8 +319,9 @@ def step_multi_bench(args, dev, stream, peak, n_inst=4096, ma=2048):
             "value": n / (m / 1e3), "unit": UNIT, "ms_per_step_cold_l2": m,
             "roofline_frac": round(32.0 * n / (m / 1e3) / 1e9 / peak, 4),
             "kernel": ("pf_multi_kernel: one CTA per instance, anchored filter or radix select, sort, admission"
-                       if prefix else "full_multi_kernel: one CTA per instance, shared-memory stable LSD sort "
-                                      "of all slots, admission over the sorted words")}
+                       if prefix else "full_multi_kernel: one CTA per instance; the previous order minus the changed "
+                                      "and out-of-place words merged with the rest, sorted in shared memory "
+                                      "(stable LSD sort of all slots when the rest exceeds 1,024); admission")}
     return res
 
 
