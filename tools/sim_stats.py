@@ -18,7 +18,7 @@ import paper_2512_04013_b200 as aug  # noqa: E402
 NAMES = {0: "steps reaching W (wall >= B)", 16: "  everything fits (WMODE_ALL)", 26: "  W pop rounds ended",
          20: "  W radix fallback", 27: "  W pop rounds", 28: "  W rescans", 17: "prefix ends in running tier",
          22: "prefix ends in swapped tier", 23: "select_cand (R)", 24: "select_arr (R)", 25: "tier-0 candidates",
-         29: "memory resolution", 18: "busy steps", 30: "R entries", 31: "W entries"}
+         29: "memory resolution", 2: "  resolution with P == 0", 3: "  paused entries scanned", 4: "  eviction needed after demotion", 18: "busy steps", 30: "R entries", 31: "W entries"}
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--instances", type=int, default=65536)
