@@ -466,15 +466,23 @@ __device__ bool inst_step(const SimParams& p, SimShm& s) {
     // ---- S2 returns --------------------------------------------------------
     if (tT >= s.min_ret) {
       const uint32_t npz = s.n_pz;
+      unsigned long long mr = ~0ull;   // the next return among the calls still out
       for (uint32_t i = tid; i < npz; i += SIM_NT) {
         const uint32_t id = c.pz_id[i];
-        if (c.ret[id] <= tT) { do_return(c, id); c.pz_id[i] = INVALID; }
+        const uint64_t rt = c.ret[id];
+        if (rt <= tT) { do_return(c, id); c.pz_id[i] = INVALID; }
+        else mr = rt < mr ? rt : mr;
       }
-      compact_paused(c);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long y = __shfl_xor_sync(FULL, mr, o);
+        mr = y < mr ? y : mr;
+      }
+      ISYNC();   // every lane has read min_ret
       if (tid == 0) s.min_ret = ~0ull;
       ISYNC();
-      for (uint32_t i = tid; i < s.n_pz; i += SIM_NT) atomicMin(&s.min_ret, (unsigned long long)c.ret[c.pz_id[i]]);
-      ISYNC();
+      if ((tid & 31) == 0) atomicMin(&s.min_ret, mr);
+      compact_paused(c);   // syncs
     }
     // ---- S3 arrivals (ticks are sorted: the arrivals are a prefix) ----------
     if (tT >= s.next_tick) for (;;) {
