@@ -19,6 +19,12 @@
 namespace augsched {
 
 constexpr int MAXPOP = 32;   // pop rounds before falling back to a radix select over W
+#ifndef AUGSCHED_SIM_WPREFETCH
+#define AUGSCHED_SIM_WPREFETCH 1
+#endif
+#ifndef AUGSCHED_SIM_RKSPEC
+#define AUGSCHED_SIM_RKSPEC 1
+#endif
 
 #ifdef AUGSCHED_SIM_STATS
 // Path counters and phase clocks of the stats build (tools/sim_stats.py).
@@ -598,30 +604,55 @@ __device__ bool inst_step(const SimParams& p, SimShm& s) {
         if (tid == 0) { s.res.found = 0; s.res.total = wall; }   // everything admitted
         wmode = WMODE_ALL;
       } else {
+#if AUGSCHED_SIM_WPREFETCH
+        // the W list's lines to L2 first (non-blocking), so the scan's rounds
+        // of dependent loads after the first find them on chip
+        {
+          const uint32_t nb = nW * (uint32_t)sizeof(QEnt);
+          const char* wb = reinterpret_cast<const char*>(c.W.q);
+          for (uint32_t o = (uint32_t)tid * 128u; o < nb; o += 128u * SIM_NT)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(wb + o));
+        }
+#endif
         // one pass over W: this lane's two smallest keys and their positions
         // (one 16-byte load per entry), then their demands
         uint64_t c1 = ~0ull, c2 = ~0ull;
         uint32_t cp1 = 0, cp2 = 0;
         constexpr int U = SIM_UNROLL;  // entries in flight per thread (independent L2 loads)
-        for (uint32_t b0 = 0; b0 < nW; b0 += SIM_NT * U) {
-          QEnt x[U];
+        auto wscan = [&](auto keyf) {
+          for (uint32_t b0 = 0; b0 < nW; b0 += SIM_NT * U) {
+            QEnt x[U];
 #pragma unroll
-          for (int u = 0; u < U; ++u) {
-            const uint32_t i = b0 + u * SIM_NT + tid;
-            if (i < nW) x[u] = c.W.q[i];
-          }
+            for (int u = 0; u < U; ++u) {
+              const uint32_t i = b0 + u * SIM_NT + tid;
+              if (i < nW) x[u] = c.W.q[i];
+            }
 #pragma unroll
-          for (int u = 0; u < U; ++u) {
-            const uint32_t i = b0 + u * SIM_NT + tid;
-            if (i < nW) {
-              const uint64_t Ki = order_key(x[u].e, key_of(x[u].V, t, x[u].last, x[u].e));
-              if (Ki < c2) {
-                if (Ki < c1) { c2 = c1; cp2 = cp1; c1 = Ki; cp1 = i; }
-                else { c2 = Ki; cp2 = i; }
+            for (int u = 0; u < U; ++u) {
+              const uint32_t i = b0 + u * SIM_NT + tid;
+              if (i < nW) {
+                const uint64_t Ki = order_key(x[u].e, keyf(x[u]));
+                if (Ki < c2) {
+                  if (Ki < c1) { c2 = c1; cp2 = cp1; c1 = Ki; cp1 = i; }
+                  else { c2 = Ki; cp2 = i; }
+                }
               }
             }
           }
-        }
+        };
+#if AUGSCHED_SIM_RKSPEC
+        if (c.ip.ranking == AUGSCHED_RANK_AUGSERVE) {
+          // the value ranking (R3) with its constants in registers: the same
+          // operations as sched_key
+          const double al = c.k.alpha, Ts = c.k.Ts;
+          wscan([&](const QEnt& x) {
+            const double s_ = dsub(x.V, dmul(al, dmul(u2d(t - x.last), Ts)));
+            const uint32_t u_ = __float_as_uint(__double2float_rn(s_));
+            return (u_ & 0x80000000u) ? ~u_ : (u_ | 0x80000000u);
+          });
+        } else
+#endif
+          wscan([&](const QEnt& x) { return key_of(x.V, t, x.last, x.e); });
         const uint32_t cw1 = c1 != ~0ull ? c.W.dem[cp1] : 0u;
         const uint32_t cw2 = c2 != ~0ull ? c.W.dem[cp2] : 0u;
         // pop the smallest remaining W keys in order, one per round (one
