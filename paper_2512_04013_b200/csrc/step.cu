@@ -1761,7 +1761,7 @@ __global__ void __launch_bounds__(NT, (NT == 256 && E == 8) ? AUGSCHED_FM_MINB :
       stv[e] = 0u; lst[e] = 0u; V[e] = 0.0; dm[e] = 0u;
       if (x < MA) {
         stv[e] = S.st[base + x]; V[e] = S.V[base + x]; lst[e] = S.last[base + x];
-        if (inc_try) dm[e] = __ldcg(&S.dmark[base + x]);
+        if (inc && S.dmark) dm[e] = __ldcg(&S.dmark[base + x]);   // kernel arguments only: no wait for ip
       }
     }
     if (tid == 0) {   // the limit's ledger loads overlap the slot loads
@@ -1821,7 +1821,8 @@ __global__ void __launch_bounds__(NT, (NT == 256 && E == 8) ? AUGSCHED_FM_MINB :
 #pragma unroll
     for (int e = 0; e < E; ++e) {
       const uint32_t j = (uint32_t)tid * E + e;
-      const uint32_t x = j < m ? __ldcg(&mord[base + j]) : INVALID_SLOT;
+      uint32_t x = j < MA ? __ldcg(&mord[base + j]) : INVALID_SLOT;   // not waiting for m
+      if (j >= m) x = INVALID_SLOT;
       pw[e] = 0;
       if (x < MA && !chg(x)) {
         const unsigned long long w = buf0[x];
