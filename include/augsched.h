@@ -263,7 +263,13 @@ AUGSCHED_API int augsched_enqueue(augsched_t* h, uint32_t instance, const augsch
 /* One scheduling step at iteration now_iter for every instance (steps 1-7
  * above, then last = now for granted requests and the granted batch's token
  * accounting: swap-in, recompute, prefill/assimilate, decode).  Fills `out`
- * with device pointers.  Asynchronous. */
+ * with device pointers.  Asynchronous.  The order is the unique sorted order
+ * of (tier, key, slot) (R2); when the previous call on the
+ * handle was also augsched_step, the handle starts from its own copy of that
+ * order and merges the slots changed since (records, grants, evictions) into
+ * it -- for time-invariant keys always, for R3 / FCFS keys after checking
+ * that the unchanged ones are still in order -- and sorts otherwise; the
+ * outputs are the same either way. */
 AUGSCHED_API int augsched_step(augsched_t* h, uint64_t now_iter, augsched_step_out* out);
 
 /* The same decision round as augsched_step (identical grants, limits, queue
