@@ -115,3 +115,31 @@ def test_bench_workload_many_steps():
         assert np.array_equal(s.slots(i), st.slots(i)), f"slots inst {i}"
     s.close()
     st.close()
+
+
+@pytest.mark.parametrize("MA", [200, 1000, 4000, 8000])
+def test_incremental_every_block_shape(MA):
+    """Every template shape of the batched kernel (256 threads x 1, 4, 16
+    words per thread; 512 x 16) over 12 steps with a burst of new requests
+    and tight memory; FCFS, value and time-invariant rankings."""
+    rng = np.random.default_rng(MA)
+    n_inst = 3
+    cfg = dict(tracegen.PRESET_G0, g_total=1000 + 4 * MA, g_model=1000)
+    ip = tracegen.inst_params(n_inst, base=tracegen.INST_G0, ranking=[0, 1, 3], budget_mode=0,
+                              target_max=[80, 160, 400], alpha=[2.0, 0.0, 0.5])
+    st = oracle.Step(cfg, ip, MA)
+    s = aug.Scheduler(cfg, ip, n_inst, MA)
+    for t in range(12):
+        p_new = 0.6 if t in (0, 7) else 0.05
+        for i in range(n_inst):
+            rec = random_events(rng, st.slots(i), t, p_new=p_new)
+            if rec is not None:
+                assert st.enqueue(i, rec) == 0
+                s.enqueue(i, rec)
+        o = st.step(t)
+        assert o["rc"] == 0
+        g = s.step_result(s.step(t))
+        compare(g, o, n_inst, f"MA {MA} step {t}")
+    compare_slots(s, st, n_inst, f"MA {MA}")
+    s.close()
+    st.close()
