@@ -172,6 +172,7 @@ __device__ void rank_select(CandShmT<C>& c, int list, SelRes& r, int m, uint64_t
   for (int a = tid; a < m; a += NT) {
     const unsigned long long key = ck[a];
     int rk = 0;
+#pragma unroll 4
     for (int j = 0; j < m; ++j) rk += ck[j] < key;
     c.rk[rk] = key;
     c.rw[rk] = cw[a];
