@@ -1913,6 +1913,11 @@ __global__ void __launch_bounds__(NT, (NT == 256 && E == 8) ? AUGSCHED_FM_MINB :
         buf0[j + lower_rank(buf1, Kt, w)] = w;
       }
       for (uint32_t j = nq + tid; j < MP; j += NT) buf0[j] = ~0ull;
+#ifdef AUGSCHED_DEBUG
+      __syncthreads();   // the merged order must be the strictly increasing one the sort gives
+      for (uint32_t j = tid; j + 1 < nq; j += NT)
+        if (buf0[j] >= buf0[j + 1]) atomicOr(S.err, 8u);
+#endif
       inc_ok = true;
 #ifdef AUGSCHED_FM_TIMING
       if (tid == 0) { atomicAdd(&g_fm_t[9], 1ull); atomicAdd(&g_fm_t[10], (unsigned long long)Dt); }
@@ -2565,6 +2570,14 @@ __device__ bool ti_incremental(const CoopArgs& a, unsigned long long* sbuf, unsi
   TT(5);
   coop_barrier(a, nbar);
   TT(6);
+#ifdef AUGSCHED_DEBUG
+  {   // the merged order is strictly increasing (checked over each CTA's share)
+    const uint32_t nt = nu + nd, per = (nt + G - 1) / G;
+    const uint32_t q0 = c * per, q1 = q0 + per < nt ? q0 + per : nt;
+    for (uint32_t i = q0 + tid; i < q1; i += CNT)
+      if (i + 1 < nt && __ldcg(&a.tiw_out[i]) >= __ldcg(&a.tiw_out[i + 1])) atomicOr(S.err, 8u);
+  }
+#endif
 #ifdef AUGSCHED_COOP_TIMING
   if (c == TT_CTA && c != 0 && tid == 0)
     printf("ti_t cta %u ns: nd %u | %llu %llu %llu %llu %llu %llu\n", c, nd, tt[1] - tt[0], tt[2] - tt[0],

@@ -49,4 +49,23 @@ for n_inst, MA, prefix in ((1, 300, False), (1, 300, True), (4, 128, False), (4,
         compare_slots(s, st, n_inst, "debug")
     s.sync()      # raises E_STATE if an invariant check fired
     s.close()
+# kept orders (session 4): batched with every ranking, and a single queue
+# whose waiting requests are re-ordered by fp32 rounding (the checked merge
+# falls back to the sort) -- the debug build also checks each merged order
+for n_inst, MA, rk in ((3, 400, [0, 1, 3]), (1, 400, [0])):
+    cfg = dict(tracegen.PRESET_G0, g_total=1000 + 10**6, g_model=1000)
+    ipx = tracegen.inst_params(n_inst, base=tracegen.INST_G0, ranking=rk, budget_mode=1, l_static=30,
+                               alpha=1e-5)
+    st = oracle.Step(cfg, ipx, MA)
+    s = aug.Scheduler(cfg, ipx, n_inst, MA)
+    for t in range(120):
+        for i in range(n_inst):
+            rec = oracle.records(1, kind=oracle.K_NEW, id=[MA - 1 - t], la=[100], lb=[10], ta=[0.0], flags=[0])
+            st.enqueue(i, rec)
+            s.enqueue(i, rec)
+        o = st.step(t)
+        gq = s.step_result(s.step(t))
+        compare(gq, o, n_inst, f"debug kept order n_inst={n_inst} t={t}")
+    s.sync()
+    s.close()
 print("debug parity ok")
